@@ -788,3 +788,111 @@ void or_step_world(double* head, size_t n, const uint32_t* offsets, double* vert
             }
     }
 }
+
+/* ========================================================================= */
+/* flat wrappers for the Python test harness (seed in, arrays out)           */
+/* ========================================================================= */
+
+int or_init_swarm_seed(const double* hypers, const double* lo, const double* hi, size_t G,
+                       size_t N, size_t D, uint64_t seed, int rng_kind, const double* prev,
+                       size_t warm, double pi_radius, double* x, double* v) {
+    or_rng rng;
+    or_rng_init(&rng, rng_kind, seed);
+    or_swarm* s = or_swarm_new(G, N, D);
+    int st;
+    if (prev) {
+        or_planner_cfg cfg = {30.0, 4.0, 0.0, 10.0, 20, pi_radius, 1, G, N, D, 1, 0};
+        /* priori_init takes warm = floor(gamma * N); choose gamma to give `warm` */
+        cfg.gamma = (double)warm / (double)N;
+        while ((size_t)(cfg.gamma * (double)N) < warm) cfg.gamma = nextafter(cfg.gamma, 2.0);
+        st = or_priori_init(prev, hypers, lo, hi, &cfg, &rng, s);
+    } else {
+        st = or_init_swarm(hypers, lo, hi, G, N, D, &rng, s);
+    }
+    if (st == 0) {
+        memcpy(x, s->x, G * N * D * sizeof(double));
+        memcpy(v, s->v, G * N * D * sizeof(double));
+    }
+    or_swarm_free(s);
+    return st;
+}
+
+int or_step_seed(const double* hypers, const double* lo, const double* hi, size_t G, size_t N,
+                 size_t D, double* x, double* v, const double* pbx, const double* gbx,
+                 const double* tbx, uint64_t seed, int rng_kind, uint64_t skip, size_t k,
+                 size_t T) {
+    or_rng rng;
+    or_rng_init(&rng, rng_kind, seed);
+    for (uint64_t i = 0; i < skip; ++i) or_rng_next(&rng);
+    or_swarm* s = or_swarm_new(G, N, D);
+    memcpy(s->x, x, G * N * D * sizeof(double));
+    memcpy(s->v, v, G * N * D * sizeof(double));
+    memcpy(s->pbest_x, pbx, G * N * D * sizeof(double));
+    memcpy(s->gbest_x, gbx, G * D * sizeof(double));
+    memcpy(s->tbest_x, tbx, D * sizeof(double));
+    const int st = or_step(s, hypers, lo, hi, &rng, k, T);
+    memcpy(x, s->x, G * N * D * sizeof(double));
+    memcpy(v, s->v, G * N * D * sizeof(double));
+    or_swarm_free(s);
+    return st;
+}
+
+void or_update_bests_arrays(size_t G, size_t N, size_t D, const double* x, double* pbx,
+                            double* pbf, double* gbx, double* gbf, double* tbx, double* tbf,
+                            const double* fitness) {
+    or_swarm s;
+    s.G = G; s.N = N; s.D = D;
+    s.x = (double*)x; s.v = NULL; s.pbest_x = pbx; s.pbest_f = pbf; s.gbest_x = gbx;
+    s.gbest_f = gbf; s.tbest_x = tbx; s.tbest_f = *tbf; s.iteration = 0;
+    or_update_bests(&s, fitness);
+    *tbf = s.tbest_f;
+}
+
+int or_run_dtpso_flat(int kind, const or_world* w, size_t D, const double* lo, const double* hi,
+                      double alpha, double beta, const double* hypers, size_t G, size_t N,
+                      size_t T, uint64_t seed, int rng_kind, double* trace, double* final_point,
+                      double* final_fitness, size_t bad[3]) {
+    double* plo = NULL;
+    double* phi = NULL;
+    if (kind == OR_PROB_PATH) {
+        plo = (double*)malloc(D * sizeof(double));
+        phi = (double*)malloc(D * sizeof(double));
+        for (size_t d = 0; d < D; ++d) { plo[d] = 0.0; phi[d] = d < D / 2 ? w->width : w->height; }
+        lo = plo;
+        hi = phi;
+    }
+    const or_problem p = {kind, D, lo, hi, w, alpha, beta};
+    const int st = or_run_dtpso(&p, hypers, G, N, T, seed, rng_kind, trace, final_point,
+                                final_fitness, bad);
+    free(plo);
+    free(phi);
+    return st;
+}
+
+double or_lfv_flat(const double* cand, size_t groups, int kind, const or_world* w, size_t D,
+                   const double* lo, const double* hi, double alpha, double beta, size_t iG,
+                   size_t iN, size_t iT, uint64_t seed, int rng_kind) {
+    double lob[64], hib[64];
+    if (kind == OR_PROB_PATH) {
+        for (size_t d = 0; d < D && d < 64; ++d) { lob[d] = 0.0; hib[d] = d < D / 2 ? w->width : w->height; }
+        lo = lob;
+        hi = hib;
+    }
+    const or_problem p = {kind, D, lo, hi, w, alpha, beta};
+    return or_lfv_fitness(cand, groups, &p, iG, iN, iT, seed, rng_kind);
+}
+
+int or_evolve_flat(int kind, const or_world* w, size_t D, const double* lo, const double* hi,
+                   double alpha, double beta, size_t iG, size_t iN, size_t iT, size_t oG,
+                   size_t oN, size_t E, uint64_t seed, const double* outer_hypers, int rng_kind,
+                   double* best_trace, double* round_trace, double* best_hypers) {
+    double lob[64], hib[64];
+    if (kind == OR_PROB_PATH) {
+        for (size_t d = 0; d < D && d < 64; ++d) { lob[d] = 0.0; hib[d] = d < D / 2 ? w->width : w->height; }
+        lo = lob;
+        hi = hib;
+    }
+    const or_problem p = {kind, D, lo, hi, w, alpha, beta};
+    return or_evolve(&p, iG, iN, iT, oG, oN, E, seed, outer_hypers, rng_kind, best_trace,
+                     round_trace, best_hypers);
+}

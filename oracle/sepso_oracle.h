@@ -160,6 +160,30 @@ int or_generate_world(const or_scenario_cfg* c, uint64_t seed, int rng_kind,
 void or_step_world(double* head, size_t n_obstacles, const uint32_t* offsets, double* verts,
                    double* vel, double dt);
 
+
+/* ---- flat wrappers for the Python harness ------------------------------- */
+int or_init_swarm_seed(const double* hypers, const double* lo, const double* hi, size_t G,
+                       size_t N, size_t D, uint64_t seed, int rng_kind, const double* prev,
+                       size_t warm, double pi_radius, double* x, double* v);
+int or_step_seed(const double* hypers, const double* lo, const double* hi, size_t G, size_t N,
+                 size_t D, double* x, double* v, const double* pbx, const double* gbx,
+                 const double* tbx, uint64_t seed, int rng_kind, uint64_t skip, size_t k,
+                 size_t T);
+void or_update_bests_arrays(size_t G, size_t N, size_t D, const double* x, double* pbx,
+                            double* pbf, double* gbx, double* gbf, double* tbx, double* tbf,
+                            const double* fitness);
+int or_run_dtpso_flat(int kind, const or_world* w, size_t D, const double* lo, const double* hi,
+                      double alpha, double beta, const double* hypers, size_t G, size_t N,
+                      size_t T, uint64_t seed, int rng_kind, double* trace, double* final_point,
+                      double* final_fitness, size_t bad[3]);
+double or_lfv_flat(const double* cand, size_t groups, int kind, const or_world* w, size_t D,
+                   const double* lo, const double* hi, double alpha, double beta, size_t iG,
+                   size_t iN, size_t iT, uint64_t seed, int rng_kind);
+int or_evolve_flat(int kind, const or_world* w, size_t D, const double* lo, const double* hi,
+                   double alpha, double beta, size_t iG, size_t iN, size_t iT, size_t oG,
+                   size_t oN, size_t E, uint64_t seed, const double* outer_hypers, int rng_kind,
+                   double* best_trace, double* round_trace, double* best_hypers);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,1006 @@
+// capi.cpp -- the extern "C" boundary of libsepso_cuda.so (include/sepso.h).
+//
+// Each entry point validates exactly what the reference validates (reporting
+// SF_INVALID_ARGUMENT where the reference throws std::invalid_argument),
+// stages its inputs in ONE pinned host block copied with one H2D transfer,
+// launches the fused swarm kernel (or the staged HBM driver for swarms that do
+// not fit a cluster), and copies results back with one D2H transfer.
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "host_runtime.hpp"
+#include "stage_kernels.cuh"
+
+using namespace sepso;
+
+namespace sepso {
+const char* last_error_cstr();
+}
+
+namespace {
+
+double now_seconds() {
+    using clock = std::chrono::steady_clock;
+    return std::chrono::duration<double>(clock::now().time_since_epoch()).count();
+}
+
+struct DeviceGuard {
+    explicit DeviceGuard(int dev) { cudaSetDevice(dev); }
+};
+
+size_t al(size_t v) { return (v + 15) & ~size_t(15); }
+
+struct Io {
+    size_t world, hyp, seed, prev, has_prev, lo, hi, win, win_len, out, best, trace, end;
+};
+
+Io io_layout(uint32_t n, size_t world_stride, uint32_t G, uint32_t D, uint32_t cap, uint32_t tw,
+             bool per_swarm_hypers) {
+    Io o{};
+    size_t at = 0;
+    auto take = [&](size_t b) { const size_t r = at; at = al(at + b); return r; };
+    o.world = take(size_t(n) * world_stride);
+    o.hyp = take(size_t(per_swarm_hypers ? n : 1) * G * 6 * 8);
+    o.seed = take(size_t(n) * 8);
+    o.prev = take(size_t(n) * D * 8);
+    o.has_prev = take(size_t(n));
+    o.lo = take(size_t(D) * 8);
+    o.hi = take(size_t(D) * 8);
+    o.win = take(size_t(n) * std::max<uint32_t>(tw, 1) * 8);
+    o.win_len = take(size_t(n) * 4);
+    o.out = take(size_t(n) * sizeof(SwarmOut));
+    o.best = take(size_t(n) * D * 8);
+    o.trace = take(size_t(n) * cap * 8);
+    o.end = at;
+    return o;
+}
+
+int ensure_io(sf_ctx* ctx, size_t bytes) {
+    cudaError_t e = ctx->io.ensure(bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "device io block");
+    e = ctx->hio.ensure(bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "pinned io block");
+    return SF_OK;
+}
+
+// Apply the reference's window bookkeeping (push_back, then erase one from the
+// front when longer than tw; planner.hpp:179-180) for each pushed value.
+int carry_window(double* window, uint32_t* window_len, uint32_t window_cap, uint32_t tw,
+                 const double* pushes, uint32_t n_push) {
+    std::vector<double> w(window, window + *window_len);
+    for (uint32_t i = 0; i < n_push; ++i) {
+        w.push_back(pushes[i]);
+        if (w.size() > tw) w.erase(w.begin());
+    }
+    if (w.size() > window_cap) return fail(SF_INVALID_ARGUMENT, "window capacity too small");
+    std::copy(w.begin(), w.end(), window);
+    *window_len = uint32_t(w.size());
+    return SF_OK;
+}
+
+std::string nonfinite_msg(uint64_t g, uint64_t n, uint64_t k) {   // runner.hpp:22-25
+    return "non-finite fitness for particle (" + std::to_string(g) + "," + std::to_string(n) +
+           ") at iteration " + std::to_string(k);
+}
+
+int beta_integer(double beta) {
+    return (beta == double(int(beta)) && beta >= 1.0 && beta <= 64.0) ? int(beta) : 0;
+}
+
+// Problem checks shared by run_dtpso / lfv (geometry.hpp:247-256, benchmarks.hpp:22)
+int validate_problem(const sf_problem* pr) {
+    if (!pr) return fail(SF_INVALID_ARGUMENT, "problem is null");
+    if (pr->kind == SF_PROBLEM_PATH) {
+        if (pr->dim == 0 || pr->dim % 2 != 0)
+            return fail(SF_INVALID_ARGUMENT, "path problem dimension must be even and positive");
+        if (!(pr->alpha >= 0.0) || !(pr->beta >= 1.0))
+            return fail(SF_INVALID_ARGUMENT, "path_fitness: need alpha >= 0 and beta >= 1");
+        return validate_world(pr->world);
+    }
+    if (pr->kind < SF_PROBLEM_SPHERE || pr->kind > SF_PROBLEM_ACKLEY)
+        return fail(SF_INVALID_ARGUMENT, "unknown problem kind");
+    if (!pr->lo || !pr->hi) return fail(SF_INVALID_ARGUMENT, "benchmark bounds are null");
+    return validate_bounds(pr->lo, pr->hi, pr->dim);
+}
+
+// Core batched runner: n swarms of one shape; fills SwarmOut / best / trace /
+// window per swarm.  hypers: per swarm (n*G*6) when per_swarm, else G*6.
+struct BatchIn {
+    int problem = kPath;
+    uint32_t n = 0, G = 0, N = 0, D = 0, cap = 0, tw = 0;
+    const sf_world* worlds = nullptr;          // n worlds (path)
+    const double* lo = nullptr;                // benchmark box
+    const double* hi = nullptr;
+    double alpha = 30.0, beta = 4.0, delta = 10.0, pi_radius = 20.0;
+    int warm = 0, auto_truncate = 0, carry = 0;
+    const double* hypers = nullptr;
+    bool per_swarm_hypers = false;
+    const uint64_t* seeds = nullptr;
+    const double* prev = nullptr;              // n*D
+    const uint8_t* has_prev = nullptr;         // n
+    const double* win_vals = nullptr;          // n*tw (oldest first), carry only
+    const uint32_t* win_lens = nullptr;        // n
+};
+struct BatchOut {
+    std::vector<SwarmOut> out;
+    std::vector<double> best, trace;
+};
+
+int run_batch(sf_ctx* ctx, const BatchIn& b, BatchOut& r) {
+    DeviceGuard guard(ctx->device);
+    const bool path = b.problem == kPath;
+    WorldPack wp;
+    if (path) pack_worlds(b.worlds, b.n, wp);
+    const int max_obs = path ? wp.lay.max_obs : 0, max_verts = path ? wp.lay.max_verts : 0;
+    FusedPlan fp = plan_fused(ctx, b.problem, int(b.n), int(b.G), int(b.N), int(b.D), max_obs,
+                              max_verts, int(b.cap), int(b.tw));
+    r.out.assign(b.n, SwarmOut{});
+    r.best.assign(size_t(b.n) * b.D, 0.0);
+    r.trace.assign(size_t(b.n) * b.cap, 0.0);
+    if (!fp.fits || force_staged()) {
+        // staged HBM driver, one swarm at a time
+        for (uint32_t s = 0; s < b.n; ++s) {
+            StagedRun sr;
+            sr.problem = b.problem;
+            sr.G = int(b.G); sr.N = int(b.N); sr.D = int(b.D); sr.cap = int(b.cap);
+            sr.world = path ? &b.worlds[s] : nullptr;
+            sr.lo = b.lo; sr.hi = b.hi;
+            sr.alpha = b.alpha; sr.beta = b.beta;
+            sr.hypers = b.hypers + (b.per_swarm_hypers ? size_t(s) * b.G * 6 : 0);
+            sr.seed = b.seeds[s];
+            const bool hp = b.prev && b.has_prev && b.has_prev[s];
+            sr.prev = hp ? b.prev + size_t(s) * b.D : nullptr;
+            sr.warm = hp ? b.warm : 0;
+            sr.pi_radius = b.pi_radius;
+            sr.auto_truncate = b.auto_truncate;
+            sr.tw = int(b.tw);
+            sr.delta = b.delta;
+            if (b.carry && b.win_vals) {
+                sr.win_in = b.win_vals + size_t(s) * b.tw;
+                sr.win_len_in = int(std::min(b.win_lens[s], b.tw));
+            }
+            const int st = run_staged(ctx, sr);
+            if (st != SF_OK) return st;
+            r.out[s] = sr.out;
+            std::copy(sr.best.begin(), sr.best.end(), r.best.begin() + size_t(s) * b.D);
+            std::copy(sr.trace.begin(), sr.trace.end(), r.trace.begin() + size_t(s) * b.cap);
+        }
+        return SF_OK;
+    }
+    SwarmParams& p = fp.p;
+    const Io io = io_layout(b.n, path ? wp.lay.stride : 0, b.G, b.D, b.cap, b.tw, b.per_swarm_hypers);
+    int st = ensure_io(ctx, io.end);
+    if (st != SF_OK) return st;
+    unsigned char* h = static_cast<unsigned char*>(ctx->hio.p);
+    unsigned char* d = static_cast<unsigned char*>(ctx->io.p);
+    if (path) std::memcpy(h + io.world, wp.bytes.data(), wp.bytes.size());
+    std::memcpy(h + io.hyp, b.hypers, size_t(b.per_swarm_hypers ? b.n : 1) * b.G * 6 * 8);
+    std::memcpy(h + io.seed, b.seeds, size_t(b.n) * 8);
+    bool any_prev = false;
+    for (uint32_t s = 0; s < b.n; ++s) {
+        const bool hp = b.prev && b.has_prev && b.has_prev[s];
+        h[io.has_prev + s] = hp ? 1 : 0;
+        any_prev |= hp;
+        if (hp) std::memcpy(h + io.prev + size_t(s) * b.D * 8, b.prev + size_t(s) * b.D, size_t(b.D) * 8);
+    }
+    if (!path) {
+        std::memcpy(h + io.lo, b.lo, size_t(b.D) * 8);
+        std::memcpy(h + io.hi, b.hi, size_t(b.D) * 8);
+    }
+    if (b.carry) {
+        const uint32_t tw = b.tw;
+        for (uint32_t s = 0; s < b.n; ++s) {
+            const uint32_t len = b.win_lens ? b.win_lens[s] : 0;
+            const uint32_t keep = std::min(len, tw);
+            double* dst = reinterpret_cast<double*>(h + io.win) + size_t(s) * tw;
+            const double* src = b.win_vals + size_t(s) * tw;
+            // caller gives the LAST min(len, tw) values, oldest first
+            std::copy(src, src + keep, dst);
+            reinterpret_cast<int*>(h + io.win_len)[s] = int(keep);
+        }
+    }
+    p.alpha = b.alpha;
+    p.beta = b.beta;
+    p.beta_int = beta_integer(b.beta);
+    p.delta = b.delta;
+    p.pi_radius = b.pi_radius;
+    p.warm = b.warm;
+    p.auto_truncate = b.auto_truncate;
+    p.carry = b.carry;
+    p.hypers = reinterpret_cast<const double*>(d + io.hyp);
+    p.hypers_stride = b.per_swarm_hypers ? (long long)b.G * 6 : 0;
+    p.seeds = reinterpret_cast<const unsigned long long*>(d + io.seed);
+    p.worlds = d + io.world;
+    p.world_stride = path ? (long long)wp.lay.stride : 0;
+    p.off_offsets = path ? int(wp.lay.off_offsets) : 0;
+    p.off_verts = path ? int(wp.lay.off_verts) : 0;
+    p.prev = reinterpret_cast<const double*>(d + io.prev);
+    p.has_prev = any_prev ? reinterpret_cast<const unsigned char*>(d + io.has_prev) : nullptr;
+    p.lo = reinterpret_cast<const double*>(d + io.lo);
+    p.hi = reinterpret_cast<const double*>(d + io.hi);
+    p.win_vals = reinterpret_cast<double*>(d + io.win);
+    p.win_len = reinterpret_cast<int*>(d + io.win_len);
+    p.out = reinterpret_cast<SwarmOut*>(d + io.out);
+    p.best_x = reinterpret_cast<double*>(d + io.best);
+    p.trace = reinterpret_cast<double*>(d + io.trace);
+    cudaError_t ce = cudaMemcpyAsync(d, h, io.out, cudaMemcpyHostToDevice, ctx->stream);
+    if (ce != cudaSuccess) return cuda_fail(ce, "H2D io");
+    st = launch_fused(ctx, fp, b.problem);
+    if (st != SF_OK) return st;
+    ce = cudaMemcpyAsync(h + io.out, d + io.out, io.end - io.out, cudaMemcpyDeviceToHost, ctx->stream);
+    if (ce != cudaSuccess) return cuda_fail(ce, "D2H io");
+    ce = cudaStreamSynchronize(ctx->stream);
+    if (ce != cudaSuccess) return cuda_fail(ce, "swarm kernel");
+    std::memcpy(r.out.data(), h + io.out, size_t(b.n) * sizeof(SwarmOut));
+    std::memcpy(r.best.data(), h + io.best, size_t(b.n) * b.D * 8);
+    std::memcpy(r.trace.data(), h + io.trace, size_t(b.n) * b.cap * 8);
+    return SF_OK;
+}
+
+void fill_record(const SwarmOut& o, double wall, sf_plan_record* rec) {
+    rec->fitness = o.fitness;
+    rec->length = o.length;
+    rec->intersections = o.q;
+    rec->iterations = o.iterations;
+    rec->truncated = int32_t(o.truncated);
+    rec->collision_free = o.q == 0;
+    rec->wall_seconds = wall;
+}
+
+} // namespace
+
+extern "C" {
+
+int sf_abi_version(void) { return SEPSO_ABI_VERSION; }
+const char* sf_last_error(void) { return last_error_cstr(); }
+
+int sf_ctx_create(int device, int precision, sf_ctx** out) {
+    if (!out) return fail(SF_INVALID_ARGUMENT, "out is null");
+    if (precision != SF_FP32 && precision != SF_FP64)
+        return fail(SF_INVALID_ARGUMENT, "precision must be SF_FP32 or SF_FP64");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) return fail(SF_CUDA_ERROR, "no CUDA device available");
+    if (device < 0 || device >= n) return fail(SF_INVALID_ARGUMENT, "device index out of range");
+    e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    sf_ctx* c = new sf_ctx();
+    c->device = device;
+    c->precision = precision;
+    e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
+    if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_fail(e, "context setup");
+    }
+    *out = c;
+    return SF_OK;
+}
+
+int sf_ctx_destroy(sf_ctx* ctx) {
+    if (!ctx) return SF_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->io.release();
+    ctx->scratch.release();
+    ctx->hio.release();
+    cudaEventDestroy(ctx->ev0);
+    cudaEventDestroy(ctx->ev1);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return SF_OK;
+}
+
+int sf_ctx_precision(const sf_ctx* ctx) { return ctx ? ctx->precision : -1; }
+void* sf_ctx_stream(sf_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int sf_ctx_synchronize(sf_ctx* ctx) {
+    cudaSetDevice(ctx->device);
+    const cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    return e == cudaSuccess ? SF_OK : cuda_fail(e, "synchronize");
+}
+
+int sf_ctx_set_launch(sf_ctx* ctx, int cluster, int threads) {
+    if (!ctx) return fail(SF_INVALID_ARGUMENT, "ctx is null");
+    if (cluster < 0 || cluster > 16) return fail(SF_INVALID_ARGUMENT, "cluster must be 0..16");
+    if (threads < 0 || threads > 512) return fail(SF_INVALID_ARGUMENT, "threads must be 0..512");
+    ctx->force_cluster = cluster;
+    ctx->force_threads = threads;
+    return SF_OK;
+}
+
+int sf_ctx_enable_timing(sf_ctx* ctx, int enable) {
+    if (!ctx) return fail(SF_INVALID_ARGUMENT, "ctx is null");
+    ctx->timing = enable != 0;
+    ctx->kernel_ms = 0.0;
+    ctx->launches = 0;
+    return SF_OK;
+}
+
+int sf_ctx_kernel_time(sf_ctx* ctx, double* total_ms, uint64_t* launches) {
+    if (!ctx) return fail(SF_INVALID_ARGUMENT, "ctx is null");
+    if (total_ms) *total_ms = ctx->kernel_ms;
+    if (launches) *launches = ctx->launches;
+    return SF_OK;
+}
+
+// planner.hpp:156-199
+int sf_plan_frame(sf_ctx* ctx, const sf_world* world, const double* prev, const double* hypers,
+                  const sf_planner_config* cfg, uint64_t seed, double* window, uint32_t* window_len,
+                  uint32_t window_cap, sf_plan_record* record, double* best, uint64_t* bad) {
+    const double t0 = now_seconds();
+    if (!ctx || !record) return fail(SF_INVALID_ARGUMENT, "ctx/record is null");
+    int st = validate_planner(cfg);
+    if (st) return st;
+    if ((st = validate_world(world))) return st;
+    if (!hypers) return fail(SF_INVALID_ARGUMENT, "hypers is null");
+    if ((st = validate_hypers(hypers, cfg->groups))) return st;
+    const bool carry = cfg->window_carryover && window && window_len;
+    BatchIn b;
+    b.problem = kPath;
+    b.n = 1;
+    b.G = cfg->groups; b.N = cfg->per_group; b.D = cfg->dim;
+    b.cap = cfg->max_iters_per_frame;
+    b.tw = cfg->tw;
+    b.worlds = world;
+    b.alpha = cfg->alpha; b.beta = cfg->beta; b.delta = cfg->delta; b.pi_radius = cfg->pi_radius;
+    b.warm = int(cfg->gamma * double(cfg->per_group));            // planner.hpp:37-39
+    b.auto_truncate = cfg->auto_truncate;
+    b.carry = carry;
+    b.hypers = hypers;
+    b.seeds = &seed;
+    const uint8_t hp = prev ? 1 : 0;
+    b.prev = prev;
+    b.has_prev = &hp;
+    std::vector<double> wtail;
+    uint32_t wl = 0;
+    if (carry) {
+        const uint32_t keep = std::min(*window_len, cfg->tw);
+        wtail.assign(window + (*window_len - keep), window + *window_len);
+        wtail.resize(cfg->tw, 0.0);
+        wl = keep;
+        b.win_vals = wtail.data();
+        b.win_lens = &wl;
+    }
+    BatchOut r;
+    if ((st = run_batch(ctx, b, r))) return st;
+    const SwarmOut& o = r.out[0];
+    if (o.status == 2) {
+        if (bad) { bad[0] = o.bad_g; bad[1] = o.bad_n; bad[2] = o.bad_k; }
+        return fail(SF_NON_FINITE, nonfinite_msg(o.bad_g, o.bad_n, o.bad_k));
+    }
+    if (carry && (st = carry_window(window, window_len, window_cap, cfg->tw, r.trace.data(), o.iterations)))
+        return st;
+    if (best) std::copy(r.best.begin(), r.best.begin() + cfg->dim, best);
+    fill_record(o, now_seconds() - t0, record);
+    return SF_OK;
+}
+
+int sf_plan_frames_batched(sf_ctx* ctx, uint32_t n, const sf_world* worlds, const double* prev,
+                           const uint8_t* has_prev, const double* hypers,
+                           const sf_planner_config* cfg, const uint64_t* seeds, double* windows,
+                           uint32_t* window_lens, sf_plan_record* records, double* best,
+                           int32_t* statuses, uint64_t* bad) {
+    const double t0 = now_seconds();
+    if (!ctx || !records || !seeds || !worlds) return fail(SF_INVALID_ARGUMENT, "null argument");
+    if (n == 0) return SF_OK;
+    int st = validate_planner(cfg);
+    if (st) return st;
+    if (!hypers) return fail(SF_INVALID_ARGUMENT, "hypers is null");
+    if ((st = validate_hypers(hypers, cfg->groups))) return st;
+    for (uint32_t s = 0; s < n; ++s)
+        if ((st = validate_world(&worlds[s]))) return st;
+    const bool carry = cfg->window_carryover && windows && window_lens;
+    BatchIn b;
+    b.problem = kPath;
+    b.n = n;
+    b.G = cfg->groups; b.N = cfg->per_group; b.D = cfg->dim;
+    b.cap = cfg->max_iters_per_frame;
+    b.tw = cfg->tw;
+    b.worlds = worlds;
+    b.alpha = cfg->alpha; b.beta = cfg->beta; b.delta = cfg->delta; b.pi_radius = cfg->pi_radius;
+    b.warm = int(cfg->gamma * double(cfg->per_group));
+    b.auto_truncate = cfg->auto_truncate;
+    b.carry = carry;
+    b.hypers = hypers;
+    b.seeds = seeds;
+    b.prev = prev;
+    b.has_prev = has_prev;
+    std::vector<double> wt;
+    std::vector<uint32_t> wl;
+    if (carry) {
+        wt.assign(size_t(n) * cfg->tw, 0.0);
+        wl.assign(n, 0);
+        for (uint32_t s = 0; s < n; ++s) {
+            const uint32_t len = std::min(window_lens[s], cfg->tw);
+            const double* src = windows + size_t(s) * cfg->tw;
+            std::copy(src, src + len, wt.begin() + size_t(s) * cfg->tw);
+            wl[s] = len;
+        }
+        b.win_vals = wt.data();
+        b.win_lens = wl.data();
+    }
+    BatchOut r;
+    if ((st = run_batch(ctx, b, r))) return st;
+    const double wall = (now_seconds() - t0) / double(n);
+    int any_bad = 0;
+    for (uint32_t s = 0; s < n; ++s) {
+        const SwarmOut& o = r.out[s];
+        if (statuses) statuses[s] = o.status == 2 ? SF_NON_FINITE : SF_OK;
+        if (o.status == 2) {
+            any_bad = 1;
+            if (bad) { bad[3 * s] = o.bad_g; bad[3 * s + 1] = o.bad_n; bad[3 * s + 2] = o.bad_k; }
+            continue;
+        }
+        fill_record(o, wall, &records[s]);
+        if (best) std::copy(r.best.begin() + size_t(s) * cfg->dim, r.best.begin() + size_t(s + 1) * cfg->dim,
+                            best + size_t(s) * cfg->dim);
+        if (carry) {
+            // windows are fixed-stride tw slots here: keep the trailing tw values
+            uint32_t len = std::min(window_lens[s], cfg->tw);
+            if ((st = carry_window(windows + size_t(s) * cfg->tw, &len, cfg->tw, cfg->tw,
+                                   r.trace.data() + size_t(s) * b.cap, o.iterations)))
+                return st;
+            window_lens[s] = len;
+        }
+    }
+    if (any_bad) set_error("one or more scenes produced a non-finite fitness");
+    return SF_OK;
+}
+
+static int run_dtpso_impl(sf_ctx* ctx, const sf_problem* pr, uint32_t n, const double* hypers,
+                          bool per_run, uint32_t G, uint32_t N, uint32_t T, const uint64_t* seeds,
+                          BatchOut& r) {
+    int st = validate_problem(pr);
+    if (st) return st;
+    if (T < 1) return fail(SF_INVALID_ARGUMENT, "run_dtpso: iteration count must be >= 1");
+    if (G < 1 || N < 1) return fail(SF_INVALID_ARGUMENT, "init_swarm: G, N, D must all be >= 1");
+    if (!hypers) return fail(SF_INVALID_ARGUMENT, "hypers is null");
+    for (uint32_t s = 0; s < (per_run ? n : 1); ++s)
+        if ((st = validate_hypers(hypers + size_t(s) * G * 6, G))) return st;
+    BatchIn b;
+    b.problem = pr->kind;
+    b.n = n;
+    b.G = G; b.N = N; b.D = pr->dim; b.cap = T; b.tw = 0;
+    std::vector<sf_world> ws;
+    if (pr->kind == SF_PROBLEM_PATH) {
+        ws.assign(n, *pr->world);
+        b.worlds = ws.data();
+    }
+    b.lo = pr->lo; b.hi = pr->hi;
+    b.alpha = pr->alpha; b.beta = pr->beta;
+    b.hypers = hypers;
+    b.per_swarm_hypers = per_run;
+    b.seeds = seeds;
+    return run_batch(ctx, b, r);
+}
+
+// runner.hpp:97-129
+int sf_run_dtpso(sf_ctx* ctx, const sf_problem* pr, const double* hypers, uint32_t G, uint32_t N,
+                 uint32_t T, uint64_t seed, double* trace, double* final_point, double* final_fitness,
+                 uint64_t* bad) {
+    if (!ctx) return fail(SF_INVALID_ARGUMENT, "ctx is null");
+    BatchOut r;
+    const int st = run_dtpso_impl(ctx, pr, 1, hypers, false, G, N, T, &seed, r);
+    if (st) return st;
+    const SwarmOut& o = r.out[0];
+    if (o.status == 2) {
+        if (bad) { bad[0] = o.bad_g; bad[1] = o.bad_n; bad[2] = o.bad_k; }
+        return fail(SF_NON_FINITE, nonfinite_msg(o.bad_g, o.bad_n, o.bad_k));
+    }
+    if (trace) std::copy(r.trace.begin(), r.trace.begin() + T, trace);
+    if (final_point) std::copy(r.best.begin(), r.best.begin() + pr->dim, final_point);
+    if (final_fitness) *final_fitness = o.fitness;
+    return SF_OK;
+}
+
+int sf_run_dtpso_batched(sf_ctx* ctx, const sf_problem* pr, uint32_t n, const double* hypers,
+                         int per_run, uint32_t G, uint32_t N, uint32_t T, const uint64_t* seeds,
+                         double* traces, double* final_points, double* final_fitness,
+                         int32_t* statuses) {
+    if (!ctx || !seeds) return fail(SF_INVALID_ARGUMENT, "null argument");
+    if (n == 0) return SF_OK;
+    BatchOut r;
+    const int st = run_dtpso_impl(ctx, pr, n, hypers, per_run != 0, G, N, T, seeds, r);
+    if (st) return st;
+    for (uint32_t s = 0; s < n; ++s) {
+        const SwarmOut& o = r.out[s];
+        if (statuses) statuses[s] = o.status == 2 ? SF_NON_FINITE : SF_OK;
+        if (traces) std::copy(r.trace.begin() + size_t(s) * T, r.trace.begin() + size_t(s + 1) * T, traces + size_t(s) * T);
+        if (final_points)
+            std::copy(r.best.begin() + size_t(s) * pr->dim, r.best.begin() + size_t(s + 1) * pr->dim,
+                      final_points + size_t(s) * pr->dim);
+        if (final_fitness) final_fitness[s] = o.status == 2 ? std::numeric_limits<double>::infinity() : o.fitness;
+    }
+    return SF_OK;
+}
+
+// hsef.hpp:108-119, m candidates per launch
+int sf_lfv_batch(sf_ctx* ctx, const sf_problem* pr, uint32_t m, const double* cand,
+                 const uint64_t* seeds, uint32_t iG, uint32_t iN, uint32_t iT, double* lfv) {
+    if (!ctx || !lfv || !seeds || !cand) return fail(SF_INVALID_ARGUMENT, "null argument");
+    const double inf = std::numeric_limits<double>::infinity();
+    for (uint32_t i = 0; i < m; ++i) lfv[i] = inf;
+    if (m == 0) return SF_OK;
+    // invalid inner budgets / problems make every candidate +inf (exceptions caught)
+    if (iT < 1 || iG < 1 || iN < 1 || validate_problem(pr) != SF_OK) return SF_OK;
+    std::vector<double> hyp(size_t(m) * iG * 6);
+    std::vector<uint64_t> sd;
+    std::vector<uint32_t> idx;
+    std::vector<double> ok_h;
+    for (uint32_t i = 0; i < m; ++i) {
+        double* h = hyp.data() + size_t(i) * iG * 6;
+        unflatten_hypers(cand + size_t(i) * iG * 6, iG, h);
+        if (validate_hypers(h, iG) != SF_OK) continue;      // NaN candidates score +inf
+        idx.push_back(i);
+        sd.push_back(seeds[i]);
+        ok_h.insert(ok_h.end(), h, h + iG * 6);
+    }
+    set_error("");
+    if (idx.empty()) return SF_OK;
+    BatchOut r;
+    const int st = run_dtpso_impl(ctx, pr, uint32_t(idx.size()), ok_h.data(), true, iG, iN, iT, sd.data(), r);
+    if (st == SF_CUDA_ERROR) return st;
+    if (st != SF_OK) return SF_OK;
+    for (size_t j = 0; j < idx.size(); ++j)
+        lfv[idx[j]] = r.out[j].status == 2 ? inf : r.out[j].fitness;
+    return SF_OK;
+}
+
+// hsef.hpp:125-171: outer PSO on the host, inner runs batched on the device
+int sf_evolve(sf_ctx* ctx, const sf_problem* pr, uint32_t iG, uint32_t iN, uint32_t iT,
+              uint32_t oG, uint32_t oN, uint32_t E, uint64_t seed, const double* outer_hypers,
+              double* best_trace, double* round_trace, double* best_hypers) {
+    if (!ctx || !outer_hypers) return fail(SF_INVALID_ARGUMENT, "null argument");
+    if (E < 1) return fail(SF_INVALID_ARGUMENT, "evolve: evolution count must be >= 1");
+    if (iT < 1) return fail(SF_INVALID_ARGUMENT, "evolve: inner iteration count must be >= 1");
+    if (iG < 1) return fail(SF_INVALID_ARGUMENT, "HyperEncoding: group count must be >= 1");
+    int st = validate_hypers(outer_hypers, oG);
+    if (st) return st;
+    if (oN < 1) return fail(SF_INVALID_ARGUMENT, "init_swarm: G, N, D must all be >= 1");
+    const uint32_t dim = 6 * iG;
+    std::vector<double> lo(dim), hi(dim);
+    static const double flo[6] = {0.5, 0.5, 0.5, 0.1, 0.05, 0.05};
+    static const double fhi[6] = {2.5, 2.5, 2.5, 1.0, 0.8, 1.0};
+    for (uint32_t g = 0; g < iG; ++g)
+        for (int f = 0; f < 6; ++f) { lo[6 * g + f] = flo[f]; hi[6 * g + f] = fhi[f]; }
+    const uint64_t outer_seed = derive_seed(seed, "outer");
+    const uint64_t lfv_root = derive_seed(seed, "lfv");
+    HostStream rng(outer_seed);
+    HostSwarm s;
+    host_init_swarm(s, outer_hypers, lo.data(), hi.data(), oG, oN, dim, rng);
+    const uint32_t cand = oG * oN;
+    std::vector<double> fit(cand);
+    std::vector<uint64_t> seeds(cand);
+    uint64_t eval_index = 0;
+    for (uint32_t e = 1; e <= E; ++e) {
+        for (uint32_t r = 0; r < cand; ++r) seeds[r] = derive_seed(lfv_root, "lfv", eval_index++);
+        st = sf_lfv_batch(ctx, pr, cand, s.x.data(), seeds.data(), iG, iN, iT, fit.data());
+        if (st) return st;
+        double round_best = std::numeric_limits<double>::infinity();
+        for (uint32_t r = 0; r < cand; ++r) round_best = std::min(round_best, fit[r]);
+        host_update_bests(s, fit.data());
+        if (best_trace) best_trace[e - 1] = s.tbf;
+        if (round_trace) round_trace[e - 1] = round_best;
+        host_step(s, outer_hypers, lo.data(), hi.data(), rng, e, E);
+    }
+    if (best_hypers) unflatten_hypers(s.tbx.data(), iG, best_hypers);
+    return SF_OK;
+}
+
+// ------------------------------------------------------------- stage entries
+static size_t tsize(sf_ctx* ctx) { return ctx->precision == SF_FP64 ? 8 : 4; }
+
+static void to_dev_type(sf_ctx* ctx, const double* src, size_t n, std::vector<unsigned char>& out) {
+    out.resize(n * tsize(ctx));
+    if (ctx->precision == SF_FP64) std::memcpy(out.data(), src, n * 8);
+    else for (size_t i = 0; i < n; ++i) reinterpret_cast<float*>(out.data())[i] = float(src[i]);
+}
+static void from_dev_type(sf_ctx* ctx, const unsigned char* src, size_t n, double* out) {
+    if (ctx->precision == SF_FP64) std::memcpy(out, src, n * 8);
+    else for (size_t i = 0; i < n; ++i) out[i] = double(reinterpret_cast<const float*>(src)[i]);
+}
+
+namespace {
+// A tiny device arena for stage calls: sequential sub-allocations of ctx->scratch.
+struct Arena {
+    sf_ctx* ctx;
+    std::vector<std::pair<size_t, size_t>> parts;
+    size_t total = 0;
+    size_t add(size_t b) { const size_t at = total; total = (total + b + 255) & ~size_t(255); return at; }
+    int commit() {
+        const cudaError_t e = ctx->scratch.ensure(total);
+        return e == cudaSuccess ? SF_OK : cuda_fail(e, "scratch");
+    }
+    unsigned char* at(size_t off) { return static_cast<unsigned char*>(ctx->scratch.p) + off; }
+};
+int up(sf_ctx* ctx, void* dst, const void* src, size_t n) {
+    const cudaError_t e = cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, ctx->stream);
+    return e == cudaSuccess ? SF_OK : cuda_fail(e, "H2D");
+}
+int down(sf_ctx* ctx, void* dst, const void* src, size_t n) {
+    const cudaError_t e = cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, ctx->stream);
+    return e == cudaSuccess ? SF_OK : cuda_fail(e, "D2H");
+}
+int sync(sf_ctx* ctx) {
+    const cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    return e == cudaSuccess ? SF_OK : cuda_fail(e, "stage kernel");
+}
+}  // namespace
+
+int sf_init_swarm(sf_ctx* ctx, const double* hypers, const double* lo, const double* hi,
+                  uint32_t G, uint32_t N, uint32_t D, uint64_t seed, const double* prev,
+                  uint32_t warm, double pi_radius, double* x, double* v) {
+    if (!ctx || !x || !v) return fail(SF_INVALID_ARGUMENT, "null argument");
+    DeviceGuard guard(ctx->device);
+    int st = validate_hypers(hypers, G);
+    if (st) return st;
+    if ((st = validate_bounds(lo, hi, D))) return st;
+    if (N < 1) return fail(SF_INVALID_ARGUMENT, "init_swarm: G, N, D must all be >= 1");
+    const size_t ts = tsize(ctx), E = size_t(G) * N * D;
+    Arena a{ctx};
+    const size_t oh = a.add(size_t(G) * 48), olo = a.add(D * ts), ohi = a.add(D * ts),
+                 op = a.add(D * 8), ox = a.add(E * ts), ov = a.add(E * ts), opb = a.add(E * ts);
+    if ((st = a.commit())) return st;
+    std::vector<unsigned char> blo, bhi;
+    to_dev_type(ctx, lo, D, blo);
+    to_dev_type(ctx, hi, D, bhi);
+    up(ctx, a.at(oh), hypers, size_t(G) * 48);
+    up(ctx, a.at(olo), blo.data(), blo.size());
+    up(ctx, a.at(ohi), bhi.data(), bhi.size());
+    if (prev) up(ctx, a.at(op), prev, size_t(D) * 8);
+    const StageShape s{int(G), int(N), int(D), 0, int(G * N)};
+    const int e = stage_init(ctx->precision == SF_FP64, s, reinterpret_cast<double*>(a.at(oh)), a.at(olo),
+                             a.at(ohi), seed, prev ? reinterpret_cast<double*>(a.at(op)) : nullptr,
+                             prev ? int(warm) : 0, pi_radius, a.at(ox), a.at(ov), a.at(opb), ctx->stream);
+    if (e) return cuda_fail(cudaError_t(e), "stage_init");
+    std::vector<unsigned char> hx(E * ts), hv(E * ts);
+    down(ctx, hx.data(), a.at(ox), hx.size());
+    down(ctx, hv.data(), a.at(ov), hv.size());
+    if ((st = sync(ctx))) return st;
+    from_dev_type(ctx, hx.data(), E, x);
+    from_dev_type(ctx, hv.data(), E, v);
+    return SF_OK;
+}
+
+int sf_step(sf_ctx* ctx, const double* hypers, const double* lo, const double* hi, uint32_t G,
+            uint32_t N, uint32_t D, double* x, double* v, const double* pbx, const double* gbx,
+            const double* tbx, uint64_t seed, uint64_t first_draw, uint32_t k, uint32_t T) {
+    if (!ctx) return fail(SF_INVALID_ARGUMENT, "ctx is null");
+    DeviceGuard guard(ctx->device);
+    if (T == 0) return fail(SF_INVALID_ARGUMENT, "inertia_at: total iteration count must be >= 1");
+    if (k > T) return fail(SF_INVALID_ARGUMENT, "inertia_at: k out of range");
+    if (G < 1 || N < 1 || D < 1) return fail(SF_INVALID_ARGUMENT, "step: empty swarm");
+    const size_t ts = tsize(ctx), E = size_t(G) * N * D;
+    Arena a{ctx};
+    const size_t oh = a.add(size_t(G) * 48), olo = a.add(D * ts), ohi = a.add(D * ts),
+                 ox = a.add(E * ts), ov = a.add(E * ts), opb = a.add(E * ts),
+                 og = a.add(size_t(G) * D * ts), ot = a.add(D * ts);
+    int st = a.commit();
+    if (st) return st;
+    std::vector<unsigned char> b;
+    up(ctx, a.at(oh), hypers, size_t(G) * 48);
+    to_dev_type(ctx, lo, D, b); up(ctx, a.at(olo), b.data(), b.size()); sync(ctx);
+    to_dev_type(ctx, hi, D, b); up(ctx, a.at(ohi), b.data(), b.size()); sync(ctx);
+    to_dev_type(ctx, x, E, b); up(ctx, a.at(ox), b.data(), b.size()); sync(ctx);
+    to_dev_type(ctx, v, E, b); up(ctx, a.at(ov), b.data(), b.size()); sync(ctx);
+    to_dev_type(ctx, pbx, E, b); up(ctx, a.at(opb), b.data(), b.size()); sync(ctx);
+    to_dev_type(ctx, gbx, size_t(G) * D, b); up(ctx, a.at(og), b.data(), b.size()); sync(ctx);
+    to_dev_type(ctx, tbx, D, b); up(ctx, a.at(ot), b.data(), b.size()); sync(ctx);
+    const StageShape s{int(G), int(N), int(D), 0, int(G * N)};
+    const int e = stage_step(ctx->precision == SF_FP64, s, reinterpret_cast<double*>(a.at(oh)), a.at(olo),
+                             a.at(ohi), a.at(ox), a.at(ov), a.at(opb), a.at(og), a.at(ot), seed,
+                             first_draw, int(k), int(T), nullptr, ctx->stream);
+    if (e) return cuda_fail(cudaError_t(e), "stage_step");
+    std::vector<unsigned char> hx(E * ts), hv(E * ts);
+    down(ctx, hx.data(), a.at(ox), hx.size());
+    down(ctx, hv.data(), a.at(ov), hv.size());
+    if ((st = sync(ctx))) return st;
+    from_dev_type(ctx, hx.data(), E, x);
+    from_dev_type(ctx, hv.data(), E, v);
+    return SF_OK;
+}
+
+int sf_update_bests(sf_ctx* ctx, uint32_t G, uint32_t N, uint32_t D, const double* x, double* pbx,
+                    double* pbf, double* gbx, double* gbf, double* tbx, double* tbf,
+                    const double* fitness) {
+    if (!ctx) return fail(SF_INVALID_ARGUMENT, "ctx is null");
+    DeviceGuard guard(ctx->device);
+    if (G < 1 || N < 1 || D < 1) return fail(SF_INVALID_ARGUMENT, "update_bests: empty swarm");
+    const bool fp64 = ctx->precision == SF_FP64;
+    const size_t ts = tsize(ctx), R = size_t(G) * N, E = R * D;
+    Arena a{ctx};
+    const size_t ox = a.add(E * ts), opb = a.add(E * ts), opbf = a.add(R * ts), ofit = a.add(R * ts),
+                 oq = a.add(R * 4), opbq = a.add(R * 4), opf = a.add(G * ts), oprow = a.add(G * 4),
+                 opq = a.add(G * 4), ogb = a.add(size_t(G) * D * ts), ogbf = a.add(G * ts),
+                 ogbq = a.add(G * 4), otb = a.add(D * ts), ocand = a.add(cand_bytes(fp64, D)),
+                 ost = a.add(sizeof(IterState));
+    int st = a.commit();
+    if (st) return st;
+    std::vector<unsigned char> b;
+    to_dev_type(ctx, x, E, b); up(ctx, a.at(ox), b.data(), b.size()); sync(ctx);
+    to_dev_type(ctx, pbx, E, b); up(ctx, a.at(opb), b.data(), b.size()); sync(ctx);
+    to_dev_type(ctx, pbf, R, b); up(ctx, a.at(opbf), b.data(), b.size()); sync(ctx);
+    to_dev_type(ctx, fitness, R, b); up(ctx, a.at(ofit), b.data(), b.size()); sync(ctx);
+    to_dev_type(ctx, gbx, size_t(G) * D, b); up(ctx, a.at(ogb), b.data(), b.size()); sync(ctx);
+    to_dev_type(ctx, gbf, G, b); up(ctx, a.at(ogbf), b.data(), b.size()); sync(ctx);
+    to_dev_type(ctx, tbx, D, b); up(ctx, a.at(otb), b.data(), b.size()); sync(ctx);
+    cudaMemsetAsync(a.at(oq), 0, R * 4, ctx->stream);
+    cudaMemsetAsync(a.at(opbq), 0, R * 4, ctx->stream);
+    cudaMemsetAsync(a.at(ogbq), 0, G * 4, ctx->stream);
+    IterState is{};
+    // the stage tbest uses the FP32/FP64 value of the incoming tbest
+    is.tbest_f = fp64 ? *tbf : double(float(*tbf));
+    is.tbest_group = -1;
+    is.nonfinite_row = INT_MAX;
+    up(ctx, a.at(ost), &is, sizeof(is));
+    const StageShape s{int(G), int(N), int(D), 0, int(R)};
+    IterState* dst = reinterpret_cast<IterState*>(a.at(ost));
+    int e = stage_pbest_partials(fp64, s, a.at(ox), a.at(ofit), reinterpret_cast<int*>(a.at(oq)), a.at(opb),
+                                 a.at(opbf), reinterpret_cast<int*>(a.at(opbq)), nullptr, a.at(opf),
+                                 reinterpret_cast<int*>(a.at(oprow)), reinterpret_cast<int*>(a.at(opq)),
+                                 nullptr, ctx->stream);
+    if (!e) e = stage_group_bests(fp64, s, a.at(opf), reinterpret_cast<int*>(a.at(oprow)),
+                                  reinterpret_cast<int*>(a.at(opq)), a.at(opb), a.at(ogb), a.at(ogbf),
+                                  reinterpret_cast<int*>(a.at(ogbq)), a.at(ocand), nullptr, ctx->stream);
+    if (!e) e = stage_finish(fp64, int(D), a.at(ocand), 1, a.at(otb), dst, nullptr, 0, 0, 0.0, 1, 1,
+                             nullptr, ctx->stream);
+    if (e) return cuda_fail(cudaError_t(e), "update_bests stages");
+    std::vector<unsigned char> hpb(E * ts), hpbf(R * ts), hgb(size_t(G) * D * ts), hgbf(G * ts), htb(D * ts);
+    IterState fin{};
+    down(ctx, hpb.data(), a.at(opb), hpb.size());
+    down(ctx, hpbf.data(), a.at(opbf), hpbf.size());
+    down(ctx, hgb.data(), a.at(ogb), hgb.size());
+    down(ctx, hgbf.data(), a.at(ogbf), hgbf.size());
+    down(ctx, htb.data(), a.at(otb), htb.size());
+    down(ctx, &fin, a.at(ost), sizeof(fin));
+    if ((st = sync(ctx))) return st;
+    from_dev_type(ctx, hpb.data(), E, pbx);
+    from_dev_type(ctx, hpbf.data(), R, pbf);
+    from_dev_type(ctx, hgb.data(), size_t(G) * D, gbx);
+    from_dev_type(ctx, hgbf.data(), G, gbf);
+    from_dev_type(ctx, htb.data(), D, tbx);
+    *tbf = fin.tbest_f;
+    return SF_OK;
+}
+
+int sf_eval_path_rows(sf_ctx* ctx, const sf_world* world, const double* xs, uint32_t rows,
+                      uint32_t D, double alpha, double beta, double* fitness, uint32_t* q) {
+    if (!ctx || !xs || !fitness) return fail(SF_INVALID_ARGUMENT, "null argument");
+    DeviceGuard guard(ctx->device);
+    if (D == 0 || D % 2 != 0) return fail(SF_INVALID_ARGUMENT, "decode_path: dimension must be even and positive");
+    if (alpha < 0.0 || beta < 1.0) return fail(SF_INVALID_ARGUMENT, "path_fitness: need alpha >= 0 and beta >= 1");
+    int st = validate_world(world);
+    if (st) return st;
+    if (rows == 0) return SF_OK;
+    const bool fp64 = ctx->precision == SF_FP64;
+    const size_t ts = tsize(ctx);
+    WorldPack wp;
+    pack_worlds(world, 1, wp);
+    Arena a{ctx};
+    const size_t ow = a.add(wp.bytes.size()), ox = a.add(size_t(rows) * D * ts), of = a.add(size_t(rows) * ts),
+                 oq = a.add(size_t(rows) * 4);
+    if ((st = a.commit())) return st;
+    std::vector<unsigned char> b;
+    up(ctx, a.at(ow), wp.bytes.data(), wp.bytes.size());
+    to_dev_type(ctx, xs, size_t(rows) * D, b);
+    up(ctx, a.at(ox), b.data(), b.size());
+    if (ctx->timing) cudaEventRecord(ctx->ev0, ctx->stream);
+    const int e = stage_eval_path(fp64, a.at(ow), wp.lay.max_obs, wp.lay.max_verts, int(wp.lay.off_offsets),
+                                  int(wp.lay.off_verts), int(D), int(rows), a.at(ox), alpha, beta, a.at(of),
+                                  reinterpret_cast<int*>(a.at(oq)), nullptr, ctx->stream);
+    if (e) return cuda_fail(cudaError_t(e), "stage_eval_path");
+    if (ctx->timing) cudaEventRecord(ctx->ev1, ctx->stream);
+    std::vector<unsigned char> hf(size_t(rows) * ts);
+    down(ctx, hf.data(), a.at(of), hf.size());
+    if (q) down(ctx, q, a.at(oq), size_t(rows) * 4);
+    if ((st = sync(ctx))) return st;
+    if (ctx->timing) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+        ctx->kernel_ms += ms;
+        ctx->launches += 1;
+    }
+    from_dev_type(ctx, hf.data(), rows, fitness);
+    return SF_OK;
+}
+
+int sf_eval_bench_rows(sf_ctx* ctx, int kind, const double* xs, uint32_t rows, uint32_t D,
+                       double* fitness) {
+    if (!ctx || !xs || !fitness) return fail(SF_INVALID_ARGUMENT, "null argument");
+    DeviceGuard guard(ctx->device);
+    if (kind < SF_PROBLEM_SPHERE || kind > SF_PROBLEM_ACKLEY) return fail(SF_INVALID_ARGUMENT, "unknown benchmark kind");
+    if (rows == 0) return SF_OK;
+    const size_t ts = tsize(ctx);
+    Arena a{ctx};
+    const size_t ox = a.add(size_t(rows) * D * ts), of = a.add(size_t(rows) * ts);
+    int st = a.commit();
+    if (st) return st;
+    std::vector<unsigned char> b;
+    to_dev_type(ctx, xs, size_t(rows) * D, b);
+    up(ctx, a.at(ox), b.data(), b.size());
+    const int e = stage_eval_bench(ctx->precision == SF_FP64, kind, int(D), int(rows), a.at(ox), a.at(of), nullptr,
+                                   nullptr, ctx->stream);
+    if (e) return cuda_fail(cudaError_t(e), "stage_eval_bench");
+    std::vector<unsigned char> hf(size_t(rows) * ts);
+    down(ctx, hf.data(), a.at(of), hf.size());
+    if ((st = sync(ctx))) return st;
+    from_dev_type(ctx, hf.data(), rows, fitness);
+    return SF_OK;
+}
+
+// planner.hpp:138-149 (the device evaluates the same predicate inside the frame loop)
+int sf_should_truncate(const double* window, uint32_t len, int cf, const sf_planner_config* cfg,
+                       int* result) {
+    if (!cfg || !result) return fail(SF_INVALID_ARGUMENT, "null argument");
+    if (len < cfg->tw) { *result = 0; return SF_OK; }
+    const double* tail = window + (len - cfg->tw);
+    double mean = 0.0;
+    for (uint32_t i = 0; i < cfg->tw; ++i) mean += tail[i];
+    mean /= double(cfg->tw);
+    double var = 0.0;
+    for (uint32_t i = 0; i < cfg->tw; ++i) var += (tail[i] - mean) * (tail[i] - mean);
+    var /= double(cfg->tw);
+    *result = std::sqrt(var) < cfg->delta && cf;
+    return SF_OK;
+}
+
+// ------------------------------------------------------------- scene state
+// simenv.hpp:83-132 over the engine stream (RngStream = Philox contract)
+int sf_generate_world(const sf_scenario_config* c, uint64_t seed, sf_world* w, uint32_t* offsets,
+                      sf_point* verts, sf_point* vel) {
+    if (!c || !w || !offsets || !verts || !vel) return fail(SF_INVALID_ARGUMENT, "null argument");
+    if (!(c->map_size > 0.0)) return fail(SF_INVALID_ARGUMENT, "scenario: map size must be positive");
+    if (!(c->min_side > 0.0) || c->min_side > c->max_side || c->max_side >= c->map_size)
+        return fail(SF_INVALID_ARGUMENT, "scenario: obstacle side range invalid");
+    if (!(c->max_speed > 0.0)) return fail(SF_INVALID_ARGUMENT, "scenario: max speed must be positive");
+    if (c->frames < 1) return fail(SF_INVALID_ARGUMENT, "scenario: frame count must be >= 1");
+    if (!(c->dt > 0.0)) return fail(SF_INVALID_ARGUMENT, "scenario: dt must be positive");
+    HostStream rng(seed);
+    const double M = c->map_size;
+    w->width = M;
+    w->height = M;
+    w->start = {0.5 * M, 0.1 * M};
+    w->target = {0.5 * M, 0.9 * M};
+    w->start_velocity = {0.0, c->start_speed};
+    w->target_velocity = {0.0, c->target_speed};
+    const double clearance = 2.0;
+    const uint32_t total = c->dynamic_obstacles + c->static_obstacles;
+    for (uint32_t i = 0; i < total; ++i) {
+        bool placed = false;
+        for (int attempt = 0; attempt < 200 && !placed; ++attempt) {
+            const double ow = rng.uniform(c->min_side, c->max_side);
+            const double oh = rng.uniform(c->min_side, c->max_side);
+            const double cx = rng.uniform(ow / 2.0, M - ow / 2.0);
+            const double cy = rng.uniform(oh / 2.0, M - oh / 2.0);
+            auto covers = [&](const sf_point& p) {
+                return p.x >= cx - ow / 2.0 - clearance && p.x <= cx + ow / 2.0 + clearance &&
+                       p.y >= cy - oh / 2.0 - clearance && p.y <= cy + oh / 2.0 + clearance;
+            };
+            if (covers(w->start) || covers(w->target)) continue;
+            verts[4 * i + 0] = {cx - ow / 2.0, cy - oh / 2.0};
+            verts[4 * i + 1] = {cx + ow / 2.0, cy - oh / 2.0};
+            verts[4 * i + 2] = {cx + ow / 2.0, cy + oh / 2.0};
+            verts[4 * i + 3] = {cx - ow / 2.0, cy + oh / 2.0};
+            placed = true;
+        }
+        if (!placed)
+            return fail(SF_INVALID_ARGUMENT, "generate_world: could not place obstacle " + std::to_string(i) +
+                                                 " clear of start/target");
+        offsets[i] = 4 * i;
+        if (i < c->dynamic_obstacles) {
+            const double speed = c->max_speed * (1.0 - rng.uniform());
+            const double angle = rng.uniform(0.0, 2.0 * 3.14159265358979323846);
+            vel[i] = {speed * std::cos(angle), speed * std::sin(angle)};
+        } else {
+            vel[i] = {0.0, 0.0};
+        }
+    }
+    offsets[total] = 4 * total;
+    w->n_obstacles = total;
+    w->vertex_offsets = offsets;
+    w->vertices = verts;
+    w->velocities = vel;
+    return SF_OK;
+}
+
+static double reflect_axis(double lo, double hi, double limit, double& v) {   // simenv.hpp:139-149
+    if (lo <= 0.0) { v = -v; return -2.0 * lo; }
+    if (hi >= limit) { v = -v; return -2.0 * (hi - limit); }
+    return 0.0;
+}
+
+// simenv.hpp:155-184
+int sf_step_world(sf_world* w, sf_point* verts, sf_point* vel, double dt) {
+    if (!w) return fail(SF_INVALID_ARGUMENT, "world is null");
+    if (!(dt > 0.0)) return fail(SF_INVALID_ARGUMENT, "step_world: dt must be positive");
+    auto move = [&](sf_point& p, sf_point& v) {
+        p.x += v.x * dt;
+        p.y += v.y * dt;
+        p.x += reflect_axis(p.x, p.x, w->width, v.x);
+        p.y += reflect_axis(p.y, p.y, w->height, v.y);
+    };
+    move(w->start, w->start_velocity);
+    move(w->target, w->target_velocity);
+    for (uint32_t o = 0; o < w->n_obstacles; ++o) {
+        sf_point& ov = vel[o];
+        if (ov.x == 0.0 && ov.y == 0.0) continue;
+        const uint32_t v0 = w->vertex_offsets[o], v1 = w->vertex_offsets[o + 1];
+        for (uint32_t i = v0; i < v1; ++i) {
+            verts[i].x += ov.x * dt;
+            verts[i].y += ov.y * dt;
+        }
+        double bx0 = verts[v0].x, by0 = verts[v0].y, bx1 = bx0, by1 = by0;
+        for (uint32_t i = v0; i < v1; ++i) {
+            bx0 = std::min(bx0, verts[i].x); by0 = std::min(by0, verts[i].y);
+            bx1 = std::max(bx1, verts[i].x); by1 = std::max(by1, verts[i].y);
+        }
+        const double sx = reflect_axis(bx0, bx1, w->width, ov.x);
+        const double sy = reflect_axis(by0, by1, w->height, ov.y);
+        if (sx != 0.0 || sy != 0.0)
+            for (uint32_t i = v0; i < v1; ++i) { verts[i].x += sx; verts[i].y += sy; }
+    }
+    return SF_OK;
+}
+
+// simenv.hpp:239-276 with variant wiring (188-234)
+int sf_run_scenario(sf_ctx* ctx, const sf_scenario_config* c, int variant, uint32_t frames,
+                    const sf_planner_config* base, const double* evolved, sf_plan_record* records,
+                    double* best) {
+    if (!ctx || !c || !base || !records) return fail(SF_INVALID_ARGUMENT, "null argument");
+    if (frames < 1) return fail(SF_INVALID_ARGUMENT, "run_scenario: frame count must be >= 1");
+    if (variant < 0 || variant > 5) return fail(SF_INVALID_ARGUMENT, "unknown planner variant");
+    sf_planner_config cfg = *base;
+    std::vector<double> hyp;
+    static const double defaults[48] = {2, 1, 1, 0.4, 0.2, 0.2, 1, 1, 2, 0.7, 0.3, 0.1,
+                                        2, 2, 1, 0.8, 0.1, 0.6, 2, 2, 1, 0.8, 0.6, 0.4,
+                                        2, 1, 2, 0.2, 0.1, 0.3, 2, 1, 2, 0.9, 0.5, 0.5,
+                                        1, 2, 2, 0.4, 0.1, 0.8, 1, 2, 2, 0.9, 0.3, 0.3};
+    switch (variant) {
+    case 0: hyp.assign(evolved, evolved + 6 * cfg.groups); break;                  // sepso
+    case 1: cfg.auto_truncate = 0; cfg.max_iters_per_frame = 30;
+            hyp.assign(evolved, evolved + 6 * cfg.groups); break;                  // sepso-noat
+    case 2: cfg.gamma = 0.0; hyp.assign(evolved, evolved + 6 * cfg.groups); break; // sepso-nopi
+    case 3: case 4:                                                                // dtpso / dppso
+        cfg.gamma = 0.0; cfg.auto_truncate = 0; cfg.max_iters_per_frame = 30;
+        hyp.assign(defaults, defaults + 48);
+        break;
+    case 5:                                                                        // pso
+        cfg.gamma = 0.0; cfg.auto_truncate = 0; cfg.max_iters_per_frame = 30;
+        cfg.per_group = base->groups * base->per_group;
+        cfg.groups = 1;
+        hyp = {2.0, 2.0, 0.0, 0.9, 0.4, 0.5};
+        break;
+    }
+    sf_scenario_config sc = *c;
+    sc.frames = std::max<uint32_t>(sc.frames, 1);
+    const uint32_t n = c->dynamic_obstacles + c->static_obstacles;
+    std::vector<uint32_t> off(n + 1);
+    std::vector<sf_point> verts(4 * size_t(n)), vel(n);
+    sf_world w{};
+    int st = sf_generate_world(&sc, derive_seed(c->root_seed, "world"), &w, off.data(), verts.data(), vel.data());
+    if (st) return st;
+    std::vector<double> prev(cfg.dim), win(std::max<uint32_t>(cfg.tw, 1) + 1);
+    uint32_t wl = 0;
+    bool have_prev = false;
+    for (uint32_t f = 0; f < frames; ++f) {
+        std::vector<double> bp(cfg.dim);
+        st = sf_plan_frame(ctx, &w, have_prev ? prev.data() : nullptr, hyp.data(), &cfg,
+                           derive_seed(c->root_seed, "plan", f), win.data(), &wl, uint32_t(win.size()),
+                           &records[f], bp.data(), nullptr);
+        if (st) return st;
+        prev = bp;
+        have_prev = true;
+        if (best) std::copy(bp.begin(), bp.end(), best + size_t(f) * cfg.dim);
+        if ((st = sf_step_world(&w, verts.data(), vel.data(), c->dt))) return st;
+    }
+    return SF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,519 @@
+// host_runtime.cpp -- context plumbing, validation, launch planning, the
+// staged (HBM-resident) swarm driver and the host half of HSEF.
+#include "host_runtime.hpp"
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdlib>
+#include <limits>
+
+#include "stage_kernels.cuh"
+
+namespace sepso {
+
+static thread_local std::string g_error;
+
+void set_error(const std::string& msg) { g_error = msg; }
+int fail(int code, const std::string& msg) {
+    g_error = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+    return fail(SF_CUDA_ERROR, std::string(where) + ": " + cudaGetErrorString(e));
+}
+const char* last_error_cstr() { return g_error.c_str(); }
+
+cudaError_t DevBuf::ensure(size_t bytes) {
+    if (bytes <= n) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    const size_t want = std::max<size_t>(bytes, 1 << 16);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) n = want;
+    return e;
+}
+void DevBuf::release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+}
+cudaError_t PinnedBuf::ensure(size_t bytes) {
+    if (bytes <= n) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+    const size_t want = std::max<size_t>(bytes, 1 << 16);
+    cudaError_t e = cudaMallocHost(&p, want);
+    if (e == cudaSuccess) n = want;
+    return e;
+}
+void PinnedBuf::release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+}
+
+// --------------------------------------------------------------- validation
+int validate_hypers(const double* h, uint32_t G) {
+    if (G == 0) return fail(SF_INVALID_ARGUMENT, "HyperMatrix: at least one group required");
+    for (uint32_t g = 0; g < G; ++g) {
+        const double* r = h + 6 * g;
+        for (int f = 0; f < 6; ++f)
+            if (!std::isfinite(r[f])) return fail(SF_INVALID_ARGUMENT, "HyperMatrix: non-finite entry");
+        if (r[0] < 0 || r[1] < 0 || r[2] < 0)
+            return fail(SF_INVALID_ARGUMENT, "HyperMatrix: acceleration constants must be >= 0");
+        if (!(0.0 <= r[4] && r[4] <= r[3] && r[3] <= 1.0))
+            return fail(SF_INVALID_ARGUMENT, "HyperMatrix: need 0 <= omega_end <= omega_init <= 1");
+        if (!(0.0 < r[5] && r[5] <= 1.0))
+            return fail(SF_INVALID_ARGUMENT, "HyperMatrix: need 0 < v_limit <= 1");
+    }
+    return SF_OK;
+}
+
+int validate_bounds(const double* lo, const double* hi, uint32_t D) {
+    if (D == 0) return fail(SF_INVALID_ARGUMENT, "SearchBounds: dimension must be >= 1");
+    for (uint32_t d = 0; d < D; ++d) {
+        if (!std::isfinite(lo[d]) || !std::isfinite(hi[d]))
+            return fail(SF_INVALID_ARGUMENT, "SearchBounds: non-finite bound");
+        if (!(lo[d] < hi[d])) return fail(SF_INVALID_ARGUMENT, "SearchBounds: need x_lo < x_hi per dimension");
+    }
+    return SF_OK;
+}
+
+int validate_world(const sf_world* w) {
+    if (!w) return fail(SF_INVALID_ARGUMENT, "world is null");
+    if (!(w->width > 0.0) || !(w->height > 0.0))
+        return fail(SF_INVALID_ARGUMENT, "world dimensions must be positive");
+    auto inside = [&](const sf_point& p) {
+        return p.x >= 0.0 && p.x <= w->width && p.y >= 0.0 && p.y <= w->height;
+    };
+    if (!inside(w->start) || !inside(w->target))
+        return fail(SF_INVALID_ARGUMENT, "start/target outside the map");
+    if (w->n_obstacles && (!w->vertex_offsets || !w->vertices))
+        return fail(SF_INVALID_ARGUMENT, "world obstacle arrays are null");
+    for (uint32_t o = 0; o < w->n_obstacles; ++o) {
+        const uint32_t v0 = w->vertex_offsets[o], v1 = w->vertex_offsets[o + 1];
+        if (v1 < v0 + 3) return fail(SF_INVALID_ARGUMENT, "obstacle needs at least 3 vertices");
+        for (uint32_t i = v0; i < v1; ++i) {
+            const sf_point& p = w->vertices[i];
+            if (!std::isfinite(p.x) || !std::isfinite(p.y))
+                return fail(SF_INVALID_ARGUMENT, "obstacle vertex is not finite");
+        }
+        for (uint32_t i = v0; i < v1; ++i)
+            if (!inside(w->vertices[i])) return fail(SF_INVALID_ARGUMENT, "obstacle vertex outside the map");
+    }
+    return SF_OK;
+}
+
+int validate_planner(const sf_planner_config* c) {
+    if (!c) return fail(SF_INVALID_ARGUMENT, "planner config is null");
+    if (!(c->alpha >= 0.0) || !(c->beta >= 1.0))
+        return fail(SF_INVALID_ARGUMENT, "planner config: need alpha >= 0 and beta >= 1");
+    if (!(c->gamma >= 0.0 && c->gamma <= 1.0))
+        return fail(SF_INVALID_ARGUMENT, "planner config: gamma must lie in [0, 1]");
+    if (c->tw < 2) return fail(SF_INVALID_ARGUMENT, "planner config: tw must be >= 2");
+    if (!(c->delta > 0.0)) return fail(SF_INVALID_ARGUMENT, "planner config: delta must be > 0");
+    if (!(c->pi_radius > 0.0)) return fail(SF_INVALID_ARGUMENT, "planner config: pi_radius must be > 0");
+    if (c->max_iters_per_frame < 1)
+        return fail(SF_INVALID_ARGUMENT, "planner config: max_iters_per_frame must be >= 1");
+    if (c->groups < 1 || c->per_group < 1)
+        return fail(SF_INVALID_ARGUMENT, "planner config: G and N must be >= 1");
+    if (c->dim < 2 || c->dim % 2 != 0)
+        return fail(SF_INVALID_ARGUMENT, "planner config: dim must be even and >= 2");
+    return SF_OK;
+}
+
+// ------------------------------------------------------------ world records
+void pack_world_into(const sf_world& w, const WorldLayout& lay, unsigned char* dst) {
+    std::memset(dst, 0, lay.stride);
+    WorldHeader h{};
+    h.width = w.width;
+    h.height = w.height;
+    h.sx = w.start.x;
+    h.sy = w.start.y;
+    h.tx = w.target.x;
+    h.ty = w.target.y;
+    h.n_obs = w.n_obstacles;
+    h.n_verts = w.n_obstacles ? w.vertex_offsets[w.n_obstacles] - w.vertex_offsets[0] : 0;
+    h.svx = w.start_velocity.x;
+    h.svy = w.start_velocity.y;
+    h.tvx = w.target_velocity.x;
+    h.tvy = w.target_velocity.y;
+    std::memcpy(dst, &h, sizeof(h));
+    uint32_t* off = reinterpret_cast<uint32_t*>(dst + lay.off_offsets);
+    double* vv = reinterpret_cast<double*>(dst + lay.off_verts);
+    double* vel = reinterpret_cast<double*>(dst + lay.off_vel);
+    const uint32_t base = w.n_obstacles ? w.vertex_offsets[0] : 0;
+    for (uint32_t o = 0; o <= w.n_obstacles; ++o) off[o] = w.n_obstacles ? w.vertex_offsets[o] - base : 0;
+    for (uint32_t i = 0; i < h.n_verts; ++i) {
+        vv[2 * i] = w.vertices[base + i].x;
+        vv[2 * i + 1] = w.vertices[base + i].y;
+    }
+    for (uint32_t o = 0; o < w.n_obstacles; ++o) {
+        vel[2 * o] = w.velocities ? w.velocities[o].x : 0.0;
+        vel[2 * o + 1] = w.velocities ? w.velocities[o].y : 0.0;
+    }
+}
+
+void pack_worlds(const sf_world* worlds, uint32_t n, WorldPack& out) {
+    int max_obs = 1, max_verts = 3;
+    for (uint32_t s = 0; s < n; ++s) {
+        const sf_world& w = worlds[s];
+        max_obs = std::max<int>(max_obs, int(w.n_obstacles));
+        const uint32_t nv = w.n_obstacles ? w.vertex_offsets[w.n_obstacles] - w.vertex_offsets[0] : 0;
+        max_verts = std::max<int>(max_verts, int(nv));
+    }
+    out.lay = world_layout(max_obs, max_verts);
+    out.bytes.assign(size_t(n) * out.lay.stride, 0);
+    for (uint32_t s = 0; s < n; ++s) pack_world_into(worlds[s], out.lay, out.bytes.data() + size_t(s) * out.lay.stride);
+}
+
+bool force_staged() {
+    const char* e = std::getenv("SEPSO_FORCE_STAGED");
+    return e && e[0] == '1';
+}
+
+static int env_int(const char* name, int def) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : def;
+}
+
+// ------------------------------------------------------------ fused planning
+FusedPlan plan_fused(sf_ctx* ctx, int problem, int n_swarms, int G, int N, int D, int max_obs,
+                     int max_verts, int cap, int tw) {
+    FusedPlan fp;
+    SwarmParams& p = fp.p;
+    const bool path = problem == kPath;
+    const bool fp64 = ctx->precision == SF_FP64;
+    const int R = G * N, S = D / 2 + 1;
+    const int smem_max = max_smem_per_block();
+    p.n_swarms = n_swarms;
+    p.G = G;
+    p.N = N;
+    p.D = D;
+    p.cap = cap;
+    p.tw = tw;
+    p.max_obs = path ? std::max(max_obs, 1) : 0;
+    p.max_verts = path ? std::max(max_verts, 3) : 0;
+    const int want_c = ctx->force_cluster ? ctx->force_cluster : env_int("SEPSO_CLUSTER", 0);
+    const int want_t = ctx->force_threads ? ctx->force_threads : env_int("SEPSO_THREADS", 0);
+    // latency-oriented default: ~192 particle rows per CTA, up to 16 CTAs per cluster
+    int C = want_c > 0 ? want_c : std::max(1, std::min(16, (R + 191) / 192));
+    for (;; C *= 2) {
+        if (C > 16) C = 16;
+        const int Rc = (R + C - 1) / C;
+        p.C = C;
+        p.rows_per_cta = Rc;
+        int lgm = 1;
+        for (int c = 0; c < C; ++c) {
+            const int r0 = c * Rc, r1 = std::min(R, r0 + Rc);
+            if (r1 > r0) lgm = std::max(lgm, (r1 - 1) / N - r0 / N + 1);
+        }
+        p.max_local_groups = lgm;
+        if (path) {
+            p.entry_cap = std::min(std::max(1024, Rc * S * 2), 6144);
+            p.nthreads = std::min(512, std::max(128, ((Rc * S / 3) + 31) / 32 * 32));
+        } else {
+            p.entry_cap = 0;
+            p.nthreads = std::min(512, std::max(32, (Rc + 31) / 32 * 32));
+        }
+        if (want_t > 0) p.nthreads = std::min(512, std::max(32, want_t / 32 * 32));
+        fp.smem = smem_layout(p, fp64 ? 8 : 4, path).total;
+        if (int(fp.smem) <= smem_max) { fp.fits = true; break; }
+        if (C >= 16 || want_c > 0) break;
+    }
+    p.beta_int = 0;
+    return fp;
+}
+
+int launch_fused(sf_ctx* ctx, FusedPlan& fp, int problem) {
+    if (ctx->timing) cudaEventRecord(ctx->ev0, ctx->stream);
+    size_t smem = 0;
+    const int e = launch_swarms(fp.p, problem, ctx->precision == SF_FP64, ctx->stream, &smem);
+    if (e != 0) return cuda_fail(cudaError_t(e), "fused swarm launch");
+    if (ctx->timing) {
+        cudaEventRecord(ctx->ev1, ctx->stream);
+        cudaEventSynchronize(ctx->ev1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+        ctx->kernel_ms += ms;
+        ctx->launches += 1;
+    }
+    return SF_OK;
+}
+
+// ---------------------------------------------------------- staged driver
+int run_staged(sf_ctx* ctx, StagedRun& r) {
+    const bool fp64 = ctx->precision == SF_FP64;
+    const size_t tsz = fp64 ? 8 : 4;
+    const int G = r.G, N = r.N, D = r.D, R = G * N;
+    const bool path = r.problem == kPath;
+    cudaStream_t st = ctx->stream;
+    // host-side staging of constants
+    WorldPack wp;
+    if (path) pack_worlds(r.world, 1, wp);
+    std::vector<double> lo(D), hi(D);
+    for (int d = 0; d < D; ++d) {
+        if (path) {
+            lo[d] = 0.0;
+            hi[d] = d < D / 2 ? r.world->width : r.world->height;
+        } else {
+            lo[d] = r.lo[d];
+            hi[d] = r.hi[d];
+        }
+    }
+    // device arena
+    size_t off = 0;
+    auto take = [&](size_t b) { const size_t at = off; off = (off + b + 255) & ~size_t(255); return at; };
+    const size_t o_world = take(path ? wp.bytes.size() : 0);
+    const size_t o_hyp = take(size_t(G) * 6 * 8);
+    const size_t o_lo = take(size_t(D) * tsz), o_hi = take(size_t(D) * tsz);
+    const size_t o_prev = take(size_t(D) * 8);
+    const size_t o_x = take(size_t(R) * D * tsz), o_v = take(size_t(R) * D * tsz);
+    const size_t o_pb = take(size_t(R) * D * tsz);
+    const size_t o_fit = take(size_t(R) * tsz), o_pbf = take(size_t(R) * tsz);
+    const size_t o_q = take(size_t(R) * 4), o_pbq = take(size_t(R) * 4);
+    const size_t o_pf = take(size_t(G) * tsz), o_prow = take(size_t(G) * 4), o_pq = take(size_t(G) * 4);
+    const size_t o_gbx = take(size_t(G) * D * tsz), o_gbf = take(size_t(G) * tsz), o_gbq = take(size_t(G) * 4);
+    const size_t o_tbx = take(size_t(D) * tsz);
+    const size_t o_cand = take(cand_bytes(fp64, D));
+    const size_t o_st = take(sizeof(IterState));
+    const size_t o_win = take(size_t(std::max(r.tw, 1)) * 8);
+    const size_t o_trace = take(size_t(r.cap) * 8);
+    cudaError_t ce = ctx->scratch.ensure(off);
+    if (ce != cudaSuccess) return cuda_fail(ce, "staged arena");
+    unsigned char* dev = static_cast<unsigned char*>(ctx->scratch.p);
+    // stage host bytes (pinned) for the small constants
+    std::vector<unsigned char> h(o_x, 0);
+    if (path) std::memcpy(h.data() + o_world, wp.bytes.data(), wp.bytes.size());
+    std::memcpy(h.data() + o_hyp, r.hypers, size_t(G) * 6 * 8);
+    for (int d = 0; d < D; ++d) {
+        if (fp64) {
+            reinterpret_cast<double*>(h.data() + o_lo)[d] = lo[d];
+            reinterpret_cast<double*>(h.data() + o_hi)[d] = hi[d];
+        } else {
+            reinterpret_cast<float*>(h.data() + o_lo)[d] = float(lo[d]);
+            reinterpret_cast<float*>(h.data() + o_hi)[d] = float(hi[d]);
+        }
+    }
+    if (r.prev) std::memcpy(h.data() + o_prev, r.prev, size_t(D) * 8);
+    ce = cudaMemcpyAsync(dev, h.data(), o_x, cudaMemcpyHostToDevice, st);
+    if (ce != cudaSuccess) return cuda_fail(ce, "staged upload");
+    // bests start at +inf (swarm.hpp:113-116)
+    std::vector<unsigned char> inf_f(size_t(std::max(R, G)) * tsz);
+    for (int i = 0; i < std::max(R, G); ++i) {
+        if (fp64) reinterpret_cast<double*>(inf_f.data())[i] = std::numeric_limits<double>::infinity();
+        else reinterpret_cast<float*>(inf_f.data())[i] = std::numeric_limits<float>::infinity();
+    }
+    cudaMemcpyAsync(dev + o_pbf, inf_f.data(), size_t(R) * tsz, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(dev + o_gbf, inf_f.data(), size_t(G) * tsz, cudaMemcpyHostToDevice, st);
+    cudaMemsetAsync(dev + o_pbq, 0, size_t(R) * 4, st);
+    cudaMemsetAsync(dev + o_gbq, 0, size_t(G) * 4, st);
+    cudaMemsetAsync(dev + o_gbx, 0, size_t(G) * D * tsz, st);
+    cudaMemsetAsync(dev + o_tbx, 0, size_t(D) * tsz, st);
+    IterState is{};
+    is.tbest_f = std::numeric_limits<double>::infinity();
+    is.tbest_group = -1;
+    is.nonfinite_row = INT_MAX;
+    is.win_len = std::min(r.win_len_in, r.tw);
+    is.win_head = 0;
+    cudaMemcpyAsync(dev + o_st, &is, sizeof(is), cudaMemcpyHostToDevice, st);
+    if (r.tw > 0 && r.win_in && is.win_len > 0)
+        cudaMemcpyAsync(dev + o_win, r.win_in, size_t(is.win_len) * 8, cudaMemcpyHostToDevice, st);
+
+    if (ctx->timing) cudaEventRecord(ctx->ev0, st);
+    const StageShape s{G, N, D, 0, R};
+    IterState* dst = reinterpret_cast<IterState*>(dev + o_st);
+    int e = stage_init(fp64, s, reinterpret_cast<double*>(dev + o_hyp), dev + o_lo, dev + o_hi, r.seed,
+                       r.prev ? reinterpret_cast<double*>(dev + o_prev) : nullptr, r.warm, r.pi_radius,
+                       dev + o_x, dev + o_v, dev + o_pb, st);
+    if (e) return cuda_fail(cudaError_t(e), "stage_init");
+    const WorldLayout& wl = wp.lay;
+    for (int k = 1; k <= r.cap; ++k) {
+        if (path)
+            e = stage_eval_path(fp64, dev + o_world, wl.max_obs, wl.max_verts, int(wl.off_offsets),
+                                int(wl.off_verts), D, R, dev + o_x, r.alpha, r.beta, dev + o_fit,
+                                reinterpret_cast<int*>(dev + o_q), dst, st);
+        else
+            e = stage_eval_bench(fp64, r.problem, D, R, dev + o_x, dev + o_fit,
+                                 reinterpret_cast<int*>(dev + o_q), dst, st);
+        if (e) return cuda_fail(cudaError_t(e), "stage_eval");
+        e = stage_pbest_partials(fp64, s, dev + o_x, dev + o_fit, reinterpret_cast<int*>(dev + o_q),
+                                 dev + o_pb, dev + o_pbf, reinterpret_cast<int*>(dev + o_pbq), dst,
+                                 dev + o_pf, reinterpret_cast<int*>(dev + o_prow),
+                                 reinterpret_cast<int*>(dev + o_pq), dst, st);
+        if (e) return cuda_fail(cudaError_t(e), "stage_pbest");
+        e = stage_group_bests(fp64, s, dev + o_pf, reinterpret_cast<int*>(dev + o_prow),
+                              reinterpret_cast<int*>(dev + o_pq), dev + o_pb, dev + o_gbx, dev + o_gbf,
+                              reinterpret_cast<int*>(dev + o_gbq), dev + o_cand, dst, st);
+        if (e) return cuda_fail(cudaError_t(e), "stage_group_bests");
+        e = stage_finish(fp64, D, dev + o_cand, 1, dev + o_tbx, dst,
+                         r.tw > 0 ? reinterpret_cast<double*>(dev + o_win) : nullptr, r.tw,
+                         r.auto_truncate, r.delta, k, r.cap, reinterpret_cast<double*>(dev + o_trace), st);
+        if (e) return cuda_fail(cudaError_t(e), "stage_finish");
+        if (k < r.cap) {
+            const uint64_t first = 2ull * uint64_t(R) * D + uint64_t(k - 1) * 3ull * R;
+            e = stage_step(fp64, s, reinterpret_cast<double*>(dev + o_hyp), dev + o_lo, dev + o_hi,
+                           dev + o_x, dev + o_v, dev + o_pb, dev + o_gbx, dev + o_tbx, r.seed, first,
+                           k, r.cap, dst, st);
+            if (e) return cuda_fail(cudaError_t(e), "stage_step");
+        }
+    }
+    if (ctx->timing) {
+        cudaEventRecord(ctx->ev1, st);
+        cudaEventSynchronize(ctx->ev1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+        ctx->kernel_ms += ms;
+        ctx->launches += 1;
+    }
+    // results
+    IterState fin{};
+    std::vector<unsigned char> tb(size_t(D) * tsz);
+    r.trace.assign(r.cap, 0.0);
+    r.win_out.assign(std::max(r.tw, 1), 0.0);
+    cudaMemcpyAsync(&fin, dev + o_st, sizeof(fin), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(tb.data(), dev + o_tbx, tb.size(), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(r.trace.data(), dev + o_trace, size_t(r.cap) * 8, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(r.win_out.data(), dev + o_win, r.win_out.size() * 8, cudaMemcpyDeviceToHost, st);
+    ce = cudaStreamSynchronize(st);
+    if (ce != cudaSuccess) return cuda_fail(ce, "staged run");
+    r.best.assign(D, 0.0);
+    for (int d = 0; d < D; ++d)
+        r.best[d] = fp64 ? reinterpret_cast<double*>(tb.data())[d] : double(reinterpret_cast<float*>(tb.data())[d]);
+    // window back in oldest-first order
+    std::vector<double> w(fin.win_len);
+    for (int i = 0; i < fin.win_len; ++i) w[i] = r.win_out[(fin.win_head + i) % std::max(r.tw, 1)];
+    r.win_out = w;
+    r.out = SwarmOut{};
+    r.out.status = uint32_t(fin.status);
+    r.out.iterations = uint32_t(fin.k_done);
+    r.out.truncated = uint32_t(fin.truncated);
+    r.out.window_len = uint32_t(fin.win_len);
+    if (fin.status == 2) {
+        r.out.bad_g = uint32_t(fin.nonfinite_row / N);
+        r.out.bad_n = uint32_t(fin.nonfinite_row % N);
+        r.out.bad_k = uint32_t(fin.k_done);
+    } else {
+        r.out.fitness = fin.tbest_f;
+        r.out.q = uint32_t(fin.tbest_q);
+        if (path) {   // record length (planner.hpp:194) on the final best path, FP64
+            double total = 0.0, px = r.world->start.x, py = r.world->start.y;
+            if (!fp64) { px = double(float(px)); py = double(float(py)); }
+            const int W = D / 2;
+            for (int j = 1; j <= W + 1; ++j) {
+                double nx = j <= W ? r.best[j - 1] : r.world->target.x;
+                double ny = j <= W ? r.best[W + j - 1] : r.world->target.y;
+                if (!fp64 && j > W) { nx = double(float(nx)); ny = double(float(ny)); }
+                total += std::hypot(nx - px, ny - py);
+                px = nx;
+                py = ny;
+            }
+            r.out.length = total;
+        }
+    }
+    return SF_OK;
+}
+
+// -------------------------------------------------------------- host PSO
+uint64_t derive_seed(uint64_t root, const char* tag) {
+    return splitmix64(root ^ fnv1a64(tag, std::strlen(tag)));
+}
+uint64_t derive_seed(uint64_t root, const char* tag, uint64_t index) {
+    return splitmix64(derive_seed(root, tag) + index);
+}
+
+static double clampd(double v, double lo, double hi) { return v < lo ? lo : (hi < v ? hi : v); }
+
+// swarm.hpp:94-132
+void host_init_swarm(HostSwarm& s, const double* hypers, const double* lo, const double* hi,
+                     uint32_t G, uint32_t N, uint32_t D, HostStream& rng) {
+    s.G = G;
+    s.N = N;
+    s.D = D;
+    const size_t total = size_t(G) * N * D;
+    s.x.resize(total);
+    s.v.resize(total);
+    s.pbf.assign(size_t(G) * N, std::numeric_limits<double>::infinity());
+    s.gbx.assign(size_t(G) * D, 0.0);
+    s.gbf.assign(G, std::numeric_limits<double>::infinity());
+    s.tbx.assign(D, 0.0);
+    s.tbf = std::numeric_limits<double>::infinity();
+    for (size_t i = 0; i < total; ++i) s.x[i] = rng.uniform(lo[i % D], hi[i % D]);
+    for (uint32_t g = 0; g < G; ++g) {
+        double* vg = s.v.data() + size_t(g) * N * D;
+        for (size_t i = 0; i < size_t(N) * D; ++i) {
+            const double vmax = hypers[6 * g + 5] * (hi[i % D] - lo[i % D]);
+            vg[i] = rng.uniform(-vmax, vmax);
+        }
+    }
+    s.pbx = s.x;
+}
+
+// swarm.hpp:138-174
+void host_step(HostSwarm& s, const double* hypers, const double* lo, const double* hi,
+               HostStream& rng, uint32_t k, uint32_t T) {
+    const size_t GN = size_t(s.G) * s.N, D = s.D;
+    std::vector<double> r(3 * GN);
+    for (double& u : r) u = rng.uniform();
+    const double frac = double(k) / double(T);
+    for (uint32_t g = 0; g < s.G; ++g) {
+        const double* h = hypers + 6 * g;
+        const double w = h[3] - (h[3] - h[4]) * frac;
+        const double* gb = s.gbx.data() + size_t(g) * D;
+        for (uint32_t n = 0; n < s.N; ++n) {
+            const size_t row = size_t(g) * s.N + n;
+            const double a1 = h[0] * r[row], a2 = h[1] * r[GN + row], a3 = h[2] * r[2 * GN + row];
+            double* xv = s.x.data() + row * D;
+            double* vv = s.v.data() + row * D;
+            const double* pb = s.pbx.data() + row * D;
+            for (size_t d = 0; d < D; ++d) {
+                const double vmax = h[5] * (hi[d] - lo[d]);
+                double nv = w * vv[d] + a1 * (pb[d] - xv[d]) + a2 * (gb[d] - xv[d]) + a3 * (s.tbx[d] - xv[d]);
+                nv = clampd(nv, -vmax, vmax);
+                vv[d] = nv;
+                xv[d] = clampd(xv[d] + nv, lo[d], hi[d]);
+            }
+        }
+    }
+}
+
+// runner.hpp:68-93
+void host_update_bests(HostSwarm& s, const double* fitness) {
+    const size_t N = s.N, D = s.D;
+    for (uint32_t g = 0; g < s.G; ++g) {
+        for (size_t n = 0; n < N; ++n) {
+            const size_t r = g * N + n;
+            if (fitness[r] < s.pbf[r]) {
+                s.pbf[r] = fitness[r];
+                std::copy_n(s.x.data() + r * D, D, s.pbx.data() + r * D);
+            }
+        }
+        for (size_t n = 0; n < N; ++n) {
+            const size_t r = g * N + n;
+            if (s.pbf[r] < s.gbf[g]) {
+                s.gbf[g] = s.pbf[r];
+                std::copy_n(s.pbx.data() + r * D, D, s.gbx.data() + g * D);
+            }
+        }
+        if (s.gbf[g] < s.tbf) {
+            s.tbf = s.gbf[g];
+            std::copy_n(s.gbx.data() + g * D, D, s.tbx.data());
+        }
+    }
+}
+
+void unflatten_hypers(const double* particle, uint32_t groups, double* out) {
+    static const double lo[6] = {0.5, 0.5, 0.5, 0.1, 0.05, 0.05};   // hsef.hpp:75
+    static const double hi[6] = {2.5, 2.5, 2.5, 1.0, 0.8, 1.0};     // hsef.hpp:76
+    for (uint32_t g = 0; g < groups; ++g) {
+        double f[6];
+        for (int i = 0; i < 6; ++i) f[i] = clampd(particle[6 * g + i], lo[i], hi[i]);
+        if (f[4] > f[3]) std::swap(f[3], f[4]);
+        std::memcpy(out + 6 * g, f, sizeof(f));
+    }
+}
+
+} // namespace sepso

@@ -1,0 +1,135 @@
+// host_runtime.hpp -- host-side C++ of the engine (context, validation,
+// staging, the HSEF outer loop and scene state).  Internal to libsepso_cuda.so.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sepso.h"
+#include "philox.cuh"
+#include "swarm_kernel.cuh"
+
+namespace sepso {
+
+// ------------------------------------------------------------------ errors
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* where);
+
+// ------------------------------------------------------------ device memory
+struct DevBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    cudaError_t ensure(size_t bytes);
+    void release();
+};
+
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    cudaError_t ensure(size_t bytes);
+    void release();
+};
+
+} // namespace sepso
+
+struct sf_ctx {
+    int device = 0;
+    int precision = SF_FP32;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    bool timing = false;
+    double kernel_ms = 0.0;
+    uint64_t launches = 0;
+    int force_cluster = 0, force_threads = 0;
+    sepso::DevBuf io, scratch;
+    sepso::PinnedBuf hio;
+};
+
+namespace sepso {
+
+// --------------------------------------------------------------- validation
+// Reference preconditions, each reported as SF_INVALID_ARGUMENT.
+int validate_hypers(const double* h, uint32_t G);                    // hypers.hpp:31-46
+int validate_bounds(const double* lo, const double* hi, uint32_t D); // hypers.hpp:109-120
+int validate_world(const sf_world* w);                               // geometry.hpp:55-66
+int validate_planner(const sf_planner_config* c);                    // planner.hpp:41-56
+
+// ------------------------------------------------------------ world records
+struct WorldPack {
+    WorldLayout lay;
+    std::vector<unsigned char> bytes;   // n_worlds * lay.stride
+};
+void pack_worlds(const sf_world* worlds, uint32_t n, WorldPack& out);
+void pack_world_into(const sf_world& w, const WorldLayout& lay, unsigned char* dst);
+
+// ------------------------------------------------------------ fused launches
+struct FusedPlan {
+    SwarmParams p{};
+    size_t smem = 0;
+    bool fits = false;
+};
+// Pick cluster size / threads / list capacity for n swarms of shape (G, N, D).
+FusedPlan plan_fused(sf_ctx* ctx, int problem, int n_swarms, int G, int N, int D, int max_obs,
+                     int max_verts, int cap, int tw);
+
+// Launch on ctx->stream, bracketed by timing events when enabled.
+int launch_fused(sf_ctx* ctx, FusedPlan& fp, int problem);
+
+// ---------------------------------------------------------- staged (HBM) run
+// One swarm with state in HBM, stage kernels per iteration (used when the
+// swarm does not fit a cluster, or when SEPSO_FORCE_STAGED=1).
+struct StagedRun {
+    int problem = kPath;
+    int G = 0, N = 0, D = 0, cap = 0;
+    const sf_world* world = nullptr;
+    const double* lo = nullptr;  // benchmark box
+    const double* hi = nullptr;
+    double alpha = 30.0, beta = 4.0;
+    const double* hypers = nullptr;
+    uint64_t seed = 0;
+    const double* prev = nullptr;
+    int warm = 0;
+    double pi_radius = 20.0;
+    int auto_truncate = 0, tw = 0;
+    double delta = 10.0;
+    const double* win_in = nullptr;   // last min(len, tw) values
+    int win_len_in = 0;
+    // outputs
+    SwarmOut out{};
+    std::vector<double> best, trace, win_out;
+};
+int run_staged(sf_ctx* ctx, StagedRun& r);
+
+bool force_staged();
+
+// --------------------------------------------------------- host-side PSO
+// The HSEF outer swarm lives on the host (hsef.hpp:144-165); this is the
+// reference's batched update restated in C++ over the engine's Philox stream
+// (sequential draw counter), compiled with -ffp-contract=off.
+struct HostStream {
+    uint64_t seed, drawn = 0;
+    explicit HostStream(uint64_t s) : seed(s) {}
+    double uniform() { return double(philox_word(seed, drawn++) >> 11) * 0x1.0p-53; }
+    double uniform(double lo, double hi) { return lo + uniform() * (hi - lo); }
+};
+
+struct HostSwarm {
+    uint32_t G = 0, N = 0, D = 0;
+    std::vector<double> x, v, pbx, pbf, gbx, gbf, tbx;
+    double tbf = 0.0;
+};
+void host_init_swarm(HostSwarm& s, const double* hypers, const double* lo, const double* hi,
+                     uint32_t G, uint32_t N, uint32_t D, HostStream& rng);
+void host_step(HostSwarm& s, const double* hypers, const double* lo, const double* hi,
+               HostStream& rng, uint32_t k, uint32_t T);
+void host_update_bests(HostSwarm& s, const double* fitness);
+void unflatten_hypers(const double* particle, uint32_t groups, double* out);   // hsef.hpp:57-71
+
+uint64_t derive_seed(uint64_t root, const char* tag);
+uint64_t derive_seed(uint64_t root, const char* tag, uint64_t index);
+
+} // namespace sepso

@@ -1,0 +1,519 @@
+// stage_kernels.cu -- HBM-resident stage kernels (see stage_kernels.cuh).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "stage_kernels.cuh"
+#include "swarm_device.cuh"
+
+namespace sepso {
+
+struct CandHdr {        // one device's population-best candidate (runner.hpp:88-91)
+    double f;
+    int q;
+    int g;
+};
+
+size_t cand_bytes(bool fp64, int D) {
+    return (sizeof(CandHdr) + size_t(D) * (fp64 ? 8 : 4) + 15) & ~size_t(15);
+}
+
+static inline unsigned grid_for(long long work, int block) {
+    long long g = (work + block - 1) / block;
+    if (g > 148LL * 32) g = 148LL * 32;
+    return unsigned(g < 1 ? 1 : g);
+}
+
+// --------------------------------------------------------------------- init
+// swarm.hpp:94-132 / planner.hpp:77-133 (draws indexed by global row)
+template <class T>
+__global__ void k_init(StageShape s, const double* __restrict__ hypers, const T* __restrict__ lo,
+                       const T* __restrict__ hi, uint64_t seed, const double* __restrict__ prev,
+                       int warm, double pi_radius, T* x, T* v, T* pb) {
+    using A = Ar<T>;
+    const long long total = (long long)s.rows * s.D;
+    const int R = s.G * s.N;
+    const T rad = T(pi_radius);
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int rl = int(e / s.D), d = int(e - (long long)rl * s.D);
+        const int row = s.row_begin + rl, g = row / s.N, n = row - g * s.N;
+        const uint64_t ix = uint64_t(row) * uint64_t(s.D) + uint64_t(d);
+        const T ux = unit_from_word<T>(philox_word(seed, ix));
+        const T l0 = lo[d], h0 = hi[d];
+        T xv;
+        if (prev != nullptr && n < warm) {
+            const T ctr = T(prev[d]);
+            const T l = A::sub(ctr, rad) > l0 ? A::sub(ctr, rad) : l0;
+            const T h = h0 < A::add(ctr, rad) ? h0 : A::add(ctr, rad);
+            xv = A::add(l, A::mul(ux, A::sub(h, l)));
+        } else {
+            xv = A::add(l0, A::mul(ux, A::sub(h0, l0)));
+        }
+        const T uv = unit_from_word<T>(philox_word(seed, uint64_t(R) * s.D + ix));
+        const T vmax = A::mul(T(hypers[g * 6 + 5]), A::sub(h0, l0));
+        const T vlo = -vmax;
+        x[e] = xv;
+        pb[e] = xv;
+        v[e] = A::add(vlo, A::mul(uv, A::sub(vmax, vlo)));
+    }
+}
+
+int stage_init(bool fp64, const StageShape& s, const double* hypers, const void* lo,
+               const void* hi, uint64_t seed, const double* prev, int warm, double pi_radius,
+               void* x, void* v, void* pb, void* stream) {
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const unsigned grid = grid_for((long long)s.rows * s.D, 256);
+    if (fp64)
+        k_init<double><<<grid, 256, 0, st>>>(s, hypers, (const double*)lo, (const double*)hi, seed,
+                                              prev, warm, pi_radius, (double*)x, (double*)v,
+                                              (double*)pb);
+    else
+        k_init<float><<<grid, 256, 0, st>>>(s, hypers, (const float*)lo, (const float*)hi, seed,
+                                             prev, warm, pi_radius, (float*)x, (float*)v, (float*)pb);
+    return int(cudaGetLastError());
+}
+
+// --------------------------------------------------------------------- step
+// K1, the fused update (swarm.hpp:138-174).  One CTA per tile of TR rows: the
+// tile's 3*TR Philox draws (draw_step_randoms order, swarm.hpp:59-70) go to
+// shared memory, then every element is read once and written once:
+// 20 B/element in FP32 (x, v, pbest in; x, v out).  VEC = 4 uses 16-byte
+// vector accesses when D % 4 == 0.
+constexpr int kStepRows = 32;
+
+template <class T, int VEC>
+__global__ void __launch_bounds__(256) k_step(StageShape s, const double* __restrict__ hypers,
+                                              const T* __restrict__ lo, const T* __restrict__ hi,
+                                              T* __restrict__ x, T* __restrict__ v,
+                                              const T* __restrict__ pb, const T* __restrict__ gbx,
+                                              const T* __restrict__ tbx, uint64_t seed,
+                                              uint64_t first_draw, int k, int total,
+                                              const IterState* gate) {
+    using A = Ar<T>;
+    if (gate != nullptr && gate->stop) return;
+    __shared__ T coef[3 * kStepRows];
+    __shared__ T hw[64 * 3];   // per group: omega_k, vmax scale (v_limit), spare
+    const int R = s.G * s.N, D = s.D;
+    const int r0 = blockIdx.x * kStepRows;
+    const int nr = min(kStepRows, s.rows - r0);
+    if (nr <= 0) return;
+    const T frac = T(double(k) / double(total));          // inertia_at (swarm.hpp:81-84)
+    const int g_lo = (s.row_begin + r0) / s.N, g_hi = (s.row_begin + r0 + nr - 1) / s.N;
+    for (int t = threadIdx.x; t <= g_hi - g_lo; t += blockDim.x) {
+        const double* h = hypers + (g_lo + t) * 6;
+        hw[t * 3 + 0] = A::sub(T(h[3]), A::mul(A::sub(T(h[3]), T(h[4])), frac));
+        hw[t * 3 + 1] = T(h[5]);
+    }
+    for (int t = threadIdx.x; t < 3 * nr; t += blockDim.x) {
+        const int j = t / nr, rl = t - j * nr;
+        const int row = s.row_begin + r0 + rl, g = row / s.N;
+        const T u = unit_from_word<T>(philox_word(seed, first_draw + uint64_t(j) * R + row));
+        coef[j * kStepRows + rl] = A::mul(T(hypers[g * 6 + j]), u);
+    }
+    __syncthreads();
+    const int DV = D / VEC;
+    for (int e = threadIdx.x; e < nr * DV; e += blockDim.x) {
+        const int rl = e / DV, dv = e - rl * DV;
+        const int row = s.row_begin + r0 + rl, g = row / s.N;
+        const T w = hw[(g - g_lo) * 3], vl = hw[(g - g_lo) * 3 + 1];
+        const T a1 = coef[rl], a2 = coef[kStepRows + rl], a3 = coef[2 * kStepRows + rl];
+        const size_t base = size_t(r0 + rl) * D + size_t(dv) * VEC;
+        T xs[VEC], vs[VEC], ps[VEC], gs[VEC], ts[VEC], ls[VEC], hs[VEC];
+        if constexpr (VEC == 4 && sizeof(T) == 4) {
+            *reinterpret_cast<float4*>(xs) = *reinterpret_cast<const float4*>(x + base);
+            *reinterpret_cast<float4*>(vs) = *reinterpret_cast<const float4*>(v + base);
+            *reinterpret_cast<float4*>(ps) = __ldcs(reinterpret_cast<const float4*>(pb + base));
+            *reinterpret_cast<float4*>(gs) = *reinterpret_cast<const float4*>(gbx + size_t(g) * D + dv * 4);
+            *reinterpret_cast<float4*>(ts) = *reinterpret_cast<const float4*>(tbx + dv * 4);
+            *reinterpret_cast<float4*>(ls) = *reinterpret_cast<const float4*>(lo + dv * 4);
+            *reinterpret_cast<float4*>(hs) = *reinterpret_cast<const float4*>(hi + dv * 4);
+        } else {
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) {
+                xs[i] = x[base + i]; vs[i] = v[base + i]; ps[i] = pb[base + i];
+                gs[i] = gbx[size_t(g) * D + dv * VEC + i]; ts[i] = tbx[dv * VEC + i];
+                ls[i] = lo[dv * VEC + i]; hs[i] = hi[dv * VEC + i];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) {
+            const T vmax = A::mul(vl, A::sub(hs[i], ls[i]));
+            const T xv = xs[i];
+            T nv = A::add(A::add(A::add(A::mul(w, vs[i]), A::mul(a1, A::sub(ps[i], xv))),
+                                 A::mul(a2, A::sub(gs[i], xv))),
+                          A::mul(a3, A::sub(ts[i], xv)));
+            nv = clampT(nv, T(-vmax), vmax);
+            vs[i] = nv;
+            xs[i] = clampT(A::add(xv, nv), ls[i], hs[i]);
+        }
+        if constexpr (VEC == 4 && sizeof(T) == 4) {
+            *reinterpret_cast<float4*>(x + base) = *reinterpret_cast<const float4*>(xs);
+            *reinterpret_cast<float4*>(v + base) = *reinterpret_cast<const float4*>(vs);
+        } else {
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) { x[base + i] = xs[i]; v[base + i] = vs[i]; }
+        }
+    }
+}
+
+int stage_step(bool fp64, const StageShape& s, const double* hypers, const void* lo,
+               const void* hi, void* x, void* v, const void* pb, const void* gbx,
+               const void* tbx, uint64_t seed, uint64_t first_draw, int k, int total,
+               const IterState* gate, void* stream) {
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const unsigned grid = unsigned((s.rows + kStepRows - 1) / kStepRows);
+    if (grid == 0) return 0;
+    if (fp64)
+        k_step<double, 1><<<grid, 256, 0, st>>>(s, hypers, (const double*)lo, (const double*)hi,
+                                                (double*)x, (double*)v, (const double*)pb,
+                                                (const double*)gbx, (const double*)tbx, seed,
+                                                first_draw, k, total, gate);
+    else if (s.D % 4 == 0)
+        k_step<float, 4><<<grid, 256, 0, st>>>(s, hypers, (const float*)lo, (const float*)hi,
+                                               (float*)x, (float*)v, (const float*)pb,
+                                               (const float*)gbx, (const float*)tbx, seed,
+                                               first_draw, k, total, gate);
+    else
+        k_step<float, 1><<<grid, 256, 0, st>>>(s, hypers, (const float*)lo, (const float*)hi,
+                                               (float*)x, (float*)v, (const float*)pb,
+                                               (const float*)gbx, (const float*)tbx, seed,
+                                               first_draw, k, total, gate);
+    return int(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------- path eval
+// K2 standalone: one CTA per tile of rows, world staged in shared memory, the
+// same cull + compaction + filtered-predicate machinery as the fused kernel.
+struct EvalSmem {
+    size_t misc, lo, hi, obb, ooff, vert, edge, seglen, q, list, total;
+};
+
+SEPSO_LHD EvalSmem eval_smem(int rows_tile, int D, int max_obs, int max_verts, int entry_cap,
+                          size_t tsz) {
+    EvalSmem L{};
+    size_t o = 0;
+    auto take = [&](size_t b) { const size_t at = o; o = sm_align(o + b); return at; };
+    const int S = D / 2 + 1;
+    L.misc = take(256);
+    L.lo = take(size_t(D) * tsz);
+    L.hi = take(size_t(D) * tsz);
+    L.obb = take(size_t(max_obs) * 4 * tsz);
+    L.ooff = take(size_t(max_obs + 1) * 4);
+    L.vert = take(size_t(max_verts) * 2 * tsz);
+    L.edge = take(size_t(max_verts) * 4 * tsz);
+    L.seglen = take(size_t(rows_tile) * S * tsz);
+    L.q = take(size_t(rows_tile) * 4);
+    L.list = take(size_t(entry_cap) * 4);
+    L.total = o;
+    return L;
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) k_eval_path(const unsigned char* __restrict__ world,
+                                                   SwarmParams pp, int rows, int rows_tile,
+                                                   const T* x, T* fit, int* qout,
+                                                   const IterState* gate) {
+    if (gate != nullptr && gate->stop) return;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const EvalSmem L = eval_smem(rows_tile, pp.D, pp.max_obs, pp.max_verts, pp.entry_cap, sizeof(T));
+    const int r0 = blockIdx.x * rows_tile;
+    Ctx<T> c{};
+    c.D = pp.D; c.W = pp.D / 2; c.S = c.W + 1;
+    c.P = min(rows_tile, rows - r0);
+    if (c.P <= 0) return;
+    c.x = const_cast<T*>(x) + size_t(r0) * pp.D;
+    c.fit = fit + r0;
+    c.lo = (T*)(smem + L.lo); c.hi = (T*)(smem + L.hi);
+    c.obb = (T*)(smem + L.obb); c.ooff = (int*)(smem + L.ooff); c.vert = (T*)(smem + L.vert);
+    c.edge = (T*)(smem + L.edge); c.seglen = (T*)(smem + L.seglen); c.q = (int*)(smem + L.q);
+    c.list = (uint32_t*)(smem + L.list); c.m = (Misc<T>*)(smem + L.misc);
+    load_world(c, world, pp.off_offsets, pp.off_verts);
+    if (threadIdx.x == 0) {
+        c.m->n_pair = 0;
+        c.m->n_cont = 0;
+        c.m->cont_cap = min(pp.entry_cap / 4, c.P * max(c.O, 1));
+    }
+    for (int i = threadIdx.x; i < c.P; i += blockDim.x) c.q[i] = 0;
+    __syncthreads();
+    path_fitness_phase(pp, c);
+    for (int i = threadIdx.x; i < c.P; i += blockDim.x) qout[r0 + i] = c.q[i];
+}
+
+int stage_eval_path(bool fp64, const unsigned char* world, int max_obs, int max_verts,
+                    int off_offsets, int off_verts, int D, int rows, const void* x, double alpha,
+                    double beta, void* fit, int* q, const IterState* gate, void* stream) {
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    SwarmParams pp{};
+    pp.D = D;
+    pp.max_obs = max_obs;
+    pp.max_verts = max_verts;
+    pp.off_offsets = off_offsets;
+    pp.off_verts = off_verts;
+    pp.alpha = alpha;
+    pp.beta = beta;
+    pp.beta_int = (beta == double(int(beta)) && beta >= 1.0 && beta <= 64.0) ? int(beta) : 0;
+    const int rows_tile = 64;
+    const int S = D / 2 + 1;
+    pp.entry_cap = std::max(1024, std::min(rows_tile * (S + 1) * std::max(max_obs, 1), 8192));
+    const size_t tsz = fp64 ? 8 : 4;
+    const EvalSmem L = eval_smem(rows_tile, D, max_obs, max_verts, pp.entry_cap, tsz);
+    const unsigned grid = unsigned((rows + rows_tile - 1) / rows_tile);
+    if (grid == 0) return 0;
+    cudaError_t e;
+    if (fp64) {
+        e = cudaFuncSetAttribute(k_eval_path<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.total));
+        if (e != cudaSuccess) return int(e);
+        k_eval_path<double><<<grid, 256, L.total, st>>>(world, pp, rows, rows_tile, (const double*)x,
+                                                        (double*)fit, q, gate);
+    } else {
+        e = cudaFuncSetAttribute(k_eval_path<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.total));
+        if (e != cudaSuccess) return int(e);
+        k_eval_path<float><<<grid, 256, L.total, st>>>(world, pp, rows, rows_tile, (const float*)x,
+                                                       (float*)fit, q, gate);
+    }
+    return int(cudaGetLastError());
+}
+
+template <class T>
+__global__ void k_eval_bench(int kind, int D, int rows, const T* x, T* fit, int* q,
+                             const IterState* gate) {
+    if (gate != nullptr && gate->stop) return;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+        fit[r] = bench_eval<T>(kind, x + size_t(r) * D, D);
+        if (q) q[r] = 0;
+    }
+}
+
+int stage_eval_bench(bool fp64, int kind, int D, int rows, const void* x, void* fit, int* q,
+                     const IterState* gate, void* stream) {
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const unsigned grid = grid_for(rows, 128);
+    if (fp64) k_eval_bench<double><<<grid, 128, 0, st>>>(kind, D, rows, (const double*)x, (double*)fit, q, gate);
+    else k_eval_bench<float><<<grid, 128, 0, st>>>(kind, D, rows, (const float*)x, (float*)fit, q, gate);
+    return int(cudaGetLastError());
+}
+
+// ------------------------------------------------------------ best tracking
+// runner.hpp:73-80: warp per row, strict '<', copy x -> pbest_x on improvement.
+template <class T>
+__global__ void k_pbest(StageShape s, const T* __restrict__ x, const T* __restrict__ fit,
+                        const int* __restrict__ q, T* pb, T* pbf, int* pbq, IterState* st,
+                        const IterState* gate) {
+    if (gate != nullptr && gate->stop) return;
+    const int lane = threadIdx.x & 31;
+    const int rl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (rl >= s.rows) return;
+    int better = 0;
+    if (lane == 0) {
+        const T f = fit[rl];
+        if (st != nullptr && !isfinite(f)) atomicMin(&st->nonfinite_row, s.row_begin + rl);
+        better = f < pbf[rl];
+        if (better) { pbf[rl] = f; pbq[rl] = q ? q[rl] : 0; }
+    }
+    better = __shfl_sync(0xffffffffu, better, 0);
+    if (better)
+        for (int d = lane; d < s.D; d += 32) pb[size_t(rl) * s.D + d] = x[size_t(rl) * s.D + d];
+}
+
+// Per local group: (pbest_f, global row) lexicographic min (runner.hpp:81-87 order).
+template <class T>
+__global__ void k_group_partial(StageShape s, const T* __restrict__ pbf, const int* __restrict__ pbq,
+                                T* part_f, int* part_row, int* part_q, const IterState* gate) {
+    if (gate != nullptr && gate->stop) return;
+    using A = Ar<T>;
+    const int g = s.row_begin / s.N + blockIdx.x;
+    const int l0 = max(g * s.N, s.row_begin) - s.row_begin;
+    const int l1 = min((g + 1) * s.N, s.row_begin + s.rows) - s.row_begin;
+    T bf = A::inf();
+    int br = INT_MAX;
+    for (int r = l0 + threadIdx.x; r < l1; r += blockDim.x) {
+        const T f = pbf[r];
+        if (f < bf) { bf = f; br = r; }
+    }
+    for (int off = 16; off; off >>= 1) {
+        const T of = __shfl_down_sync(0xffffffffu, bf, off);
+        const int orow = __shfl_down_sync(0xffffffffu, br, off);
+        if (of < bf || (of == bf && orow < br)) { bf = of; br = orow; }
+    }
+    __shared__ T wf[32];
+    __shared__ int wr[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) { wf[warp] = bf; wr[warp] = br; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < int(blockDim.x >> 5); ++w)
+            if (wf[w] < bf || (wf[w] == bf && wr[w] < br)) { bf = wf[w]; br = wr[w]; }
+        part_f[blockIdx.x] = bf;
+        part_row[blockIdx.x] = br == INT_MAX ? -1 : br;     // local row
+        part_q[blockIdx.x] = br == INT_MAX ? 0 : pbq[br];
+    }
+}
+
+int stage_pbest_partials(bool fp64, const StageShape& s, const void* x, const void* fit,
+                         const int* q, void* pb, void* pbf, int* pbq, IterState* stt,
+                         void* part_f, int* part_row, int* part_q, const IterState* gate,
+                         void* stream) {
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const unsigned grid = unsigned((s.rows * 32LL + 255) / 256);
+    const int n_groups = (s.row_begin + s.rows - 1) / s.N - s.row_begin / s.N + 1;
+    if (fp64) {
+        k_pbest<double><<<grid, 256, 0, st>>>(s, (const double*)x, (const double*)fit, q,
+                                              (double*)pb, (double*)pbf, pbq, stt, gate);
+        k_group_partial<double><<<n_groups, 256, 0, st>>>(s, (const double*)pbf, pbq,
+                                                          (double*)part_f, part_row, part_q, gate);
+    } else {
+        k_pbest<float><<<grid, 256, 0, st>>>(s, (const float*)x, (const float*)fit, q,
+                                             (float*)pb, (float*)pbf, pbq, stt, gate);
+        k_group_partial<float><<<n_groups, 256, 0, st>>>(s, (const float*)pbf, pbq,
+                                                         (float*)part_f, part_row, part_q, gate);
+    }
+    return int(cudaGetLastError());
+}
+
+// gbest for the local groups, then this device's tbest candidate.
+template <class T>
+__global__ void k_group_bests(StageShape s, const T* __restrict__ part_f,
+                              const int* __restrict__ part_row, const int* __restrict__ part_q,
+                              const T* __restrict__ pb, T* gbx, T* gbf, int* gbq,
+                              unsigned char* cand, const IterState* gate) {
+    if (gate != nullptr && gate->stop) return;
+    extern __shared__ int chg[];
+    const int g0 = s.row_begin / s.N;
+    const int ng = (s.row_begin + s.rows - 1) / s.N - g0 + 1;
+    for (int lg = threadIdx.x; lg < ng; lg += blockDim.x) {
+        const int g = g0 + lg;
+        if (part_row[lg] >= 0 && part_f[lg] < gbf[g]) {
+            gbf[g] = part_f[lg];
+            gbq[g] = part_q[lg];
+            chg[lg] = part_row[lg];
+        } else {
+            chg[lg] = -1;
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < ng * s.D; t += blockDim.x) {
+        const int lg = t / s.D, d = t - lg * s.D;
+        if (chg[lg] >= 0) gbx[size_t(g0 + lg) * s.D + d] = pb[size_t(chg[lg]) * s.D + d];
+    }
+    __shared__ int best_g;
+    if (threadIdx.x == 0) {
+        CandHdr h{__longlong_as_double(0x7ff0000000000000ll), 0, -1};
+        for (int lg = 0; lg < ng; ++lg) {
+            const double f = double(gbf[g0 + lg]);
+            if (f < h.f) { h.f = f; h.q = gbq[g0 + lg]; h.g = g0 + lg; }
+        }
+        *reinterpret_cast<CandHdr*>(cand) = h;
+        best_g = h.g;
+    }
+    __syncthreads();
+    T* cx = reinterpret_cast<T*>(cand + sizeof(CandHdr));
+    if (best_g >= 0)
+        for (int d = threadIdx.x; d < s.D; d += blockDim.x) cx[d] = gbx[size_t(best_g) * s.D + d];
+}
+
+int stage_group_bests(bool fp64, const StageShape& s, const void* part_f, const int* part_row,
+                      const int* part_q, const void* pb, void* gbx, void* gbf, int* gbq,
+                      void* cand, const IterState* gate, void* stream) {
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int ng = (s.row_begin + s.rows - 1) / s.N - s.row_begin / s.N + 1;
+    const size_t sm = size_t(ng) * 4;
+    if (fp64)
+        k_group_bests<double><<<1, 256, sm, st>>>(s, (const double*)part_f, part_row, part_q,
+                                                  (const double*)pb, (double*)gbx, (double*)gbf,
+                                                  gbq, (unsigned char*)cand, gate);
+    else
+        k_group_bests<float><<<1, 256, sm, st>>>(s, (const float*)part_f, part_row, part_q,
+                                                 (const float*)pb, (float*)gbx, (float*)gbf, gbq,
+                                                 (unsigned char*)cand, gate);
+    return int(cudaGetLastError());
+}
+
+// tbest over candidates (ascending group order, strict '<'), window + AT.
+template <class T>
+__global__ void k_finish(int D, const unsigned char* __restrict__ cands, int n_cand, size_t cstride,
+                         T* tbx, IterState* st, double* win, int tw, int auto_truncate,
+                         double delta, int k, double* trace) {
+    if (st->stop) return;
+    __shared__ int src;
+    if (threadIdx.x == 0) {
+        src = -1;
+        if (st->nonfinite_row != INT_MAX) {
+            st->status = 2;
+            st->stop = 1;
+        } else {
+            // candidates come from disjoint group ranges; scan in group order
+            int order[64];
+            const int nc = n_cand < 64 ? n_cand : 64;
+            for (int i = 0; i < nc; ++i) order[i] = i;
+            for (int i = 1; i < nc; ++i) {      // insertion sort by group
+                const int t = order[i];
+                const int gt = reinterpret_cast<const CandHdr*>(cands + t * cstride)->g;
+                int j = i - 1;
+                while (j >= 0 && reinterpret_cast<const CandHdr*>(cands + order[j] * cstride)->g > gt) {
+                    order[j + 1] = order[j];
+                    --j;
+                }
+                order[j + 1] = t;
+            }
+            for (int i = 0; i < nc; ++i) {
+                const CandHdr* h = reinterpret_cast<const CandHdr*>(cands + order[i] * cstride);
+                if (h->g >= 0 && h->f < st->tbest_f) {
+                    st->tbest_f = h->f;
+                    st->tbest_q = h->q;
+                    st->tbest_group = h->g;
+                    src = order[i];
+                }
+            }
+            if (trace) trace[k - 1] = st->tbest_f;
+            if (win != nullptr && tw > 0) {
+                const double tv = st->tbest_f;
+                if (st->win_len < tw) {
+                    win[(st->win_head + st->win_len) % tw] = tv;
+                    ++st->win_len;
+                } else {
+                    win[st->win_head] = tv;
+                    st->win_head = (st->win_head + 1) % tw;
+                }
+                if (auto_truncate && st->win_len >= tw) {
+                    double mean = 0.0;
+                    for (int i = 0; i < tw; ++i) mean = __dadd_rn(mean, win[(st->win_head + i) % tw]);
+                    mean = __ddiv_rn(mean, double(tw));
+                    double var = 0.0;
+                    for (int i = 0; i < tw; ++i) {
+                        const double dv = __dsub_rn(win[(st->win_head + i) % tw], mean);
+                        var = __dadd_rn(var, __dmul_rn(dv, dv));
+                    }
+                    var = __ddiv_rn(var, double(tw));
+                    if (__dsqrt_rn(var) < delta && st->tbest_q == 0) {
+                        st->truncated = 1;
+                        st->stop = 1;
+                    }
+                }
+            }
+        }
+        st->k_done = k;
+    }
+    __syncthreads();
+    if (src >= 0) {
+        const T* cx = reinterpret_cast<const T*>(cands + src * cstride + sizeof(CandHdr));
+        for (int d = threadIdx.x; d < D; d += blockDim.x) tbx[d] = cx[d];
+    }
+}
+
+int stage_finish(bool fp64, int D, const void* cands, int n_cand, void* tbx, IterState* stt,
+                 double* win, int tw, int auto_truncate, double delta, int k, int cap,
+                 double* trace, void* stream) {
+    (void)cap;
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t cs = cand_bytes(fp64, D);
+    if (fp64)
+        k_finish<double><<<1, 128, 0, st>>>(D, (const unsigned char*)cands, n_cand, cs, (double*)tbx,
+                                            stt, win, tw, auto_truncate, delta, k, trace);
+    else
+        k_finish<float><<<1, 128, 0, st>>>(D, (const unsigned char*)cands, n_cand, cs, (float*)tbx,
+                                           stt, win, tw, auto_truncate, delta, k, trace);
+    return int(cudaGetLastError());
+}
+
+} // namespace sepso

@@ -1,0 +1,374 @@
+// swarm_device.cuh -- device building blocks shared by the fused swarm kernel
+// (swarm_kernel.cu) and the HBM-resident stage kernels (stage_kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cmath>
+
+#include "geometry.cuh"
+#include "philox.cuh"
+#include "swarm_kernel.cuh"
+
+namespace sepso {
+
+// ---------------------------------------------------------------- arithmetic
+// FP64: no contraction, so every rounding happens where the reference's
+// -ffp-contract=off build rounds.  FP32: plain operators (FMA allowed).
+template <class T> struct Ar;
+template <> struct Ar<double> {
+    static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+    static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+    static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+    static __device__ __forceinline__ double inf() { return __longlong_as_double(0x7ff0000000000000ll); }
+};
+template <> struct Ar<float> {
+    static __device__ __forceinline__ float add(float a, float b) { return a + b; }
+    static __device__ __forceinline__ float sub(float a, float b) { return a - b; }
+    static __device__ __forceinline__ float mul(float a, float b) { return a * b; }
+    static __device__ __forceinline__ float inf() { return __int_as_float(0x7f800000); }
+};
+
+template <class T> __device__ __forceinline__ T clampT(T v, T lo, T hi) {   // std::clamp
+    return v < lo ? lo : (hi < v ? hi : v);
+}
+
+template <class T> struct Misc {
+    T tbf;
+    int tbq, tsrc_slot, stop, truncated, status, bad_row, bad_min, n_pair, n_cont;
+    int win_len, win_head, k_done, cont_cap;
+};
+
+// alpha * q^beta (geometry.hpp:240): exact repeated product for small integer
+// beta (std::pow is exact there), libm pow otherwise.
+__device__ __forceinline__ double penalty(double alpha, double beta, int beta_int, int q) {
+    double qp;
+    if (beta_int > 0) {
+        const double qd = double(q);
+        qp = qd;
+        for (int i = 1; i < beta_int; ++i) qp = __dmul_rn(qp, qd);
+    } else {
+        qp = pow(double(q), beta);
+    }
+    return __dmul_rn(alpha, qp);
+}
+
+// benchmarks.hpp:56-88 (+ Ackley extension)
+template <class T> __device__ T bench_eval(int kind, const T* p, int D);
+template <> inline __device__ double bench_eval<double>(int kind, const double* p, int D) {
+    using A = Ar<double>;
+    const double two_pi = 6.283185307179586;   // 2.0 * std::numbers::pi
+    switch (kind) {
+    case kSphere: {
+        double s = 0.0;
+        for (int i = 0; i < D; ++i) s = A::add(s, A::mul(p[i], p[i]));
+        return s;
+    }
+    case kRosenbrock: {
+        double s = 0.0;
+        for (int i = 0; i + 1 < D; ++i) {
+            const double a = A::sub(p[i + 1], A::mul(p[i], p[i]));
+            const double b = A::sub(1.0, p[i]);
+            s = A::add(s, A::add(A::mul(A::mul(100.0, a), a), A::mul(b, b)));
+        }
+        return s;
+    }
+    case kRastrigin: {
+        double s = 0.0;
+        for (int i = 0; i < D; ++i)
+            s = A::add(s, A::add(A::sub(A::mul(p[i], p[i]), A::mul(10.0, cos(A::mul(two_pi, p[i])))),
+                                 10.0));
+        return s;
+    }
+    case kGriewank: {
+        double sum = 0.0, prod = 1.0;
+        for (int i = 0; i < D; ++i) {
+            sum = A::add(sum, A::mul(p[i], p[i]));
+            prod = A::mul(prod, cos(__ddiv_rn(p[i], __dsqrt_rn(double(i + 1)))));
+        }
+        return A::sub(A::add(1.0, __ddiv_rn(sum, 4000.0)), prod);
+    }
+    case kAckley: {
+        double s1 = 0.0, s2 = 0.0;
+        for (int i = 0; i < D; ++i) {
+            s1 = A::add(s1, A::mul(p[i], p[i]));
+            s2 = A::add(s2, cos(A::mul(two_pi, p[i])));
+        }
+        const double dd = double(D);
+        return -20.0 * exp(-0.2 * sqrt(s1 / dd)) - exp(s2 / dd) + 20.0 + 2.718281828459045;
+    }
+    }
+    return __longlong_as_double(0x7ff8000000000000ll);
+}
+template <> inline __device__ float bench_eval<float>(int kind, const float* p, int D) {
+    const float two_pi = 6.2831853f;
+    switch (kind) {
+    case kSphere: {
+        float s = 0.f;
+        for (int i = 0; i < D; ++i) s += p[i] * p[i];
+        return s;
+    }
+    case kRosenbrock: {
+        float s = 0.f;
+        for (int i = 0; i + 1 < D; ++i) {
+            const float a = p[i + 1] - p[i] * p[i];
+            const float b = 1.f - p[i];
+            s += 100.f * a * a + b * b;
+        }
+        return s;
+    }
+    case kRastrigin: {
+        float s = 0.f;
+        for (int i = 0; i < D; ++i) s += p[i] * p[i] - 10.f * cosf(two_pi * p[i]) + 10.f;
+        return s;
+    }
+    case kGriewank: {
+        float sum = 0.f, prod = 1.f;
+        for (int i = 0; i < D; ++i) {
+            sum += p[i] * p[i];
+            prod *= cosf(p[i] * rsqrtf(float(i + 1)));
+        }
+        return 1.f + sum / 4000.f - prod;
+    }
+    case kAckley: {
+        float s1 = 0.f, s2 = 0.f;
+        for (int i = 0; i < D; ++i) {
+            s1 += p[i] * p[i];
+            s2 += cosf(two_pi * p[i]);
+        }
+        const float dd = float(D);
+        return -20.f * expf(-0.2f * sqrtf(s1 / dd)) - expf(s2 / dd) + 20.f + 2.7182817f;
+    }
+    }
+    return __int_as_float(0x7fc00000);
+}
+
+// ------------------------------------------------------------ swarm context
+template <class T> struct Ctx {
+    // shape
+    int G, N, D, W, S, R, P, row0, LG, O, C, crank;
+    // shared arrays
+    T *x, *v, *pb, *pbf, *fit, *seglen, *coef, *lo, *hi, *hyp, *gbx, *gbf, *tbx, *pf, *px, *allf;
+    int *pbq, *q, *imp, *gbq, *chg, *prow, *pq, *allrow, *allq, *ooff;
+    T *obb, *vert, *edge;
+    double* win;
+    uint32_t* list;
+    Misc<T>* m;
+    // path constants
+    T sx, sy, tx, ty, margin;
+};
+
+// chain point j of start -> w_1..w_W -> target for local particle pl (geometry.hpp:157-165)
+template <class T>
+__device__ __forceinline__ void chain_pt(const Ctx<T>& c, int pl, int j, T& px, T& py) {
+    if (j == 0) { px = c.sx; py = c.sy; }
+    else if (j == c.W + 1) { px = c.tx; py = c.ty; }
+    else { px = c.x[pl * c.D + j - 1]; py = c.x[pl * c.D + c.W + j - 1]; }
+}
+
+template <class T> __device__ __forceinline__ T seg_length(T dx, T dy);
+template <> __device__ __forceinline__ double seg_length<double>(double dx, double dy) {
+    return hypot_glibc(dx, dy);                       // std::hypot, geometry.hpp:228
+}
+template <> __device__ __forceinline__ float seg_length<float>(float dx, float dy) {
+    return sqrtf(fmaf(dx, dx, dy * dy));
+}
+
+// Segment (item) x obstacle edges: number of intersecting (segment, edge) pairs.
+template <class T>
+__device__ int pair_count(const Ctx<T>& c, int item, int o);
+
+template <>
+inline __device__ int pair_count<double>(const Ctx<double>& c, int item, int o) {
+    const int pl = item / c.S, s = item - pl * c.S;
+    double a1x, a1y, a2x, a2y;
+    chain_pt(c, pl, s, a1x, a1y);
+    chain_pt(c, pl, s + 1, a2x, a2y);
+    const int v0 = c.ooff[o], v1 = c.ooff[o + 1];
+    int cnt = 0;
+    for (int i = v0; i < v1; ++i) {
+        const int j = (i + 1 == v1) ? v0 : i + 1;
+        cnt += segments_intersect_ref(a1x, a1y, a2x, a2y, c.vert[2 * i], c.vert[2 * i + 1],
+                                      c.vert[2 * j], c.vert[2 * j + 1]);
+    }
+    return cnt;
+}
+
+template <>
+inline __device__ int pair_count<float>(const Ctx<float>& c, int item, int o) {
+    const int pl = item / c.S, s = item - pl * c.S;
+    float a1x, a1y, a2x, a2y;
+    chain_pt(c, pl, s, a1x, a1y);
+    chain_pt(c, pl, s + 1, a2x, a2y);
+    const float dx = a2x - a1x, dy = a2y - a1y;
+    // Error bound for every cross product of this (segment, obstacle) pair:
+    // all operand components are bounded by the extent L of the union box.
+    const float* bb = c.obb + 4 * o;
+    const float ux = fmaxf(fmaxf(a1x, a2x), bb[2]) - fminf(fminf(a1x, a2x), bb[0]);
+    const float uy = fmaxf(fmaxf(a1y, a2y), bb[3]) - fminf(fminf(a1y, a2y), bb[1]);
+    const float L = fmaxf(ux, uy);
+    const float B = 1.5e-6f * L * L + 2e-12f;
+    const int v0 = c.ooff[o], v1 = c.ooff[o + 1];
+    int cnt = 0;
+    for (int i = v0; i < v1; ++i) {
+        const float4 e = reinterpret_cast<const float4*>(c.edge)[i];
+        int r = fast_pair(a1x, a1y, dx, dy, e.x, e.y, e.z, e.w, B);
+        if (r < 0) {
+            const int j = (i + 1 == v1) ? v0 : i + 1;
+            r = segments_intersect_ref(a1x, a1y, a2x, a2y, c.vert[2 * i], c.vert[2 * i + 1],
+                                       c.vert[2 * j], c.vert[2 * j + 1]);
+        }
+        cnt += r;
+    }
+    return cnt;
+}
+
+// First waypoint strictly inside obstacle o (geometry.hpp:217-218), FP64 always.
+template <class T>
+__device__ int contain_count(const Ctx<T>& c, int pl, int o) {
+    const double px = double(c.x[pl * c.D]), py = double(c.x[pl * c.D + c.W]);
+    const int v0 = c.ooff[o], n = c.ooff[o + 1] - v0;
+    const T* vb = c.vert + 2 * v0;
+    return point_strictly_inside_ref(
+        px, py, n, [vb](int i) { return double(vb[2 * i]); },
+        [vb](int i) { return double(vb[2 * i + 1]); });
+}
+
+template <class T>
+__device__ __forceinline__ bool box_overlap(T lx, T ly, T hx, T hy, const T* bb, T m) {
+    return lx <= bb[2] + m && bb[0] <= hx + m && ly <= bb[3] + m && bb[1] <= hy + m;
+}
+
+
+// Stage one world record (double) into shared memory as T: vertices, edge
+// records (b1, b2 - b1) and obstacle boxes (geometry.hpp:167-177); sets the
+// endpoints, the cull margin and the path search box (geometry.hpp:252-255).
+template <class T>
+__device__ void load_world(Ctx<T>& c, const unsigned char* wrec, int off_offsets, int off_verts) {
+    using A = Ar<T>;
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const WorldHeader* wh = reinterpret_cast<const WorldHeader*>(wrec);
+    const uint32_t* woff = reinterpret_cast<const uint32_t*>(wrec + off_offsets);
+    const double* wv = reinterpret_cast<const double*>(wrec + off_verts);
+    c.O = int(wh->n_obs);
+    const int nv = int(wh->n_verts);
+    c.sx = T(wh->sx); c.sy = T(wh->sy); c.tx = T(wh->tx); c.ty = T(wh->ty);
+    const T width = T(wh->width), height = T(wh->height);
+    // FP32 engine: the world is the FP32-rounded world; the cull margin is
+    // conservative (never drops a pair the reference's 1e-9 cull keeps).
+    c.margin = sizeof(T) == 8 ? T(1e-9) : T(1e-6) * (T(1) + (width > height ? width : height));
+    for (int d = tid; d < c.D; d += nthr) {
+        c.lo[d] = T(0);
+        c.hi[d] = d < c.W ? width : height;                  // geometry.hpp:252-255
+    }
+    for (int i = tid; i <= c.O; i += nthr) c.ooff[i] = int(woff[i]);
+    for (int i = tid; i < 2 * nv; i += nthr) c.vert[i] = T(wv[i]);
+    __syncthreads();
+    for (int o = tid; o < c.O; o += nthr) {                  // bbox_of, geometry.hpp:167-177
+        const int v0 = c.ooff[o], v1 = c.ooff[o + 1];
+        T bx0 = c.vert[2 * v0], by0 = c.vert[2 * v0 + 1], bx1 = bx0, by1 = by0;
+        for (int i = v0; i < v1; ++i) {
+            const T vx = c.vert[2 * i], vy = c.vert[2 * i + 1];
+            bx0 = vx < bx0 ? vx : bx0;
+            by0 = vy < by0 ? vy : by0;
+            bx1 = bx1 < vx ? vx : bx1;
+            by1 = by1 < vy ? vy : by1;
+            const int j = (i + 1 == v1) ? v0 : i + 1;
+            T* e = c.edge + 4 * i;
+            e[0] = vx;
+            e[1] = vy;
+            e[2] = A::sub(c.vert[2 * j], vx);
+            e[3] = A::sub(c.vert[2 * j + 1], vy);
+        }
+        T* bb = c.obb + 4 * o;
+        bb[0] = bx0; bb[1] = by0; bb[2] = bx1; bb[3] = by1;
+    }
+}
+
+// Path fitness of the CTA's particles into c.fit (before pbest logic).
+template <class T>
+__device__ void path_fitness_phase(const SwarmParams& p, Ctx<T>& c) {
+    const int tid = threadIdx.x, lane = tid & 31, nthr = blockDim.x;
+    const int items = c.P * c.S;
+    const int pair_cap = p.entry_cap - c.m->cont_cap;
+    uint32_t* clist = c.list + pair_cap;
+    // A1: per (particle, segment) item: length, obstacle bbox cull -> work list
+    for (int base = tid - lane; base < items; base += nthr) {
+        const int it = base + lane;
+        const bool act = it < items;
+        int pl = 0, s = 0;
+        T a1x = 0, a1y = 0, a2x = 0, a2y = 0;
+        if (act) {
+            pl = it / c.S;
+            s = it - pl * c.S;
+            chain_pt(c, pl, s, a1x, a1y);
+            chain_pt(c, pl, s + 1, a2x, a2y);
+            c.seglen[it] = seg_length<T>(Ar<T>::sub(a2x, a1x), Ar<T>::sub(a2y, a1y));
+        }
+        const T lx = a1x < a2x ? a1x : a2x, hx = a1x < a2x ? a2x : a1x;
+        const T ly = a1y < a2y ? a1y : a2y, hy = a1y < a2y ? a2y : a1y;
+        for (int o = 0; o < c.O; ++o) {
+            const bool ov = act && box_overlap(lx, ly, hx, hy, c.obb + 4 * o, c.margin);
+            const unsigned mask = __ballot_sync(0xffffffffu, ov);
+            if (!mask) continue;
+            int basei = 0;
+            if (lane == __ffs(mask) - 1) basei = atomicAdd(&c.m->n_pair, __popc(mask));
+            basei = __shfl_sync(0xffffffffu, basei, __ffs(mask) - 1);
+            if (ov) {
+                const int idx = basei + __popc(mask & ((1u << lane) - 1u));
+                if (idx < pair_cap) c.list[idx] = uint32_t(it) * uint32_t(c.O) + uint32_t(o);
+                else {   // list overflow: evaluate in place (correct, just divergent)
+                    const int n = pair_count(c, it, o);
+                    if (n) atomicAdd(&c.q[pl], n);
+                }
+            }
+        }
+        // containment candidates for the first waypoint (s == 0 -> endpoint b)
+        if (act && s == 0) {
+            const T wx = a2x, wy = a2y;
+            for (int o = 0; o < c.O; ++o) {
+                const T* bb = c.obb + 4 * o;
+                if (wx >= bb[0] - c.margin && wx <= bb[2] + c.margin && wy >= bb[1] - c.margin &&
+                    wy <= bb[3] + c.margin) {
+                    const int idx = atomicAdd(&c.m->n_cont, 1);
+                    if (idx < c.m->cont_cap) clist[idx] = uint32_t(pl) * uint32_t(c.O) + uint32_t(o);
+                    else if (contain_count(c, pl, o)) atomicAdd(&c.q[pl], 1);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    // A2: dense evaluation of the compacted work list
+    const int np = min(c.m->n_pair, pair_cap), nc = min(c.m->n_cont, c.m->cont_cap);
+    for (int e = tid; e < np + nc; e += nthr) {
+        if (e < np) {
+            const uint32_t w = c.list[e];
+            const int it = int(w / uint32_t(c.O)), o = int(w - uint32_t(it) * uint32_t(c.O));
+            const int n = pair_count(c, it, o);
+            if (n) atomicAdd(&c.q[it / c.S], n);
+        } else {
+            const uint32_t w = clist[e - np];
+            const int pl = int(w / uint32_t(c.O)), o = int(w - uint32_t(pl) * uint32_t(c.O));
+            if (contain_count(c, pl, o)) atomicAdd(&c.q[pl], 1);
+        }
+    }
+    __syncthreads();
+    if (tid == 0) { c.m->n_pair = 0; c.m->n_cont = 0; }
+    // A3: fitness = sum of segment lengths (in chain order) + alpha * Q^beta
+    for (int pl = tid; pl < c.P; pl += nthr) {
+        T len = T(0);
+        for (int s = 0; s < c.S; ++s) len = Ar<T>::add(len, c.seglen[pl * c.S + s]);
+        const double pen = penalty(p.alpha, p.beta, p.beta_int, c.q[pl]);
+        c.fit[pl] = Ar<T>::add(len, T(pen));
+    }
+}
+
+template <class T>
+__device__ void bench_fitness_phase(int kind, Ctx<T>& c) {
+    for (int pl = threadIdx.x; pl < c.P; pl += blockDim.x) {
+        c.fit[pl] = bench_eval<T>(kind, c.x + pl * c.D, c.D);
+        c.q[pl] = 0;
+    }
+}
+
+} // namespace sepso

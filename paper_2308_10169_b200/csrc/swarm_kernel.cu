@@ -1,0 +1,360 @@
+// swarm_kernel.cu -- the fused SEPSO swarm kernel (sm_100a).
+//
+// See swarm_kernel.cuh for the execution model.  Reference citations are
+// relative to proj/include/swarmforge/ in the reference tree.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include "swarm_device.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace sepso {
+
+// ------------------------------------------------------------------ kernel
+template <class T, bool PATH>
+__global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ SwarmParams p,
+                                                        int problem) {
+    using A = Ar<T>;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ __align__(16) unsigned char smem[];
+    const SmemLayout L = smem_layout(p, sizeof(T), PATH);
+    const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    const int swarm = blockIdx.x / p.C;
+
+    Ctx<T> c;
+    c.G = p.G; c.N = p.N; c.D = p.D; c.W = p.D / 2; c.S = c.W + 1; c.R = p.G * p.N;
+    c.C = p.C; c.crank = int(cluster.block_rank());
+    c.row0 = c.crank * p.rows_per_cta;
+    const int row1 = min(c.R, c.row0 + p.rows_per_cta);
+    c.P = max(0, row1 - c.row0);
+    const int gfirst = c.row0 / c.N;
+    c.LG = c.P > 0 ? (row1 - 1) / c.N - gfirst + 1 : 0;
+    auto S8 = [&](size_t off) { return smem + off; };
+    c.x = (T*)S8(L.x); c.v = (T*)S8(L.v); c.pb = (T*)S8(L.pb); c.pbf = (T*)S8(L.pbf);
+    c.pbq = (int*)S8(L.pbq); c.q = (int*)S8(L.q); c.fit = (T*)S8(L.fit); c.imp = (int*)S8(L.imp);
+    c.seglen = (T*)S8(L.seglen); c.coef = (T*)S8(L.coef); c.lo = (T*)S8(L.lo); c.hi = (T*)S8(L.hi);
+    c.hyp = (T*)S8(L.hyp); c.gbx = (T*)S8(L.gbx); c.gbf = (T*)S8(L.gbf); c.gbq = (int*)S8(L.gbq);
+    c.chg = (int*)S8(L.chg); c.tbx = (T*)S8(L.tbx); c.win = (double*)S8(L.win);
+    c.pf = (T*)S8(L.pf); c.prow = (int*)S8(L.prow); c.pq = (int*)S8(L.pq); c.px = (T*)S8(L.px);
+    c.allf = (T*)S8(L.allf); c.allrow = (int*)S8(L.allrow); c.allq = (int*)S8(L.allq);
+    c.obb = (T*)S8(L.obb); c.ooff = (int*)S8(L.ooff); c.vert = (T*)S8(L.vert);
+    c.edge = (T*)S8(L.edge); c.list = (uint32_t*)S8(L.list); c.m = (Misc<T>*)S8(L.misc);
+    int* allbad = c.allrow + c.C * p.max_local_groups;
+    const int LGM = p.max_local_groups;
+    const uint64_t seed = p.seeds[swarm];
+    const int G = c.G, N = c.N, D = c.D, R = c.R;
+
+    // ---------------------------------------------------------- constants
+    const double* hyp_src = p.hypers + size_t(swarm) * size_t(p.hypers_stride);
+    for (int i = tid; i < G * 6; i += nthr) c.hyp[i] = T(hyp_src[i]);
+    c.O = 0;
+    if (PATH) {
+        load_world(c, p.worlds + size_t(swarm) * size_t(p.world_stride), p.off_offsets, p.off_verts);
+    } else {
+        for (int d = tid; d < D; d += nthr) { c.lo[d] = T(p.lo[d]); c.hi[d] = T(p.hi[d]); }
+    }
+    if (tid == 0) {
+        Misc<T>* m = c.m;
+        m->tbf = A::inf(); m->tbq = 0; m->tsrc_slot = -1; m->stop = 0; m->truncated = 0;
+        m->status = 0; m->bad_row = INT_MAX; m->bad_min = INT_MAX; m->n_pair = 0; m->n_cont = 0;
+        m->k_done = 0;
+        m->cont_cap = PATH ? min(p.entry_cap / 4, c.P * max(c.O, 1)) : 0;
+        const int wl = p.carry ? p.win_len[swarm] : 0;
+        m->win_len = wl < p.tw ? wl : p.tw;
+        m->win_head = 0;
+    }
+    if (p.carry)
+        for (int i = tid; i < p.tw; i += nthr) c.win[i] = p.win_vals[size_t(swarm) * p.tw + i];
+    for (int g = tid; g < G; g += nthr) { c.gbf[g] = A::inf(); c.gbq[g] = 0; c.chg[g] = -1; }
+    for (int pl = tid; pl < c.P; pl += nthr) { c.pbf[pl] = A::inf(); c.pbq[pl] = 0; c.q[pl] = 0; }
+    __syncthreads();
+
+    // ------------------------------------------------------- initialisation
+    // swarm.hpp:94-132 / planner.hpp:77-133: x draws [0, R*D), v draws [R*D, 2*R*D)
+    {
+        const bool warm_on = p.has_prev != nullptr && p.has_prev[swarm] != 0;
+        const double* prev = warm_on ? p.prev + size_t(swarm) * D : nullptr;
+        const T rad = T(p.pi_radius);
+        for (int e = tid; e < c.P * D; e += nthr) {
+            const int pl = e / D, d = e - pl * D;
+            const int row = c.row0 + pl, g = row / N, n = row - g * N;
+            const uint64_t ix = uint64_t(row) * uint64_t(D) + uint64_t(d);
+            const T ux = unit_from_word<T>(philox_word(seed, ix));
+            const T lo = c.lo[d], hi = c.hi[d];
+            T xv;
+            if (warm_on && n < p.warm) {
+                const T ctr = T(prev[d]);            // waypoint d % W, x- or y-block
+                const T l = A::sub(ctr, rad) > lo ? A::sub(ctr, rad) : lo;   // std::max(lo, c - r)
+                const T h = hi < A::add(ctr, rad) ? hi : A::add(ctr, rad);  // std::min(hi, c + r)
+                xv = A::add(l, A::mul(ux, A::sub(h, l)));
+            } else {
+                xv = A::add(lo, A::mul(ux, A::sub(hi, lo)));
+            }
+            const T uv = unit_from_word<T>(philox_word(seed, uint64_t(R) * D + ix));
+            const T vmax = A::mul(c.hyp[g * 6 + 5], A::sub(hi, lo));
+            const T vlo = -vmax;
+            c.x[e] = xv;
+            c.pb[e] = xv;
+            c.v[e] = A::add(vlo, A::mul(uv, A::sub(vmax, vlo)));
+        }
+    }
+    __syncthreads();
+
+    // ------------------------------------------------------------ iterations
+    int k = 1;
+    for (; k <= p.cap; ++k) {
+        const int buf = k & 1;
+        // fitness (geometry.hpp:262-267 / benchmarks.hpp:45-53)
+        if (PATH) path_fitness_phase(p, c);
+        else bench_fitness_phase(problem, c);
+        // pbest (runner.hpp:73-80), non-finite detection (runner.hpp:56-61)
+        for (int pl = tid; pl < c.P; pl += nthr) {
+            const T f = c.fit[pl];
+            if (!isfinite(f)) atomicMin(&c.m->bad_row, c.row0 + pl);
+            const bool better = f < c.pbf[pl];
+            if (better) { c.pbf[pl] = f; c.pbq[pl] = c.q[pl]; }
+            c.imp[pl] = better;
+            if (PATH) c.q[pl] = 0;
+        }
+        __syncthreads();
+        for (int e = tid; e < c.P * D; e += nthr)
+            if (c.imp[e / D]) c.pb[e] = c.x[e];
+        __syncthreads();
+        // per-CTA group partials: (pbest_f, row) lexicographic min, one warp per group
+        for (int lg = warp; lg < c.LG; lg += nthr >> 5) {
+            const int g = gfirst + lg;
+            const int l0 = max(c.row0, g * N) - c.row0, l1 = min(row1, (g + 1) * N) - c.row0;
+            T bf = A::inf();
+            int br = INT_MAX, bq = 0;
+            for (int pl = l0 + lane; pl < l1; pl += 32) {
+                const T f = c.pbf[pl];
+                if (f < bf) { bf = f; br = pl; bq = c.pbq[pl]; }   // lanes scan ascending
+            }
+            for (int off = 16; off; off >>= 1) {
+                const T of = __shfl_down_sync(0xffffffffu, bf, off);
+                const int orow = __shfl_down_sync(0xffffffffu, br, off);
+                const int oq = __shfl_down_sync(0xffffffffu, bq, off);
+                if (of < bf || (of == bf && orow < br)) { bf = of; br = orow; bq = oq; }
+            }
+            br = __shfl_sync(0xffffffffu, br, 0);
+            if (lane == 0) {
+                c.pf[buf * LGM + lg] = bf;
+                c.prow[buf * LGM + lg] = br == INT_MAX ? INT_MAX : br + c.row0;
+                c.pq[buf * LGM + lg] = bq;
+            }
+            if (br != INT_MAX)
+                for (int d = lane; d < D; d += 32) c.px[(buf * LGM + lg) * D + d] = c.pb[br * D + d];
+        }
+        cluster.sync();   // partials of every CTA visible cluster-wide
+
+        // gather partials (one DSMEM round trip, all threads in parallel)
+        for (int t = tid; t < c.C * LGM + c.C; t += nthr) {
+            if (t < c.C * LGM) {
+                const int cc = t / LGM, lg = t - cc * LGM;
+                const T* rpf = cluster.map_shared_rank(c.pf, cc);
+                const int* rrow = cluster.map_shared_rank(c.prow, cc);
+                const int* rq = cluster.map_shared_rank(c.pq, cc);
+                c.allf[t] = rpf[buf * LGM + lg];
+                c.allrow[t] = rrow[buf * LGM + lg];
+                c.allq[t] = rq[buf * LGM + lg];
+            } else {
+                const int cc = t - c.C * LGM;
+                const Misc<T>* rm = cluster.map_shared_rank(c.m, cc);
+                allbad[cc] = rm->bad_row;
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            Misc<T>* m = c.m;
+            int bad = INT_MAX;
+            for (int cc = 0; cc < c.C; ++cc) bad = min(bad, allbad[cc]);
+            if (bad != INT_MAX) {
+                m->status = 2; m->bad_min = bad; m->stop = 1;
+            } else {
+                // gbest: scan n ascending, strict '<' vs the incumbent (runner.hpp:81-87)
+                const int Rc = p.rows_per_cta;
+                for (int g = 0; g < G; ++g) {
+                    const int cf = (g * N) / Rc, cl = ((g + 1) * N - 1) / Rc;
+                    T bf = A::inf();
+                    int bslot = -1, bq = 0;
+                    for (int cc = cf; cc <= cl; ++cc) {
+                        const int lg = g - (cc * Rc) / N;
+                        const int slot = cc * LGM + lg;
+                        if (c.allf[slot] < bf) { bf = c.allf[slot]; bslot = slot; bq = c.allq[slot]; }
+                    }
+                    if (bf < c.gbf[g]) { c.gbf[g] = bf; c.gbq[g] = bq; c.chg[g] = bslot; }
+                    else c.chg[g] = -1;
+                }
+                // tbest: scan g ascending, strict '<' (runner.hpp:88-91)
+                int tg = -1;
+                for (int g = 0; g < G; ++g)
+                    if (c.gbf[g] < m->tbf) { m->tbf = c.gbf[g]; m->tbq = c.gbq[g]; tg = g; }
+                m->tsrc_slot = tg >= 0 ? tg : -1;
+                if (c.crank == 0) p.trace[size_t(swarm) * p.cap + (k - 1)] = double(m->tbf);
+                // window push + trim to tw (planner.hpp:179-180)
+                const double tv = double(m->tbf);
+                if (p.tw <= 0) {
+                } else if (m->win_len < p.tw) {
+                    c.win[(m->win_head + m->win_len) % p.tw] = tv;
+                    ++m->win_len;
+                } else {
+                    c.win[m->win_head] = tv;
+                    m->win_head = (m->win_head + 1) % p.tw;
+                }
+                // auto truncation (planner.hpp:181-187, 138-149), Q(tbest) tracked
+                if (p.auto_truncate && m->win_len >= p.tw) {
+                    double mean = 0.0;
+                    for (int i = 0; i < p.tw; ++i) mean = __dadd_rn(mean, c.win[(m->win_head + i) % p.tw]);
+                    mean = __ddiv_rn(mean, double(p.tw));
+                    double var = 0.0;
+                    for (int i = 0; i < p.tw; ++i) {
+                        const double dv = __dsub_rn(c.win[(m->win_head + i) % p.tw], mean);
+                        var = __dadd_rn(var, __dmul_rn(dv, dv));
+                    }
+                    var = __ddiv_rn(var, double(p.tw));
+                    if (__dsqrt_rn(var) < p.delta && m->tbq == 0) { m->truncated = 1; m->stop = 1; }
+                }
+            }
+            m->k_done = k;
+        }
+        __syncthreads();
+        if (c.m->status) break;
+        // copy improved group bests (and the new tbest) from their owners' partials
+        {
+            const int tg = c.m->tsrc_slot;
+            for (int t = tid; t < G * D; t += nthr) {
+                const int g = t / D, d = t - g * D;
+                const int slot = c.chg[g];
+                if (slot >= 0) {
+                    const int cc = slot / LGM, lg = slot - cc * LGM;
+                    const T* rpx = cluster.map_shared_rank(c.px, cc);
+                    const T val = rpx[(buf * LGM + lg) * D + d];
+                    c.gbx[g * D + d] = val;
+                    if (g == tg) c.tbx[d] = val;
+                }
+            }
+        }
+        __syncthreads();
+        if (c.m->stop) break;
+        if (k == p.cap) break;        // plan_frame: no step after the last iteration
+        // --------------------------------------------------- step k (swarm.hpp:138-174)
+        const uint64_t base = 2ull * uint64_t(R) * uint64_t(D) + uint64_t(k - 1) * 3ull * uint64_t(R);
+        for (int t = tid; t < 3 * c.P; t += nthr) {     // draw_step_randoms (swarm.hpp:59-70)
+            const int j = t / c.P, pl = t - j * c.P;
+            const int row = c.row0 + pl, g = row / N;
+            const T u = unit_from_word<T>(philox_word(seed, base + uint64_t(j) * R + row));
+            c.coef[j * c.P + pl] = A::mul(c.hyp[g * 6 + j], u);   // a_j = c_j * r_j
+        }
+        __syncthreads();
+        {
+            const T frac = T(double(k) / double(p.cap));           // inertia_at (swarm.hpp:81-84)
+            for (int e = tid; e < c.P * D; e += nthr) {
+                const int pl = e / D, d = e - pl * D;
+                const int g = (c.row0 + pl) / N;
+                const T* h = c.hyp + g * 6;
+                const T w = A::sub(h[3], A::mul(A::sub(h[3], h[4]), frac));
+                const T lo = c.lo[d], hi = c.hi[d];
+                const T vmax = A::mul(h[5], A::sub(hi, lo));
+                const T xv = c.x[e];
+                T nv = A::add(A::add(A::add(A::mul(w, c.v[e]), A::mul(c.coef[pl], A::sub(c.pb[e], xv))),
+                                     A::mul(c.coef[c.P + pl], A::sub(c.gbx[g * D + d], xv))),
+                              A::mul(c.coef[2 * c.P + pl], A::sub(c.tbx[d], xv)));
+                nv = clampT(nv, T(-vmax), vmax);
+                c.v[e] = nv;
+                c.x[e] = clampT(A::add(xv, nv), lo, hi);
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---------------------------------------------------------------- results
+    if (c.crank == 0 && tid == 0) {
+        const Misc<T>* m = c.m;
+        SwarmOut o{};
+        o.status = uint32_t(m->status);
+        o.iterations = uint32_t(m->k_done);
+        o.truncated = uint32_t(m->truncated);
+        o.window_len = uint32_t(m->win_len);
+        if (m->status == 2) {
+            o.bad_g = uint32_t(m->bad_min / N);
+            o.bad_n = uint32_t(m->bad_min % N);
+            o.bad_k = uint32_t(m->k_done);
+        } else {
+            o.fitness = double(m->tbf);
+            o.q = uint32_t(m->tbq);
+            if (PATH) {   // record length = path_length(best) in FP64 (planner.hpp:194)
+                double total = 0.0;
+                double px = double(c.sx), py = double(c.sy);
+                for (int j = 1; j <= c.W + 1; ++j) {
+                    const double nx = j <= c.W ? double(c.tbx[j - 1]) : double(c.tx);
+                    const double ny = j <= c.W ? double(c.tbx[c.W + j - 1]) : double(c.ty);
+                    total = __dadd_rn(total, hypot_glibc(__dsub_rn(nx, px), __dsub_rn(ny, py)));
+                    px = nx; py = ny;
+                }
+                o.length = total;
+            }
+        }
+        p.out[swarm] = o;
+    }
+    if (c.crank == 0) {
+        for (int d = tid; d < D; d += nthr) p.best_x[size_t(swarm) * D + d] = double(c.tbx[d]);
+        if (p.carry)
+            for (int i = tid; i < c.m->win_len; i += nthr)
+                p.win_vals[size_t(swarm) * p.tw + i] = c.win[(c.m->win_head + i) % p.tw];
+        if (tid == 0 && p.carry) p.win_len[swarm] = c.m->win_len;
+    }
+    cluster.sync();   // no CTA leaves while a peer may still read its shared memory
+}
+
+// ------------------------------------------------------------------ launcher
+template <class T, bool PATH>
+static int launch_t(const SwarmParams& p, int problem, cudaStream_t st, size_t* smem_out) {
+    const SmemLayout L = smem_layout(p, sizeof(T), PATH);
+    if (smem_out) *smem_out = L.total;
+    auto kern = swarm_kernel<T, PATH>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(L.total));
+    if (e != cudaSuccess) return int(e);
+    if (p.C > 8) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return int(e);
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(p.n_swarms * p.C));
+    cfg.blockDim = dim3(unsigned(p.nthreads));
+    cfg.dynamicSmemBytes = L.total;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(p.C);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, p, problem);
+    return int(e);
+}
+
+int launch_swarms(const SwarmParams& p, int problem, bool fp64, void* stream, size_t* smem) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const bool path = problem == kPath;
+    if (fp64) return path ? launch_t<double, true>(p, problem, st, smem)
+                          : launch_t<double, false>(p, problem, st, smem);
+    return path ? launch_t<float, true>(p, problem, st, smem)
+                : launch_t<float, false>(p, problem, st, smem);
+}
+
+int swarm_smem_bytes(const SwarmParams& p, int problem, bool fp64, size_t* bytes) {
+    *bytes = smem_layout(p, fp64 ? 8 : 4, problem == kPath).total;
+    return 0;
+}
+
+int max_smem_per_block() {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return v;
+}
+
+} // namespace sepso

@@ -1,0 +1,145 @@
+// swarm_kernel.cuh -- shared declarations of the fused swarm kernel.
+//
+// One thread-block CLUSTER runs one whole swarm (a planning frame, a DTPSO run
+// or one HSEF inner run) from initialisation to its last iteration with the
+// swarm state resident in shared memory.  CTA c of the cluster owns the
+// contiguous particle rows [c*Rc, min(G*N, (c+1)*Rc)) of the reference's
+// row-major (g, n) order (swarm.hpp:18-49).  Per iteration:
+//   fitness (+ Q)           geometry.hpp:196-241 / benchmarks.hpp:56-88
+//   pbest + group partials  runner.hpp:68-80     (per CTA)
+//   cluster barrier, DSMEM gather of partials, gbest/tbest    runner.hpp:81-91
+//   window push + AT test   planner.hpp:179-187, 138-149
+//   Philox draws + update   swarm.hpp:138-174
+// A grid of n_swarms clusters batches independent swarms (HSEF candidates,
+// planning queries, benchmark trials) into one launch.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+namespace sepso {
+
+enum ProblemKind : int {
+    kPath = 0, kSphere = 1, kRosenbrock = 2, kRastrigin = 3, kGriewank = 4, kAckley = 5
+};
+
+// Device world record (one per scene), built by the host from sf_world.
+//   [0, 64)   header: width, height, start xy, target xy (double), n_obs, n_verts
+//   [64, ..)  uint32 vertex offsets[max_obs + 1]
+//   then      double verts[2 * max_verts]           (8-byte aligned)
+//   then      double vel[2 * max_obs]               (dynamic obstacles; world stepping)
+struct WorldHeader {
+    double width, height, sx, sy, tx, ty;
+    uint32_t n_obs, n_verts;
+    double svx, svy, tvx, tvy;   // endpoint velocities (world stepping only)
+};
+static_assert(sizeof(WorldHeader) == 88, "world header layout");
+
+struct WorldLayout {
+    int max_obs, max_verts;
+    size_t off_offsets, off_verts, off_vel, stride;
+};
+
+inline WorldLayout world_layout(int max_obs, int max_verts) {
+    WorldLayout w{max_obs, max_verts, 0, 0, 0, 0};
+    w.off_offsets = 96;
+    w.off_verts = (w.off_offsets + 4 * size_t(max_obs + 1) + 7) & ~size_t(7);
+    w.off_vel = w.off_verts + 16 * size_t(max_verts);
+    w.stride = (w.off_vel + 16 * size_t(max_obs) + 15) & ~size_t(15);
+    return w;
+}
+
+struct SwarmOut {
+    double fitness;
+    double length;
+    uint32_t q;
+    uint32_t iterations;
+    uint32_t truncated;
+    uint32_t status;        // 0 ok, 2 non-finite fitness
+    uint32_t bad_g, bad_n, bad_k, window_len;
+};
+
+struct SwarmParams {
+    // shape
+    int n_swarms, G, N, D, C, rows_per_cta, max_local_groups;
+    int nthreads, entry_cap;
+    int cap;                 // iteration budget (T or max_iters_per_frame)
+    int auto_truncate, carry, tw, warm;
+    double alpha, beta, delta, pi_radius;
+    int beta_int;            // >= 1: beta is this small integer (exact repeated product)
+    // inputs
+    const double* hypers;  long long hypers_stride;   // doubles between swarms (0 = shared)
+    const unsigned long long* seeds;
+    const unsigned char* worlds; long long world_stride; int max_obs, max_verts;
+    int off_offsets, off_verts;
+    const double* prev; const unsigned char* has_prev;  // per swarm: D values + flag
+    const double* lo; const double* hi;                 // benchmark box (D); path: from world
+    // window state (per swarm: tw values oldest..newest, effective length)
+    double* win_vals; int* win_len;
+    // outputs
+    SwarmOut* out; double* best_x; double* trace;
+};
+
+struct SmemLayout {
+    size_t x, v, pb, pbf, pbq, q, fit, imp, seglen, coef, lo, hi, hyp, gbx, gbf, gbq, chg, tbx,
+        win, pf, prow, pq, px, allf, allrow, allq, obb, ooff, vert, edge, list, misc, total;
+};
+
+#ifdef __CUDACC__
+#define SEPSO_LHD __host__ __device__ inline
+#else
+#define SEPSO_LHD inline
+#endif
+
+SEPSO_LHD size_t sm_align(size_t v) { return (v + 15) & ~size_t(15); }
+
+// Shared-memory carve-up of one CTA; identical on host (launch size) and device.
+SEPSO_LHD SmemLayout smem_layout(const SwarmParams& p, size_t tsz, bool path) {
+    SmemLayout L{};
+    const size_t P = size_t(p.rows_per_cta), D = size_t(p.D), G = size_t(p.G);
+    const size_t S = size_t(p.D / 2 + 1), LG = size_t(p.max_local_groups), C = size_t(p.C);
+    const size_t O = path ? size_t(p.max_obs) : 0, V = path ? size_t(p.max_verts) : 0;
+    size_t o = 0;
+    auto take = [&](size_t bytes) { const size_t at = o; o = sm_align(o + bytes); return at; };
+    L.misc = take(256);
+    L.x = take(P * D * tsz);
+    L.v = take(P * D * tsz);
+    L.pb = take(P * D * tsz);
+    L.pbf = take(P * tsz);
+    L.pbq = take(P * 4);
+    L.q = take(P * 4);
+    L.fit = take(P * tsz);
+    L.imp = take(P * 4);
+    L.seglen = take(path ? P * S * tsz : 0);
+    L.coef = take(3 * P * tsz);
+    L.lo = take(D * tsz);
+    L.hi = take(D * tsz);
+    L.hyp = take(G * 6 * tsz);
+    L.gbx = take(G * D * tsz);
+    L.gbf = take(G * tsz);
+    L.gbq = take(G * 4);
+    L.chg = take(G * 4);
+    L.tbx = take(D * tsz);
+    L.win = take(size_t(p.tw) * 8);
+    L.pf = take(2 * LG * tsz);
+    L.prow = take(2 * LG * 4);
+    L.pq = take(2 * LG * 4);
+    L.px = take(2 * LG * D * tsz);
+    L.allf = take(C * LG * tsz);
+    L.allrow = take(C * LG * 4 + C * 4);   // + per-CTA bad row
+    L.allq = take(C * LG * 4);
+    L.obb = take(O * 4 * tsz);
+    L.ooff = take((O + 1) * 4);
+    L.vert = take(V * 2 * tsz);
+    L.edge = take(V * 4 * tsz);
+    L.list = take(path ? size_t(p.entry_cap) * 4 : 0);
+    L.total = o;
+    return L;
+}
+
+// host launchers (swarm_kernel.cu)
+int launch_swarms(const SwarmParams& p, int problem, bool fp64, void* stream,
+                  size_t* smem_bytes_out);
+int swarm_smem_bytes(const SwarmParams& p, int problem, bool fp64, size_t* bytes);
+int max_smem_per_block();
+
+} // namespace sepso

@@ -160,6 +160,23 @@ def oracle():
     _sig(lib, "or_generate_world", C.c_int,
          [C.POINTER(ScenarioCfg), C.c_uint64, C.c_int, dp, u32p, dp, dp, u8p])
     _sig(lib, "or_step_world", None, [dp, C.c_size_t, u32p, dp, dp, C.c_double])
+    _sig(lib, "or_init_swarm_seed", C.c_int,
+         [dp, dp, dp, C.c_size_t, C.c_size_t, C.c_size_t, C.c_uint64, C.c_int, dp, C.c_size_t,
+          C.c_double, dp, dp])
+    _sig(lib, "or_step_seed", C.c_int,
+         [dp, dp, dp, C.c_size_t, C.c_size_t, C.c_size_t, dp, dp, dp, dp, dp, C.c_uint64, C.c_int,
+          C.c_uint64, C.c_size_t, C.c_size_t])
+    _sig(lib, "or_update_bests_arrays", None,
+         [C.c_size_t, C.c_size_t, C.c_size_t, dp, dp, dp, dp, dp, dp, dp, dp])
+    _sig(lib, "or_run_dtpso_flat", C.c_int,
+         [C.c_int, W, C.c_size_t, dp, dp, C.c_double, C.c_double, dp, C.c_size_t, C.c_size_t,
+          C.c_size_t, C.c_uint64, C.c_int, dp, dp, dp, szp])
+    _sig(lib, "or_lfv_flat", C.c_double,
+         [dp, C.c_size_t, C.c_int, W, C.c_size_t, dp, dp, C.c_double, C.c_double, C.c_size_t,
+          C.c_size_t, C.c_size_t, C.c_uint64, C.c_int])
+    _sig(lib, "or_evolve_flat", C.c_int,
+         [C.c_int, W, C.c_size_t, dp, dp, C.c_double, C.c_double, C.c_size_t, C.c_size_t,
+          C.c_size_t, C.c_size_t, C.c_size_t, C.c_size_t, C.c_uint64, dp, C.c_int, dp, dp, dp])
     _cache["oracle"] = lib
     return lib
 
@@ -281,3 +298,36 @@ def ref_plan_frame(kind, world: WorldBuf, prev, hypers, cfg: PlannerCfg, seed, w
     st = r.ref_plan_frame(C.byref(world.struct()), ptr(prev_a), ptr(hyp), C.byref(cfg), seed,
                           ptr(wbuf), C.byref(wl), C.byref(rec), ptr(best), bad)
     return st, rec, best, wbuf[:wl.value].copy(), tuple(bad)
+
+
+def world_from_engine(pw) -> WorldBuf:
+    """oracle WorldBuf from a paper_2308_10169_b200.PolygonWorld (same doubles)."""
+    w = WorldBuf(pw.width, pw.height, pw.start, pw.target, pw.obstacles(), pw.start_velocity,
+                 pw.target_velocity, pw.velocities[:pw.n_obstacles] if pw.n_obstacles else None)
+    return w
+
+
+def float_world(pw):
+    """The FP32 engine plans on the FP32-rounded world; give the oracle the same."""
+    import paper_2308_10169_b200 as pe
+    r = lambda a: np.asarray(a, dtype=np.float32).astype(np.float64)
+    return pe.PolygonWorld(float(np.float32(pw.width)), float(np.float32(pw.height)), r(pw.start),
+                           r(pw.target), [r(p) for p in pw.obstacles()], pw.start_velocity,
+                           pw.target_velocity, pw.velocities)
+
+
+def oracle_run_dtpso(kind, hypers, G, N, T, seed, D=30, lo=None, hi=None, world=None,
+                     alpha=30.0, beta=4.0, rng=RNG_PHILOX):
+    o = oracle()
+    trace = np.zeros(T)
+    fp = np.zeros(D)
+    ff = C.c_double(0)
+    bad = (C.c_size_t * 3)()
+    lo_a = None if lo is None else np.ascontiguousarray(lo, dtype=np.float64)
+    hi_a = None if hi is None else np.ascontiguousarray(hi, dtype=np.float64)
+    wb = world_from_engine(world) if world is not None else None
+    ws = C.byref(wb.struct()) if wb is not None else None
+    hyp = np.ascontiguousarray(hypers, dtype=np.float64)
+    st = o.or_run_dtpso_flat(kind, ws, D, ptr(lo_a), ptr(hi_a), alpha, beta, ptr(hyp), G, N, T,
+                             seed, rng, ptr(trace), ptr(fp), C.byref(ff), bad)
+    return st, trace, fp, ff.value, tuple(bad)
