@@ -1,0 +1,445 @@
+#!/usr/bin/env python
+"""bench.py -- SEPSO planning throughput on B200 (BASELINE.json metric: plans/sec).
+
+Workload (N=1 headline = BASELINE config 2, the paper's dynamic scene): one
+100-frame scenario stream per GPU (ScenarioConfig defaults, root seed 3 + rank,
+variant sepso = evolved hypers + PI + AT, cap 30, window carryover -- the
+reference's acceptance scenario, tests/acceptance.cpp:245-264).  A "step" is
+one frame: plan_frame on the frozen world, then step_world.
+
+  value  device-resident: sf_scene_batch (world, prev best, window and records
+         in HBM; one fused planning launch + one on-device step_world launch
+         per frame), CUDA events per step on the engine stream, L2 flushed
+         between steps, max over ranks.
+  e2e    the reference-facing call: sf_plan_frame with HOST world/prev/window
+         buffers (one H2D + one D2H inside every step) + host step_world.
+
+`--workload batched` runs BASELINE config 5 instead (B independent scenes per
+GPU, one frame of all of them per step).  N>1 runs independent replicas (the
+scene stream does not shard).  `--impl reference` times
+the reference's own CPU implementation (oracle/_ref/libsfref_mt.so, compiled
+unmodified from the reference headers) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+PUBLISHED_PLANS_PER_S = 1.0 / 0.0153     # C++ reference, proj/test_output.txt:28
+FLOP_PER_EVAL = lambda S, E: 18 * S * E + 10 * E + 6 * S + 3
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=60)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="sepso", choices=["sepso", "reference"])
+    ap.add_argument("--workload", default="scene", choices=["scene", "batched"])
+    ap.add_argument("--scenes", type=int, default=1024, help="scenes per GPU (batched)")
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Dist:
+    def __init__(self, ws, rank, local, backend):
+        self.ws, self.rank, self.local = ws, rank, local
+        self.pg = None
+        if ws > 1:
+            import torch.distributed as td
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            td.init_process_group(backend=backend, rank=rank, world_size=ws)
+            self.td = td
+
+    def barrier(self):
+        if self.ws > 1:
+            self.td.barrier()
+
+    def max(self, v: float) -> float:
+        if self.ws == 1:
+            return v
+        import torch
+        dev = torch.device("cuda", self.local) if torch.cuda.is_available() else torch.device("cpu")
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.ws > 1:
+            self.td.destroy_process_group()
+
+
+# --------------------------------------------------------------- clocks
+class Clocks:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.15)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            if len(r) >= 9:
+                for i, n in enumerate(names):
+                    if "Active" in r[5 + i] and "Not" not in r[5 + i]:
+                        reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+# ------------------------------------------------------ reference (CPU) arm
+def cpu_reference_scene(frames: int, skip: int, root_seed: int = 3):
+    """Reference run_scenario (unmodified, mt19937) on the host: plans/sec over
+    frames [skip, frames) from the reference's own PlanRecord.wall_seconds."""
+    import ctypes as C
+    from oracle_lib import PlanRecord, planner_cfg, ref
+    r = ref("mt")
+    if r is None:
+        return None
+    cfg = planner_cfg(max_iters=30, window_carryover=1)
+    recs = (PlanRecord * frames)()
+    wall = np.zeros(frames)
+    t0 = time.perf_counter()
+    st = r.ref_run_scenario(root_seed, 0, frames, C.byref(cfg), recs, wall.ctypes.data_as(C.POINTER(C.c_double)))
+    t1 = time.perf_counter()
+    assert st == 0
+    timed = wall[skip:]
+    iters = np.mean([recs[i].iterations for i in range(skip, frames)])
+    return {"plans_per_s": len(timed) / timed.sum(), "wall_s": t1 - t0, "mean_iterations": float(iters),
+            "frames": len(timed)}
+
+
+def cpu_reference_batched(n_scenes: int, seconds: float = 15.0):
+    """Config 5 on the host: independent cold plans (frame 0 of scenes
+    0..n-1, the first frame of each scenario) on all host threads."""
+    import ctypes as C
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle_lib import PlanRecord, planner_cfg, ref, generate_world, oracle
+    r = ref("mt")
+    if r is None:
+        return None
+    o = oracle()
+    cores = os.cpu_count() or 1
+    cfg = planner_cfg(max_iters=30, window_carryover=1)
+
+    def one(s):
+        w = generate_world("mt", o.or_derive_seed(s, b"world"))
+        rec = PlanRecord()
+        best = np.zeros(16)
+        win = np.zeros(32)
+        wl = C.c_size_t(0)
+        r.ref_plan_frame(C.byref(w.struct()), None, EVOLVED.ctypes.data_as(C.POINTER(C.c_double)),
+                         C.byref(cfg), o.or_derive_seed_idx(s, b"plan", 0),
+                         win.ctypes.data_as(C.POINTER(C.c_double)), C.byref(wl), C.byref(rec),
+                         best.ctypes.data_as(C.POINTER(C.c_double)), None)
+        return 1
+
+    done = 0
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(cores) as ex:
+        s = 0
+        while time.perf_counter() - t0 < seconds and s < n_scenes:
+            chunk = list(range(s, min(n_scenes, s + cores * 4)))
+            done += sum(ex.map(one, chunk))
+            s += len(chunk)
+    dt = time.perf_counter() - t0
+    return {"plans_per_s": done / dt, "plans": done, "cores": cores}
+
+
+EVOLVED = None
+
+
+def main():
+    global EVOLVED
+    a = parse()
+    ws, rank, local = dist_env()
+    if a.impl == "reference":
+        return reference_arm(a, ws, rank)
+    import torch
+    import paper_2308_10169_b200 as pe
+    EVOLVED = pe.EVOLVED_PATH_HYPERS
+    torch.cuda.set_device(local)
+    dist = Dist(ws, rank, local, "nccl")
+    eng = pe.Engine(local, a.precision)
+    stream = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", local))
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    root = 3 + rank
+    planner = pe.PlannerConfig(max_iters_per_frame=30, window_carryover=True)
+    K, W = a.steps, a.warmup
+    n_sc = 1 if a.workload == "scene" else a.scenes
+    scen = [pe.ScenarioConfig(root_seed=(root if n_sc == 1 else rank * n_sc + s)) for s in range(n_sc)]
+
+    # ---------------------------------------------------- device-resident value
+    sb = pe.SceneBatch(eng, scen, planner, pe.EVOLVED_PATH_HYPERS, W + K)
+    sb.run(W)
+    eng.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    clocks = Clocks(local)
+    dist.barrier()
+    torch.cuda.synchronize()
+    eng.synchronize()
+    t_wall0 = time.perf_counter()
+    with torch.cuda.stream(stream):
+        for i in range(K):
+            flush.zero_()                      # L2 (126 MB) flushed between steps
+            evs[i][0].record(stream)
+            sb.run(1)
+            evs[i][1].record(stream)
+    eng.synchronize()
+    torch.cuda.synchronize()
+    t_wall1 = time.perf_counter()
+    dist.barrier()
+    clk = clocks.stop()
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    dev_ms = dist.max(float(np.sum(step_ms)))
+    recs, _ = sb.records(W, K)
+    iters = np.array([r.iterations for r in recs], dtype=np.float64)
+    plans = K * n_sc
+    value = plans * ws / (dev_ms / 1e3)
+    evals = float(iters.sum()) * planner.groups * planner.per_group
+    # kernel-only time of the fused planning kernel (same frames, timing pass)
+    eng.enable_timing(True)
+    sb2 = pe.SceneBatch(eng, scen, planner, pe.EVOLVED_PATH_HYPERS, W + K)
+    sb2.run(W)
+    eng.enable_timing(True)
+    sb2.run(K)
+    k_ms, k_n = eng.kernel_time()
+    eng.enable_timing(False)
+    recs2, _ = sb2.records(W, K)
+    iters2 = np.array([r.iterations for r in recs2], dtype=np.float64)
+    sb2.close()
+    sb.close()
+    S, E = planner.dim // 2 + 1, 32
+    flop_launch = float(iters2.sum()) * planner.groups * planner.per_group * FLOP_PER_EVAL(S, E) / K
+    achieved = flop_launch / (k_ms / k_n / 1e3) / 1e12
+    peak = eng.measure_fp32_peak()
+
+    # ------------------------------------------------------------ e2e (host API)
+    e2e = None
+    h2d = d2h = 0
+    if a.workload == "scene":
+        w = pe.generate_world(scen[0], _derive(root, "world"))
+        prev, win = None, []
+        def one_frame(f, w, prev):
+            rec = eng.plan_frame(w, prev, pe.EVOLVED_PATH_HYPERS, planner, _derive(root, "plan", f), win)
+            return rec, pe.step_world(w, 1.0)
+        for f in range(W):
+            rec, w = one_frame(f, w, prev)
+            prev = rec.best_path
+        ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+        ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+        dist.barrier()
+        eng.synchronize()
+        for i in range(K):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+                ev0[i].record(stream)
+            rec, w = one_frame(W + i, w, prev)
+            prev = rec.best_path
+            with torch.cuda.stream(stream):
+                ev1[i].record(stream)
+        torch.cuda.synchronize()
+        h2d, d2h = eng.last_io_bytes()
+        e2e_ms = dist.max(float(sum(e0.elapsed_time(e1) for e0, e1 in zip(ev0, ev1))))
+        e2e = {"value": K * ws / (e2e_ms / 1e3), "unit": "plans/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h)}
+    else:
+        worlds = [pe.generate_world(s, _derive(s.root_seed, "world")) for s in scen]
+        seeds = [_derive(s.root_seed, "plan", 0) for s in scen]
+        cfg0 = pe.PlannerConfig(max_iters_per_frame=30)
+        eng.plan_frames_batched(worlds, None, None, pe.EVOLVED_PATH_HYPERS, cfg0, seeds)
+        dist.barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(1, min(K, 5))
+        ms_tot = 0.0
+        for _ in range(reps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+                ev0.record(stream)
+            eng.plan_frames_batched(worlds, None, None, pe.EVOLVED_PATH_HYPERS, cfg0, seeds)
+            with torch.cuda.stream(stream):
+                ev1.record(stream)
+            torch.cuda.synchronize()
+            ms_tot += ev0.elapsed_time(ev1)
+        h2d, d2h = eng.last_io_bytes()
+        e2e_ms = dist.max(ms_tot / reps)
+        e2e = {"value": n_sc * ws / (e2e_ms / 1e3), "unit": "plans/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h)}
+
+    # ------------------------------------------------------------ extra: config 5
+    extra = None
+    if a.workload == "scene" and not a.no_extra:
+        nb = 1024
+        scb = [pe.ScenarioConfig(root_seed=rank * nb + s) for s in range(nb)]
+        bb = pe.SceneBatch(eng, scb, planner, pe.EVOLVED_PATH_HYPERS, 4)
+        bb.run(1)
+        eng.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            e0.record(stream)
+            bb.run(3)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        rb, _ = bb.records(1, 3)
+        bb.close()
+        extra = {"workload": f"config5: {nb} independent paper scenes per GPU, frames 1-3 (warm-started)",
+                 "plans_per_s": 3 * nb * ws / (dist.max(ms) / 1e3),
+                 "mean_iterations": float(np.mean([r.iterations for r in rb]))}
+
+    # ------------------------------------------------------------ CPU baseline
+    cpu = None
+    if rank == 0 and not a.no_cpu_baseline:
+        if a.workload == "scene":
+            c = cpu_reference_scene(100, 0)
+            if c:
+                cpu = {"value": c["plans_per_s"], "unit": "plans/s", "cores": 1, "kind": "reference",
+                       "sample": f"reference run_scenario (unmodified, mt19937), root seed 3, 100 frames, "
+                                 f"cap 30, carryover; mean {c['mean_iterations']:.1f} iterations/frame"}
+        else:
+            c = cpu_reference_batched(min(n_sc, 4096))
+            if c:
+                cpu = {"value": c["plans_per_s"], "unit": "plans/s", "cores": c["cores"], "kind": "reference",
+                       "sample": f"{c['plans']} cold plans (frame 0 of scenes 0..), scene-parallel, ~15 s"}
+
+    if rank == 0:
+        cpu_thr = os.cpu_count() or 1
+        line = {
+            "metric": "plans_per_sec",
+            "value": value,
+            "unit": "plans/s",
+            "n_gpus": ws,
+            "steps": K,
+            "warmup": W,
+            "ms_per_step": dev_ms / K,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": value / PUBLISHED_PLANS_PER_S if a.workload == "scene" else None,
+            "dtype": a.precision,
+            "data": "synthetic (seeded generate_world scenes, Philox draw stream)",
+            "config": {
+                "workload": ("config2: paper dynamic scene (366 cm, 6 dynamic + 2 static obstacles), "
+                             "SEPSO evolved hypers + PI + AT, G=8 N=170 D=16, cap 30, window carryover, "
+                             f"root seed {root}; one frame per step" if a.workload == "scene" else
+                             f"config5: {n_sc} independent paper scenes per GPU, one frame each per step"),
+                "scenes_per_gpu": n_sc,
+                "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                "l2": "flushed between steps (256 MiB write)",
+                "mean_iterations_per_frame": float(iters.mean()),
+                "fitness_evals": evals,
+                "evals_per_sec": evals * ws / (dev_ms / 1e3),
+            },
+            "roofline": {
+                "kernel": "swarm_kernel<float,path> (fused frame: fitness+bests+AT+update)",
+                "bound": "fp32",
+                "achieved": achieved,
+                "peak": peak,
+                "peak_source": "measured FFMA probe (sf_measure_fp32_peak) on this GPU",
+                "unit": "TFLOP/s",
+                "frac": achieved / peak if peak else None,
+                "traffic": None,
+                "flop_per_launch": flop_launch,
+                "flop_per_eval": FLOP_PER_EVAL(S, E),
+                "avg_launch_us": 1e3 * k_ms / k_n,
+                "launches": int(k_n),
+            },
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": 2 * K,
+            "clocks": clk,
+            "batched": extra,
+            "host_threads": cpu_thr,
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    dist.close()
+
+
+def _derive(root, tag, idx=None):
+    from oracle_lib import oracle   # seed derivation only (rng.hpp:52-59)
+    o = oracle()
+    return o.or_derive_seed(root, tag.encode()) if idx is None else o.or_derive_seed_idx(root, tag.encode(), idx)
+
+
+def reference_arm(a, ws, rank):
+    if rank != 0:
+        return 0
+    from oracle_lib import ref
+    if ref("mt") is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libsfref_mt.so not built"}))
+        return 0
+    K, W = a.steps, a.warmup
+    if a.workload == "scene":
+        c = cpu_reference_scene(W + K, W)
+        value, cores = c["plans_per_s"], 1
+        sample = f"reference run_scenario root seed 3, frames {W}..{W + K - 1} timed (cap 30, carryover)"
+        cfgd = {"workload": "config2: paper dynamic scene, reference CPU (unmodified, mt19937)",
+                "mean_iterations_per_frame": c["mean_iterations"]}
+    else:
+        global EVOLVED
+        from oracle_lib import EVOLVED_PATH_HYPERS
+        EVOLVED = np.ascontiguousarray(EVOLVED_PATH_HYPERS)
+        c = cpu_reference_batched(a.scenes * max(1, a.gpus), seconds=20.0)
+        value, cores = c["plans_per_s"], c["cores"]
+        sample = f"{c['plans']} cold plans, scene-parallel on {cores} threads"
+        cfgd = {"workload": "config5: independent paper scenes, reference CPU"}
+    line = {"impl": "reference", "metric": "plans_per_sec", "value": value, "unit": "plans/s",
+            "n_gpus": a.gpus, "steps": K, "warmup": W, "ms_per_step": 1e3 / value,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": value / PUBLISHED_PLANS_PER_S,
+            "dtype": "fp64", "data": "synthetic", "config": cfgd,
+            "cpu_baseline": {"value": value, "unit": "plans/s", "cores": cores, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "plans/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main() or 0)

@@ -204,6 +204,31 @@ int sf_run_scenario(sf_ctx* ctx, const sf_scenario_config* cfg, int variant, uin
                     const sf_planner_config* base, const double* evolved_hypers,
                     sf_plan_record* records, double* best);
 
+/* ---- device-resident scenarios (run_scenario frame loop on the device) --- */
+/* n independent scenarios (simenv.hpp:239-276) kept in HBM: worlds are made by
+ * generate_world(cfgs[s], derive_seed(cfgs[s].root_seed, "world")) once; each
+ * frame is ONE fused planning launch (seed derive_seed(root, "plan", f) derived
+ * on the device, prev best and carried window chained in HBM) followed by one
+ * on-device step_world launch.  `cfg` is the final planner config (variant
+ * already applied).  Up to max_frames frames may be run in total. */
+typedef struct sf_scene_batch sf_scene_batch;
+int sf_scene_batch_create(sf_ctx* ctx, uint32_t n, const sf_scenario_config* cfgs,
+                          const sf_planner_config* cfg, const double* hypers, uint32_t max_frames,
+                          sf_scene_batch** out);
+/* enqueue `frames` more frames on the context stream (asynchronous) */
+int sf_scene_batch_run(sf_scene_batch* b, uint32_t frames);
+/* synchronize and copy the records (frames x n, frame-major) of frames
+ * [first, first + count) and their best particles (NULL to skip) */
+int sf_scene_batch_records(sf_scene_batch* b, uint32_t first, uint32_t count,
+                           sf_plan_record* records, double* best);
+int sf_scene_batch_destroy(sf_scene_batch* b);
+
+/* FP32 FFMA throughput of the device (TFLOP/s): roofline denominator probe. */
+int sf_measure_fp32_peak(sf_ctx* ctx, double* tflops);
+
+/* Bytes moved host->device and device->host by the last host-buffer call. */
+int sf_ctx_last_io_bytes(sf_ctx* ctx, uint64_t* h2d, uint64_t* d2h);
+
 #ifdef __cplusplus
 }
 #endif

@@ -230,6 +230,8 @@ int run_batch(sf_ctx* ctx, const BatchIn& b, BatchOut& r) {
     p.trace = reinterpret_cast<double*>(d + io.trace);
     cudaError_t ce = cudaMemcpyAsync(d, h, io.out, cudaMemcpyHostToDevice, ctx->stream);
     if (ce != cudaSuccess) return cuda_fail(ce, "H2D io");
+    ctx->last_h2d = io.out;
+    ctx->last_d2h = io.end - io.out;
     st = launch_fused(ctx, fp, b.problem);
     if (st != SF_OK) return st;
     ce = cudaMemcpyAsync(h + io.out, d + io.out, io.end - io.out, cudaMemcpyDeviceToHost, ctx->stream);
@@ -1000,6 +1002,179 @@ int sf_run_scenario(sf_ctx* ctx, const sf_scenario_config* c, int variant, uint3
         if (best) std::copy(bp.begin(), bp.end(), best + size_t(f) * cfg.dim);
         if ((st = sf_step_world(&w, verts.data(), vel.data(), c->dt))) return st;
     }
+    return SF_OK;
+}
+
+int sf_ctx_last_io_bytes(sf_ctx* ctx, uint64_t* h2d, uint64_t* d2h) {
+    if (!ctx) return fail(SF_INVALID_ARGUMENT, "ctx is null");
+    if (h2d) *h2d = ctx->last_h2d;
+    if (d2h) *d2h = ctx->last_d2h;
+    return SF_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------ device-resident scenes
+struct sf_scene_batch {
+    sf_ctx* ctx = nullptr;
+    uint32_t n = 0, max_frames = 0, frames_done = 0;
+    sf_planner_config cfg{};
+    double dt = 1.0;
+    WorldLayout lay{};
+    FusedPlan fp;
+    DevBuf worlds, hyp, roots, ones, win_vals, win_len, out, best, trace;
+    bool staged = false;
+};
+
+extern "C" {
+
+int sf_scene_batch_create(sf_ctx* ctx, uint32_t n, const sf_scenario_config* cfgs,
+                          const sf_planner_config* cfg, const double* hypers, uint32_t max_frames,
+                          sf_scene_batch** out) {
+    if (!ctx || !cfgs || !out || n == 0 || max_frames == 0) return fail(SF_INVALID_ARGUMENT, "bad scene batch arguments");
+    DeviceGuard guard(ctx->device);
+    int st = validate_planner(cfg);
+    if (st) return st;
+    if ((st = validate_hypers(hypers, cfg->groups))) return st;
+    // worlds on the host (scene state is host-owned until it is staged)
+    std::vector<std::vector<uint32_t>> off(n);
+    std::vector<std::vector<sf_point>> verts(n), vel(n);
+    std::vector<sf_world> ws(n);
+    for (uint32_t s = 0; s < n; ++s) {
+        const uint32_t k = cfgs[s].dynamic_obstacles + cfgs[s].static_obstacles;
+        off[s].resize(k + 1);
+        verts[s].resize(4 * size_t(k) + 1);
+        vel[s].resize(size_t(k) + 1);
+        if ((st = sf_generate_world(&cfgs[s], derive_seed(cfgs[s].root_seed, "world"), &ws[s], off[s].data(),
+                                    verts[s].data(), vel[s].data())))
+            return st;
+    }
+    WorldPack wp;
+    pack_worlds(ws.data(), n, wp);
+    auto* b = new sf_scene_batch();
+    b->ctx = ctx;
+    b->n = n;
+    b->max_frames = max_frames;
+    b->cfg = *cfg;
+    b->dt = cfgs[0].dt;
+    b->lay = wp.lay;
+    const uint32_t D = cfg->dim, tw = cfg->tw, cap = cfg->max_iters_per_frame;
+    b->fp = plan_fused(ctx, kPath, int(n), int(cfg->groups), int(cfg->per_group), int(D), wp.lay.max_obs,
+                       wp.lay.max_verts, int(cap), int(tw));
+    if (!b->fp.fits) {
+        delete b;
+        return fail(SF_UNSUPPORTED, "scene batch: swarm does not fit a cluster");
+    }
+    cudaError_t e = cudaSuccess;
+    auto alloc = [&](DevBuf& buf, size_t bytes) { if (e == cudaSuccess) e = buf.ensure(bytes); };
+    alloc(b->worlds, wp.bytes.size());
+    alloc(b->hyp, size_t(cfg->groups) * 48);
+    alloc(b->roots, size_t(n) * 8);
+    alloc(b->ones, size_t(n));
+    alloc(b->win_vals, size_t(n) * tw * 8);
+    alloc(b->win_len, size_t(n) * 4);
+    alloc(b->out, size_t(max_frames) * n * sizeof(SwarmOut));
+    alloc(b->best, size_t(max_frames) * n * D * 8);
+    alloc(b->trace, size_t(n) * cap * 8);
+    if (e != cudaSuccess) {
+        delete b;
+        return cuda_fail(e, "scene batch allocation");
+    }
+    std::vector<uint64_t> roots(n);
+    for (uint32_t s = 0; s < n; ++s) roots[s] = cfgs[s].root_seed;
+    std::vector<uint8_t> ones(n, 1);
+    cudaMemcpyAsync(b->worlds.p, wp.bytes.data(), wp.bytes.size(), cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemcpyAsync(b->hyp.p, hypers, size_t(cfg->groups) * 48, cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemcpyAsync(b->roots.p, roots.data(), size_t(n) * 8, cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemcpyAsync(b->ones.p, ones.data(), size_t(n), cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemsetAsync(b->win_len.p, 0, size_t(n) * 4, ctx->stream);
+    e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) {
+        delete b;
+        return cuda_fail(e, "scene batch upload");
+    }
+    SwarmParams& p = b->fp.p;
+    p.alpha = cfg->alpha;
+    p.beta = cfg->beta;
+    p.beta_int = beta_integer(cfg->beta);
+    p.delta = cfg->delta;
+    p.pi_radius = cfg->pi_radius;
+    p.warm = int(cfg->gamma * double(cfg->per_group));
+    p.auto_truncate = cfg->auto_truncate;
+    p.carry = cfg->window_carryover;
+    p.hypers = static_cast<const double*>(b->hyp.p);
+    p.hypers_stride = 0;
+    p.seeds = nullptr;
+    p.roots = static_cast<const unsigned long long*>(b->roots.p);
+    p.tag_hash = fnv1a64("plan", 4);
+    p.worlds = static_cast<const unsigned char*>(b->worlds.p);
+    p.world_stride = (long long)wp.lay.stride;
+    p.off_offsets = int(wp.lay.off_offsets);
+    p.off_verts = int(wp.lay.off_verts);
+    p.lo = nullptr;
+    p.hi = nullptr;
+    p.win_vals = static_cast<double*>(b->win_vals.p);
+    p.win_len = static_cast<int*>(b->win_len.p);
+    p.trace = static_cast<double*>(b->trace.p);
+    *out = b;
+    return SF_OK;
+}
+
+int sf_scene_batch_run(sf_scene_batch* b, uint32_t frames) {
+    if (!b) return fail(SF_INVALID_ARGUMENT, "batch is null");
+    if (b->frames_done + frames > b->max_frames) return fail(SF_INVALID_ARGUMENT, "scene batch: max_frames exceeded");
+    sf_ctx* ctx = b->ctx;
+    DeviceGuard guard(ctx->device);
+    SwarmParams& p = b->fp.p;
+    const size_t D = b->cfg.dim;
+    for (uint32_t i = 0; i < frames; ++i) {
+        const uint32_t f = b->frames_done + i;
+        p.frame_index = int(f);
+        p.prev = f == 0 ? nullptr : static_cast<const double*>(b->best.p) + size_t(f - 1) * b->n * D;
+        p.has_prev = f == 0 ? nullptr : static_cast<const unsigned char*>(b->ones.p);
+        p.best_x = static_cast<double*>(b->best.p) + size_t(f) * b->n * D;
+        p.out = static_cast<SwarmOut*>(b->out.p) + size_t(f) * b->n;
+        int st = launch_fused(ctx, b->fp, kPath);
+        if (st) return st;
+        const int e = launch_step_worlds(static_cast<unsigned char*>(b->worlds.p), int(b->n), (long long)b->lay.stride,
+                                         int(b->lay.off_offsets), int(b->lay.off_verts), int(b->lay.off_vel), b->dt,
+                                         ctx->stream);
+        if (e) return cuda_fail(cudaError_t(e), "step_worlds");
+    }
+    b->frames_done += frames;
+    return SF_OK;
+}
+
+int sf_scene_batch_records(sf_scene_batch* b, uint32_t first, uint32_t count, sf_plan_record* records,
+                           double* best) {
+    if (!b || !records) return fail(SF_INVALID_ARGUMENT, "null argument");
+    if (first + count > b->frames_done) return fail(SF_INVALID_ARGUMENT, "frames not run yet");
+    sf_ctx* ctx = b->ctx;
+    DeviceGuard guard(ctx->device);
+    const size_t m = size_t(count) * b->n, D = b->cfg.dim;
+    std::vector<SwarmOut> outs(m);
+    cudaMemcpyAsync(outs.data(), static_cast<SwarmOut*>(b->out.p) + size_t(first) * b->n, m * sizeof(SwarmOut),
+                    cudaMemcpyDeviceToHost, ctx->stream);
+    if (best)
+        cudaMemcpyAsync(best, static_cast<double*>(b->best.p) + size_t(first) * b->n * D, m * D * 8,
+                        cudaMemcpyDeviceToHost, ctx->stream);
+    const cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "scene batch records");
+    for (size_t i = 0; i < m; ++i) fill_record(outs[i], 0.0, &records[i]);
+    for (size_t i = 0; i < m; ++i)
+        if (outs[i].status == 2)
+            return fail(SF_NON_FINITE, nonfinite_msg(outs[i].bad_g, outs[i].bad_n, outs[i].bad_k));
+    return SF_OK;
+}
+
+int sf_scene_batch_destroy(sf_scene_batch* b) {
+    if (!b) return SF_OK;
+    cudaSetDevice(b->ctx->device);
+    cudaStreamSynchronize(b->ctx->stream);
+    for (DevBuf* d : {&b->worlds, &b->hyp, &b->roots, &b->ones, &b->win_vals, &b->win_len, &b->out, &b->best,
+                      &b->trace})
+        d->release();
+    delete b;
     return SF_OK;
 }
 

@@ -45,6 +45,7 @@ struct sf_ctx {
     double kernel_ms = 0.0;
     uint64_t launches = 0;
     int force_cluster = 0, force_threads = 0;
+    uint64_t last_h2d = 0, last_d2h = 0;
     sepso::DevBuf io, scratch;
     sepso::PinnedBuf hio;
 };

@@ -42,7 +42,9 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
     c.edge = (T*)S8(L.edge); c.list = (uint32_t*)S8(L.list); c.m = (Misc<T>*)S8(L.misc);
     int* allbad = c.allrow + c.C * p.max_local_groups;
     const int LGM = p.max_local_groups;
-    const uint64_t seed = p.seeds[swarm];
+    const uint64_t seed =
+        p.roots ? splitmix64(splitmix64(p.roots[swarm] ^ p.tag_hash) + uint64_t(p.frame_index))
+                : p.seeds[swarm];
     const int G = c.G, N = c.N, D = c.D, R = c.R;
 
     // ---------------------------------------------------------- constants
@@ -348,6 +350,64 @@ int launch_swarms(const SwarmParams& p, int problem, bool fp64, void* stream, si
 int swarm_smem_bytes(const SwarmParams& p, int problem, bool fp64, size_t* bytes) {
     *bytes = smem_layout(p, fp64 ? 8 : 4, problem == kPath).total;
     return 0;
+}
+
+// ------------------------------------------------------------ world stepping
+// simenv.hpp:139-149
+__device__ __forceinline__ double reflect_axis_dev(double lo, double hi, double limit, double& v) {
+    if (lo <= 0.0) { v = -v; return __dmul_rn(-2.0, lo); }
+    if (hi >= limit) { v = -v; return __dmul_rn(-2.0, __dsub_rn(hi, limit)); }
+    return 0.0;
+}
+
+// simenv.hpp:155-184, one thread per world record
+__global__ void k_step_worlds(unsigned char* worlds, int n, long long stride, int off_offsets,
+                              int off_verts, int off_vel, double dt) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    unsigned char* rec = worlds + size_t(s) * size_t(stride);
+    WorldHeader* h = reinterpret_cast<WorldHeader*>(rec);
+    const uint32_t* off = reinterpret_cast<const uint32_t*>(rec + off_offsets);
+    double* vv = reinterpret_cast<double*>(rec + off_verts);
+    double* vel = reinterpret_cast<double*>(rec + off_vel);
+    auto move = [&](double& px, double& py, double& vx, double& vy) {
+        px = __dadd_rn(px, __dmul_rn(vx, dt));
+        py = __dadd_rn(py, __dmul_rn(vy, dt));
+        px = __dadd_rn(px, reflect_axis_dev(px, px, h->width, vx));
+        py = __dadd_rn(py, reflect_axis_dev(py, py, h->height, vy));
+    };
+    move(h->sx, h->sy, h->svx, h->svy);
+    move(h->tx, h->ty, h->tvx, h->tvy);
+    for (uint32_t o = 0; o < h->n_obs; ++o) {
+        double& ovx = vel[2 * o];
+        double& ovy = vel[2 * o + 1];
+        if (ovx == 0.0 && ovy == 0.0) continue;
+        const uint32_t v0 = off[o], v1 = off[o + 1];
+        for (uint32_t i = v0; i < v1; ++i) {
+            vv[2 * i] = __dadd_rn(vv[2 * i], __dmul_rn(ovx, dt));
+            vv[2 * i + 1] = __dadd_rn(vv[2 * i + 1], __dmul_rn(ovy, dt));
+        }
+        double bx0 = vv[2 * v0], by0 = vv[2 * v0 + 1], bx1 = bx0, by1 = by0;
+        for (uint32_t i = v0; i < v1; ++i) {
+            bx0 = smin(bx0, vv[2 * i]); by0 = smin(by0, vv[2 * i + 1]);
+            bx1 = smax(bx1, vv[2 * i]); by1 = smax(by1, vv[2 * i + 1]);
+        }
+        const double sx = reflect_axis_dev(bx0, bx1, h->width, ovx);
+        const double sy = reflect_axis_dev(by0, by1, h->height, ovy);
+        if (sx != 0.0 || sy != 0.0)
+            for (uint32_t i = v0; i < v1; ++i) {
+                vv[2 * i] = __dadd_rn(vv[2 * i], sx);
+                vv[2 * i + 1] = __dadd_rn(vv[2 * i + 1], sy);
+            }
+    }
+}
+
+int launch_step_worlds(unsigned char* worlds, int n, long long stride, int off_offsets,
+                       int off_verts, int off_vel, double dt, void* stream) {
+    if (n <= 0) return 0;
+    k_step_worlds<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+        worlds, n, stride, off_offsets, off_verts, off_vel, dt);
+    return int(cudaGetLastError());
 }
 
 int max_smem_per_block() {

@@ -69,6 +69,9 @@ struct SwarmParams {
     // inputs
     const double* hypers;  long long hypers_stride;   // doubles between swarms (0 = shared)
     const unsigned long long* seeds;
+    // alternatively seeds derived on device: derive_seed(roots[s], tag, frame_index)
+    // (rng.hpp:52-59) with tag_hash = fnv1a64(tag)
+    const unsigned long long* roots; unsigned long long tag_hash; int frame_index;
     const unsigned char* worlds; long long world_stride; int max_obs, max_verts;
     int off_offsets, off_verts;
     const double* prev; const unsigned char* has_prev;  // per swarm: D values + flag
@@ -141,5 +144,10 @@ int launch_swarms(const SwarmParams& p, int problem, bool fp64, void* stream,
                   size_t* smem_bytes_out);
 int swarm_smem_bytes(const SwarmParams& p, int problem, bool fp64, size_t* bytes);
 int max_smem_per_block();
+
+// simenv.hpp:155-184 on the device: advance n world records in place (FP64,
+// the reference's exact operation order).
+int launch_step_worlds(unsigned char* worlds, int n, long long stride, int off_offsets,
+                       int off_verts, int off_vel, double dt, void* stream);
 
 } // namespace sepso

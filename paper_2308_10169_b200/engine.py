@@ -35,7 +35,9 @@ ABI_SYMBOLS = [
     "sf_ctx_kernel_time", "sf_plan_frame", "sf_plan_frames_batched", "sf_run_dtpso",
     "sf_run_dtpso_batched", "sf_lfv_batch", "sf_evolve", "sf_init_swarm", "sf_step",
     "sf_update_bests", "sf_eval_path_rows", "sf_eval_bench_rows", "sf_should_truncate",
-    "sf_generate_world", "sf_step_world", "sf_run_scenario",
+    "sf_generate_world", "sf_step_world", "sf_run_scenario", "sf_scene_batch_create",
+    "sf_scene_batch_run", "sf_scene_batch_records", "sf_scene_batch_destroy",
+    "sf_ctx_last_io_bytes", "sf_measure_fp32_peak",
 ]
 
 
@@ -156,12 +158,28 @@ def lib():
         "sf_step_world": (C.c_int, [W, C.POINTER(_Point), C.POINTER(_Point), C.c_double]),
         "sf_run_scenario": (C.c_int, [C.c_void_p, C.POINTER(_ScenarioCfg), C.c_int, C.c_uint32,
                                       P, _dp, Pr, _dp]),
+        "sf_scene_batch_create": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(_ScenarioCfg), P,
+                                            _dp, C.c_uint32, C.POINTER(C.c_void_p)]),
+        "sf_scene_batch_run": (C.c_int, [C.c_void_p, C.c_uint32]),
+        "sf_scene_batch_records": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, Pr, _dp]),
+        "sf_scene_batch_destroy": (C.c_int, [C.c_void_p]),
+        "sf_ctx_last_io_bytes": (C.c_int, [C.c_void_p, _u64p, _u64p]),
+        "sf_measure_fp32_peak": (C.c_int, [C.c_void_p, _dp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
         f.restype, f.argtypes = res, args
     _LIB = L
     return L
+
+
+def _hyper_rows(hypers, groups, where):
+    """The C ABI reads exactly `groups` rows; a mismatch is the reference's
+    "hyper matrix group count != G" (swarm.hpp:101-102, planner.hpp:87-88)."""
+    h = np.ascontiguousarray(hypers, dtype=np.float64)
+    if h.ndim != 2 or h.shape[1] != 6 or h.shape[0] != groups:
+        raise ValueError(f"{where}: hyper matrix group count != G")
+    return h
 
 
 def _check(status, bad=None):
@@ -393,6 +411,16 @@ class Engine:
     def enable_timing(self, on=True):
         _check(self._L.sf_ctx_enable_timing(self._h, int(on)))
 
+    def measure_fp32_peak(self):
+        t = C.c_double(0)
+        _check(self._L.sf_measure_fp32_peak(self._h, C.byref(t)))
+        return t.value
+
+    def last_io_bytes(self):
+        a, b = C.c_uint64(0), C.c_uint64(0)
+        _check(self._L.sf_ctx_last_io_bytes(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def kernel_time(self):
         ms, n = C.c_double(0), C.c_uint64(0)
         _check(self._L.sf_ctx_kernel_time(self._h, C.byref(ms), C.byref(n)))
@@ -402,7 +430,7 @@ class Engine:
     def plan_frame(self, world: PolygonWorld, prev_best, hypers, config: PlannerConfig,
                    seed: int, carried_window: Optional[list] = None):
         """Returns a PlanRecord; `carried_window` (a list) is updated in place."""
-        hyp = np.ascontiguousarray(hypers, dtype=np.float64)
+        hyp = _hyper_rows(hypers, config.groups, "priori_init")
         prev = None if prev_best is None else np.ascontiguousarray(
             encode_path(prev_best) if np.ndim(prev_best) == 2 else prev_best, dtype=np.float64)
         best = np.zeros(config.dim)
@@ -428,7 +456,7 @@ class Engine:
                             config: PlannerConfig, seeds, windows=None, window_lens=None):
         n = len(worlds)
         cw = (_World * n)(*[w._c() for w in worlds])
-        hyp = np.ascontiguousarray(hypers, dtype=np.float64)
+        hyp = _hyper_rows(hypers, config.groups, "priori_init")
         prev_a = None if prev is None else np.ascontiguousarray(prev, dtype=np.float64)
         hp = None if has_prev is None else np.ascontiguousarray(has_prev, dtype=np.uint8)
         sd = np.ascontiguousarray(seeds, dtype=np.uint64)
@@ -462,7 +490,7 @@ class Engine:
     # -- runner.hpp:97-129
     def run_dtpso(self, problem, hypers, groups, per_group, iterations, seed, dim=30, **kw):
         pr, keep = self._problem(problem, dim, **kw)
-        hyp = np.ascontiguousarray(hypers, dtype=np.float64)
+        hyp = _hyper_rows(hypers, groups, "init_swarm")
         trace = np.zeros(iterations)
         fp = np.zeros(dim)
         ff = C.c_double(0)
@@ -577,3 +605,42 @@ class Engine:
         _check(self._L.sf_run_scenario(self._h, C.byref(config._c()), VARIANTS.index(variant),
                                        frames, C.byref(base._c()), _p(ev), recs, _p(best)))
         return [PlanRecord._from(recs[i], best[i]) for i in range(frames)]
+
+
+class SceneBatch:
+    """Device-resident run_scenario for n scenarios (sf_scene_batch_*): each
+    frame is one fused planning launch + one on-device step_world launch."""
+
+    def __init__(self, engine: Engine, scenarios: Sequence[ScenarioConfig],
+                 planner: PlannerConfig, hypers, max_frames: int):
+        self._e = engine
+        self.n = len(scenarios)
+        self.dim = planner.dim
+        cfgs = (_ScenarioCfg * self.n)(*[s._c() for s in scenarios])
+        hyp = _hyper_rows(hypers, planner.groups, "priori_init")
+        h = C.c_void_p()
+        _check(engine._L.sf_scene_batch_create(engine._h, self.n, cfgs, C.byref(planner._c()),
+                                               _p(hyp), max_frames, C.byref(h)))
+        self._h = h
+
+    def run(self, frames: int):
+        _check(self._e._L.sf_scene_batch_run(self._h, frames))
+
+    def records(self, first: int, count: int, with_best: bool = False):
+        recs = (_PlanRecord * (count * self.n))()
+        best = np.zeros((count, self.n, self.dim)) if with_best else None
+        _check(self._e._L.sf_scene_batch_records(self._h, first, count, recs, _p(best)))
+        out = [PlanRecord._from(recs[i], best.reshape(-1, self.dim)[i] if with_best
+                                else np.zeros(self.dim)) for i in range(count * self.n)]
+        return out, best
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._e._L.sf_scene_batch_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
