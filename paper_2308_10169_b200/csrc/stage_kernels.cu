@@ -186,7 +186,7 @@ int stage_step(bool fp64, const StageShape& s, const double* hypers, const void*
 // K2 standalone: one CTA per tile of rows, world staged in shared memory, the
 // same cull + compaction + filtered-predicate machinery as the fused kernel.
 struct EvalSmem {
-    size_t misc, lo, hi, obb, ooff, vert, edge, seglen, q, list, total;
+    size_t misc, lo, hi, obb, ooff, ofl, vert, edge, seglen, q, list, total;
 };
 
 SEPSO_LHD EvalSmem eval_smem(int rows_tile, int D, int max_obs, int max_verts, int entry_cap,
@@ -200,6 +200,7 @@ SEPSO_LHD EvalSmem eval_smem(int rows_tile, int D, int max_obs, int max_verts, i
     L.hi = take(size_t(D) * tsz);
     L.obb = take(size_t(max_obs) * 4 * tsz);
     L.ooff = take(size_t(max_obs + 1) * 4);
+    L.ofl = take(size_t(max_obs) * 4);
     L.vert = take(size_t(max_verts) * 2 * tsz);
     L.edge = take(size_t(max_verts) * 4 * tsz);
     L.seglen = take(size_t(rows_tile) * S * tsz);
@@ -220,23 +221,26 @@ __global__ void __launch_bounds__(256) k_eval_path(const unsigned char* __restri
     const int r0 = blockIdx.x * rows_tile;
     Ctx<T> c{};
     c.D = pp.D; c.W = pp.D / 2; c.S = c.W + 1;
+    c.fS.init(uint32_t(c.S));
+    c.fD.init(uint32_t(c.D));
+    c.fN.init(1u);
     c.P = min(rows_tile, rows - r0);
     if (c.P <= 0) return;
     c.x = const_cast<T*>(x) + size_t(r0) * pp.D;
     c.fit = fit + r0;
     c.lo = (T*)(smem + L.lo); c.hi = (T*)(smem + L.hi);
-    c.obb = (T*)(smem + L.obb); c.ooff = (int*)(smem + L.ooff); c.vert = (T*)(smem + L.vert);
+    c.obb = (T*)(smem + L.obb); c.ooff = (int*)(smem + L.ooff); c.ofl = (int*)(smem + L.ofl);
+    c.vert = (T*)(smem + L.vert);
     c.edge = (T*)(smem + L.edge); c.seglen = (T*)(smem + L.seglen); c.q = (int*)(smem + L.q);
     c.list = (uint32_t*)(smem + L.list); c.m = (Misc<T>*)(smem + L.misc);
     load_world(c, world, pp.off_offsets, pp.off_verts);
     if (threadIdx.x == 0) {
         c.m->n_pair = 0;
-        c.m->n_cont = 0;
-        c.m->cont_cap = min(pp.entry_cap / 4, c.P * max(c.O, 1));
     }
     for (int i = threadIdx.x; i < c.P; i += blockDim.x) c.q[i] = 0;
     __syncthreads();
     path_fitness_phase(pp, c);
+    __syncthreads();
     for (int i = threadIdx.x; i < c.P; i += blockDim.x) qout[r0 + i] = c.q[i];
 }
 

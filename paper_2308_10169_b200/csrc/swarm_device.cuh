@@ -143,13 +143,34 @@ template <> inline __device__ float bench_eval<float>(int kind, const float* p, 
     return __int_as_float(0x7fc00000);
 }
 
+// -------------------------------------------------------- fast division
+// n / d for 0 <= n < 2^31 by multiply-high + shift (Granlund-Montgomery);
+// the loops below index (particle, segment) and (particle, dim) pairs without
+// hardware-emulated integer division.
+struct FastDiv {
+    uint32_t d = 1, mul = 0, shr = 0;
+    __host__ __device__ void init(uint32_t div) {
+        d = div;
+        if (div <= 1) { mul = 0; shr = 0; return; }
+        uint32_t l = 0;
+        while ((1u << l) < div) ++l;
+        const uint32_t p = 31 + l;
+        mul = uint32_t(((1ull << p) + div - 1) / div);
+        shr = p - 32;
+    }
+    __device__ __forceinline__ uint32_t div(uint32_t n) const {
+        return d == 1 ? n : (__umulhi(n, mul) >> shr);
+    }
+};
+
 // ------------------------------------------------------------ swarm context
 template <class T> struct Ctx {
     // shape
     int G, N, D, W, S, R, P, row0, LG, O, C, crank;
+    FastDiv fS, fD, fN;
     // shared arrays
     T *x, *v, *pb, *pbf, *fit, *seglen, *coef, *lo, *hi, *hyp, *gbx, *gbf, *tbx, *pf, *px, *allf;
-    int *pbq, *q, *imp, *gbq, *chg, *prow, *pq, *allrow, *allq, *ooff;
+    int *pbq, *q, *imp, *gbq, *chg, *prow, *pq, *allrow, *allq, *ooff, *ofl;
     T *obb, *vert, *edge;
     double* win;
     uint32_t* list;
@@ -157,6 +178,12 @@ template <class T> struct Ctx {
     // path constants
     T sx, sy, tx, ty, margin;
 };
+
+// Work-list entry: local particle (13 bits) | segment (8 bits) | obstacle (11 bits).
+constexpr int kMaxTileRows = 8191, kMaxSegments = 255, kMaxObstacles = 2047;
+__device__ __forceinline__ uint32_t pack_entry(int pl, int s, int o) {
+    return (uint32_t(pl) << 19) | (uint32_t(s) << 11) | uint32_t(o);
+}
 
 // chain point j of start -> w_1..w_W -> target for local particle pl (geometry.hpp:157-165)
 template <class T>
@@ -174,13 +201,14 @@ template <> __device__ __forceinline__ float seg_length<float>(float dx, float d
     return sqrtf(fmaf(dx, dx, dy * dy));
 }
 
-// Segment (item) x obstacle edges: number of intersecting (segment, edge) pairs.
+// Segment s of particle pl against every edge of obstacle o: the number of
+// intersecting (segment, edge) pairs (geometry.hpp:210-214).
 template <class T>
-__device__ int pair_count(const Ctx<T>& c, int item, int o);
+__device__ int pair_count(const Ctx<T>& c, int pl, int s, int o);
 
+// FP64 engine: the reference predicate on every edge, bit for bit.
 template <>
-inline __device__ int pair_count<double>(const Ctx<double>& c, int item, int o) {
-    const int pl = item / c.S, s = item - pl * c.S;
+inline __device__ int pair_count<double>(const Ctx<double>& c, int pl, int s, int o) {
     double a1x, a1y, a2x, a2y;
     chain_pt(c, pl, s, a1x, a1y);
     chain_pt(c, pl, s + 1, a2x, a2y);
@@ -194,24 +222,42 @@ inline __device__ int pair_count<double>(const Ctx<double>& c, int item, int o) 
     return cnt;
 }
 
+// FP32 engine: filtered orientation signs.
+// Vertex crosses cv_i = d x (v_i - a1) are shared by the two edges meeting at
+// v_i (o1 of edge i is o2 of edge i-1).  With every |cv| above the bound B and
+// one common sign, no edge can be hit -- neither properly (o1 == o2 on every
+// edge) nor through the collinear cases, which need an endpoint of the path
+// segment on an edge and therefore opposite vertex signs -- provided the
+// obstacle has no edge shorter than 1e-3 (ofl[o]); otherwise every edge takes
+// the per-pair test.  Uncertain signs fall back to the FP64 reference.
 template <>
-inline __device__ int pair_count<float>(const Ctx<float>& c, int item, int o) {
-    const int pl = item / c.S, s = item - pl * c.S;
+inline __device__ int pair_count<float>(const Ctx<float>& c, int pl, int s, int o) {
     float a1x, a1y, a2x, a2y;
     chain_pt(c, pl, s, a1x, a1y);
     chain_pt(c, pl, s + 1, a2x, a2y);
     const float dx = a2x - a1x, dy = a2y - a1y;
-    // Error bound for every cross product of this (segment, obstacle) pair:
-    // all operand components are bounded by the extent L of the union box.
     const float* bb = c.obb + 4 * o;
     const float ux = fmaxf(fmaxf(a1x, a2x), bb[2]) - fminf(fminf(a1x, a2x), bb[0]);
     const float uy = fmaxf(fmaxf(a1y, a2y), bb[3]) - fminf(fminf(a1y, a2y), bb[1]);
     const float L = fmaxf(ux, uy);
-    const float B = 1.5e-6f * L * L + 2e-12f;
+    // |error| of any cross product below <= 31 u L^2 (u = 2^-24); 48 u L^2
+    // leaves margin, 4e-12 covers the reference's 1e-12 dead band.
+    const float B = 2.9e-6f * L * L + 4e-12f;
     const int v0 = c.ooff[o], v1 = c.ooff[o + 1];
+    const float4* E = reinterpret_cast<const float4*>(c.edge);
+    if (c.ofl[o]) {
+        bool pos = true, neg = true;
+        for (int i = v0; i < v1; ++i) {
+            const float4 e = E[i];
+            const float cv = fmaf(dx, e.y - a1y, -(dy * (e.x - a1x)));
+            pos &= cv > B;
+            neg &= cv < -B;
+        }
+        if (pos || neg) return 0;
+    }
     int cnt = 0;
     for (int i = v0; i < v1; ++i) {
-        const float4 e = reinterpret_cast<const float4*>(c.edge)[i];
+        const float4 e = E[i];
         int r = fast_pair(a1x, a1y, dx, dy, e.x, e.y, e.z, e.w, B);
         if (r < 0) {
             const int j = (i + 1 == v1) ? v0 : i + 1;
@@ -239,10 +285,10 @@ __device__ __forceinline__ bool box_overlap(T lx, T ly, T hx, T hy, const T* bb,
     return lx <= bb[2] + m && bb[0] <= hx + m && ly <= bb[3] + m && bb[1] <= hy + m;
 }
 
-
 // Stage one world record (double) into shared memory as T: vertices, edge
-// records (b1, b2 - b1) and obstacle boxes (geometry.hpp:167-177); sets the
-// endpoints, the cull margin and the path search box (geometry.hpp:252-255).
+// records (b1, b2 - b1), obstacle boxes (geometry.hpp:167-177) and the
+// short-edge flag; sets endpoints, the cull margin and the path search box
+// (geometry.hpp:252-255).
 template <class T>
 __device__ void load_world(Ctx<T>& c, const unsigned char* wrec, int off_offsets, int off_verts) {
     using A = Ar<T>;
@@ -267,6 +313,7 @@ __device__ void load_world(Ctx<T>& c, const unsigned char* wrec, int off_offsets
     for (int o = tid; o < c.O; o += nthr) {                  // bbox_of, geometry.hpp:167-177
         const int v0 = c.ooff[o], v1 = c.ooff[o + 1];
         T bx0 = c.vert[2 * v0], by0 = c.vert[2 * v0 + 1], bx1 = bx0, by1 = by0;
+        bool long_edges = true;
         for (int i = v0; i < v1; ++i) {
             const T vx = c.vert[2 * i], vy = c.vert[2 * i + 1];
             bx0 = vx < bx0 ? vx : bx0;
@@ -279,85 +326,104 @@ __device__ void load_world(Ctx<T>& c, const unsigned char* wrec, int off_offsets
             e[1] = vy;
             e[2] = A::sub(c.vert[2 * j], vx);
             e[3] = A::sub(c.vert[2 * j + 1], vy);
+            const T ax = e[2] < T(0) ? -e[2] : e[2], ay = e[3] < T(0) ? -e[3] : e[3];
+            long_edges &= (ax > ay ? ax : ay) >= T(1e-3);
         }
         T* bb = c.obb + 4 * o;
         bb[0] = bx0; bb[1] = by0; bb[2] = bx1; bb[3] = by1;
+        c.ofl[o] = long_edges ? 1 : 0;
     }
 }
 
 // Path fitness of the CTA's particles into c.fit (before pbest logic).
+//   A1  one thread per (particle, segment): segment length, obstacle-box cull
+//       into a bit mask, warp-aggregated append of (particle, segment, obstacle)
+//       work entries (one shared atomic per warp and 32-obstacle chunk);
+//       first-waypoint containment per particle (FP64, rare).
+//   A2  the compacted entries, densely: pair_count per entry.
+//   A3  fitness = sum of lengths in chain order + alpha * Q^beta.
+// Entries beyond the list capacity are evaluated in place (correct, divergent).
 template <class T>
 __device__ void path_fitness_phase(const SwarmParams& p, Ctx<T>& c) {
     const int tid = threadIdx.x, lane = tid & 31, nthr = blockDim.x;
-    const int items = c.P * c.S;
-    const int pair_cap = p.entry_cap - c.m->cont_cap;
-    uint32_t* clist = c.list + pair_cap;
-    // A1: per (particle, segment) item: length, obstacle bbox cull -> work list
-    for (int base = tid - lane; base < items; base += nthr) {
-        const int it = base + lane;
-        const bool act = it < items;
-        int pl = 0, s = 0;
-        T a1x = 0, a1y = 0, a2x = 0, a2y = 0;
-        if (act) {
-            pl = it / c.S;
-            s = it - pl * c.S;
-            chain_pt(c, pl, s, a1x, a1y);
-            chain_pt(c, pl, s + 1, a2x, a2y);
-            c.seglen[it] = seg_length<T>(Ar<T>::sub(a2x, a1x), Ar<T>::sub(a2y, a1y));
-        }
-        const T lx = a1x < a2x ? a1x : a2x, hx = a1x < a2x ? a2x : a1x;
-        const T ly = a1y < a2y ? a1y : a2y, hy = a1y < a2y ? a2y : a1y;
-        for (int o = 0; o < c.O; ++o) {
-            const bool ov = act && box_overlap(lx, ly, hx, hy, c.obb + 4 * o, c.margin);
-            const unsigned mask = __ballot_sync(0xffffffffu, ov);
-            if (!mask) continue;
-            int basei = 0;
-            if (lane == __ffs(mask) - 1) basei = atomicAdd(&c.m->n_pair, __popc(mask));
-            basei = __shfl_sync(0xffffffffu, basei, __ffs(mask) - 1);
-            if (ov) {
-                const int idx = basei + __popc(mask & ((1u << lane) - 1u));
-                if (idx < pair_cap) c.list[idx] = uint32_t(it) * uint32_t(c.O) + uint32_t(o);
-                else {   // list overflow: evaluate in place (correct, just divergent)
-                    const int n = pair_count(c, it, o);
-                    if (n) atomicAdd(&c.q[pl], n);
+    const int S = c.S, items = c.P * S, O = c.O;
+    const int cap = p.entry_cap;
+    // ---- A1
+    {
+        const int step_pl = int(c.fS.div(uint32_t(nthr))), step_s = nthr - step_pl * S;
+        int pl = int(c.fS.div(uint32_t(tid))), s = tid - pl * S;
+        for (int base = 0; base < items; base += nthr) {
+            const bool act = base + tid < items;
+            T a1x = 0, a1y = 0, a2x = 0, a2y = 0;
+            if (act) {
+                chain_pt(c, pl, s, a1x, a1y);
+                chain_pt(c, pl, s + 1, a2x, a2y);
+                c.seglen[pl * S + s] = seg_length<T>(Ar<T>::sub(a2x, a1x), Ar<T>::sub(a2y, a1y));
+            }
+            const T lx = a1x < a2x ? a1x : a2x, hx = a1x < a2x ? a2x : a1x;
+            const T ly = a1y < a2y ? a1y : a2y, hy = a1y < a2y ? a2y : a1y;
+            for (int o0 = 0; o0 < O; o0 += 32) {
+                uint32_t mask = 0;
+                if (act) {
+                    const int oe = min(32, O - o0);
+                    for (int j = 0; j < oe; ++j)
+                        if (box_overlap(lx, ly, hx, hy, c.obb + 4 * (o0 + j), c.margin)) mask |= 1u << j;
+                }
+                const int n = __popc(mask);
+                int incl = n;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int t = __shfl_up_sync(0xffffffffu, incl, off);
+                    if (lane >= off) incl += t;
+                }
+                const int total = __shfl_sync(0xffffffffu, incl, 31);
+                if (total == 0) continue;
+                int wbase = 0;
+                if (lane == 31) wbase = atomicAdd(&c.m->n_pair, total);
+                wbase = __shfl_sync(0xffffffffu, wbase, 31);
+                int idx = wbase + incl - n;
+                while (mask) {
+                    const int j = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    if (idx < cap) {
+                        c.list[idx] = pack_entry(pl, s, o0 + j);
+                    } else {
+                        const int k = pair_count(c, pl, s, o0 + j);
+                        if (k) atomicAdd(&c.q[pl], k);
+                    }
+                    ++idx;
                 }
             }
+            pl += step_pl;
+            s += step_s;
+            if (s >= S) { s -= S; ++pl; }
         }
-        // containment candidates for the first waypoint (s == 0 -> endpoint b)
-        if (act && s == 0) {
-            const T wx = a2x, wy = a2y;
-            for (int o = 0; o < c.O; ++o) {
+        // first waypoint strictly inside an obstacle (geometry.hpp:217-218)
+        for (int q = tid; q < c.P; q += nthr) {
+            const T wx = c.x[q * c.D], wy = c.x[q * c.D + c.W];
+            for (int o = 0; o < O; ++o) {
                 const T* bb = c.obb + 4 * o;
                 if (wx >= bb[0] - c.margin && wx <= bb[2] + c.margin && wy >= bb[1] - c.margin &&
-                    wy <= bb[3] + c.margin) {
-                    const int idx = atomicAdd(&c.m->n_cont, 1);
-                    if (idx < c.m->cont_cap) clist[idx] = uint32_t(pl) * uint32_t(c.O) + uint32_t(o);
-                    else if (contain_count(c, pl, o)) atomicAdd(&c.q[pl], 1);
-                }
+                    wy <= bb[3] + c.margin && contain_count(c, q, o))
+                    atomicAdd(&c.q[q], 1);
             }
         }
     }
     __syncthreads();
-    // A2: dense evaluation of the compacted work list
-    const int np = min(c.m->n_pair, pair_cap), nc = min(c.m->n_cont, c.m->cont_cap);
-    for (int e = tid; e < np + nc; e += nthr) {
-        if (e < np) {
-            const uint32_t w = c.list[e];
-            const int it = int(w / uint32_t(c.O)), o = int(w - uint32_t(it) * uint32_t(c.O));
-            const int n = pair_count(c, it, o);
-            if (n) atomicAdd(&c.q[it / c.S], n);
-        } else {
-            const uint32_t w = clist[e - np];
-            const int pl = int(w / uint32_t(c.O)), o = int(w - uint32_t(pl) * uint32_t(c.O));
-            if (contain_count(c, pl, o)) atomicAdd(&c.q[pl], 1);
-        }
+    // ---- A2
+    const int np = min(c.m->n_pair, cap);
+    for (int e = tid; e < np; e += nthr) {
+        const uint32_t w = c.list[e];
+        const int pl = int(w >> 19), s = int((w >> 11) & 0xffu), o = int(w & 0x7ffu);
+        const int k = pair_count(c, pl, s, o);
+        if (k) atomicAdd(&c.q[pl], k);
     }
     __syncthreads();
-    if (tid == 0) { c.m->n_pair = 0; c.m->n_cont = 0; }
-    // A3: fitness = sum of segment lengths (in chain order) + alpha * Q^beta
+    if (tid == 0) c.m->n_pair = 0;
+    // ---- A3
     for (int pl = tid; pl < c.P; pl += nthr) {
         T len = T(0);
-        for (int s = 0; s < c.S; ++s) len = Ar<T>::add(len, c.seglen[pl * c.S + s]);
+        for (int s = 0; s < S; ++s) len = Ar<T>::add(len, c.seglen[pl * S + s]);
         const double pen = penalty(p.alpha, p.beta, p.beta_int, c.q[pl]);
         c.fit[pl] = Ar<T>::add(len, T(pen));
     }

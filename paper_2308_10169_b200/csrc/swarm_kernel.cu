@@ -12,6 +12,23 @@ namespace cg = cooperative_groups;
 namespace sepso {
 
 // ------------------------------------------------------------------ kernel
+// Element loops walk (particle, column) pairs with an incremental carry instead
+// of integer division: thread t starts at element t and advances by nthr.
+struct ElemWalk {
+    int pl, col, dpl, dcol, ncol;
+    __device__ ElemWalk(const FastDiv& f, int tid, int nthr, int ncols) : ncol(ncols) {
+        pl = int(f.div(uint32_t(tid)));
+        col = tid - pl * ncols;
+        dpl = int(f.div(uint32_t(nthr)));
+        dcol = nthr - dpl * ncols;
+    }
+    __device__ __forceinline__ void next() {
+        pl += dpl;
+        col += dcol;
+        if (col >= ncol) { col -= ncol; ++pl; }
+    }
+};
+
 template <class T, bool PATH>
 __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ SwarmParams p,
                                                         int problem) {
@@ -24,6 +41,9 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
 
     Ctx<T> c;
     c.G = p.G; c.N = p.N; c.D = p.D; c.W = p.D / 2; c.S = c.W + 1; c.R = p.G * p.N;
+    c.fS.init(uint32_t(c.S));
+    c.fD.init(uint32_t(c.D));
+    c.fN.init(uint32_t(c.N));
     c.C = p.C; c.crank = int(cluster.block_rank());
     c.row0 = c.crank * p.rows_per_cta;
     const int row1 = min(c.R, c.row0 + p.rows_per_cta);
@@ -38,7 +58,7 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
     c.chg = (int*)S8(L.chg); c.tbx = (T*)S8(L.tbx); c.win = (double*)S8(L.win);
     c.pf = (T*)S8(L.pf); c.prow = (int*)S8(L.prow); c.pq = (int*)S8(L.pq); c.px = (T*)S8(L.px);
     c.allf = (T*)S8(L.allf); c.allrow = (int*)S8(L.allrow); c.allq = (int*)S8(L.allq);
-    c.obb = (T*)S8(L.obb); c.ooff = (int*)S8(L.ooff); c.vert = (T*)S8(L.vert);
+    c.obb = (T*)S8(L.obb); c.ooff = (int*)S8(L.ooff); c.ofl = (int*)S8(L.ofl); c.vert = (T*)S8(L.vert);
     c.edge = (T*)S8(L.edge); c.list = (uint32_t*)S8(L.list); c.m = (Misc<T>*)S8(L.misc);
     int* allbad = c.allrow + c.C * p.max_local_groups;
     const int LGM = p.max_local_groups;
@@ -61,7 +81,7 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
         m->tbf = A::inf(); m->tbq = 0; m->tsrc_slot = -1; m->stop = 0; m->truncated = 0;
         m->status = 0; m->bad_row = INT_MAX; m->bad_min = INT_MAX; m->n_pair = 0; m->n_cont = 0;
         m->k_done = 0;
-        m->cont_cap = PATH ? min(p.entry_cap / 4, c.P * max(c.O, 1)) : 0;
+        m->cont_cap = 0;
         const int wl = p.carry ? p.win_len[swarm] : 0;
         m->win_len = wl < p.tw ? wl : p.tw;
         m->win_head = 0;
@@ -78,9 +98,10 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
         const bool warm_on = p.has_prev != nullptr && p.has_prev[swarm] != 0;
         const double* prev = warm_on ? p.prev + size_t(swarm) * D : nullptr;
         const T rad = T(p.pi_radius);
-        for (int e = tid; e < c.P * D; e += nthr) {
-            const int pl = e / D, d = e - pl * D;
-            const int row = c.row0 + pl, g = row / N, n = row - g * N;
+        ElemWalk w(c.fD, tid, nthr, D);
+        for (int e = tid; e < c.P * D; e += nthr, w.next()) {
+            const int pl = w.pl, d = w.col;
+            const int row = c.row0 + pl, g = int(c.fN.div(uint32_t(row))), n = row - g * N;
             const uint64_t ix = uint64_t(row) * uint64_t(D) + uint64_t(d);
             const T ux = unit_from_word<T>(philox_word(seed, ix));
             const T lo = c.lo[d], hi = c.hi[d];
@@ -110,18 +131,20 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
         // fitness (geometry.hpp:262-267 / benchmarks.hpp:45-53)
         if (PATH) path_fitness_phase(p, c);
         else bench_fitness_phase(problem, c);
-        // pbest (runner.hpp:73-80), non-finite detection (runner.hpp:56-61)
+        // pbest (runner.hpp:73-80) incl. the x -> pbest_x row copy; non-finite
+        // detection (runner.hpp:56-61).  Same thread owns fit[pl] (A3 above).
         for (int pl = tid; pl < c.P; pl += nthr) {
             const T f = c.fit[pl];
             if (!isfinite(f)) atomicMin(&c.m->bad_row, c.row0 + pl);
-            const bool better = f < c.pbf[pl];
-            if (better) { c.pbf[pl] = f; c.pbq[pl] = c.q[pl]; }
-            c.imp[pl] = better;
+            if (f < c.pbf[pl]) {
+                c.pbf[pl] = f;
+                c.pbq[pl] = c.q[pl];
+                const T* xs = c.x + pl * D;
+                T* ps = c.pb + pl * D;
+                for (int d = 0; d < D; ++d) ps[d] = xs[d];
+            }
             if (PATH) c.q[pl] = 0;
         }
-        __syncthreads();
-        for (int e = tid; e < c.P * D; e += nthr)
-            if (c.imp[e / D]) c.pb[e] = c.x[e];
         __syncthreads();
         // per-CTA group partials: (pbest_f, row) lexicographic min, one warp per group
         for (int lg = warp; lg < c.LG; lg += nthr >> 5) {
@@ -204,8 +227,9 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
                     c.win[m->win_head] = tv;
                     m->win_head = (m->win_head + 1) % p.tw;
                 }
-                // auto truncation (planner.hpp:181-187, 138-149), Q(tbest) tracked
-                if (p.auto_truncate && m->win_len >= p.tw) {
+                // auto truncation (planner.hpp:181-187, 138-149), Q(tbest) tracked;
+                // the std is only needed when the cheap conjuncts hold
+                if (p.auto_truncate && m->win_len >= p.tw && m->tbq == 0) {
                     double mean = 0.0;
                     for (int i = 0; i < p.tw; ++i) mean = __dadd_rn(mean, c.win[(m->win_head + i) % p.tw]);
                     mean = __ddiv_rn(mean, double(p.tw));
@@ -215,10 +239,20 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
                         var = __dadd_rn(var, __dmul_rn(dv, dv));
                     }
                     var = __ddiv_rn(var, double(p.tw));
-                    if (__dsqrt_rn(var) < p.delta && m->tbq == 0) { m->truncated = 1; m->stop = 1; }
+                    if (__dsqrt_rn(var) < p.delta) { m->truncated = 1; m->stop = 1; }
                 }
             }
             m->k_done = k;
+        } else if (k < p.cap) {
+            // meanwhile: this step's draws (draw_step_randoms, swarm.hpp:59-70) --
+            // they depend only on (seed, k, row), not on the bests
+            const uint64_t base = 2ull * uint64_t(R) * uint64_t(D) + uint64_t(k - 1) * 3ull * uint64_t(R);
+            for (int t = tid - 1; t < 3 * c.P; t += nthr - 1) {
+                const int j = t >= 2 * c.P ? 2 : (t >= c.P ? 1 : 0), pl = t - j * c.P;
+                const int row = c.row0 + pl, g = int(c.fN.div(uint32_t(row)));
+                const T u = unit_from_word<T>(philox_word(seed, base + uint64_t(j) * R + row));
+                c.coef[j * c.P + pl] = A::mul(c.hyp[g * 6 + j], u);   // a_j = c_j * r_j
+            }
         }
         __syncthreads();
         if (c.m->status) break;
@@ -226,7 +260,7 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
         {
             const int tg = c.m->tsrc_slot;
             for (int t = tid; t < G * D; t += nthr) {
-                const int g = t / D, d = t - g * D;
+                const int g = int(c.fD.div(uint32_t(t))), d = t - g * D;
                 const int slot = c.chg[g];
                 if (slot >= 0) {
                     const int cc = slot / LGM, lg = slot - cc * LGM;
@@ -241,25 +275,19 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
         if (c.m->stop) break;
         if (k == p.cap) break;        // plan_frame: no step after the last iteration
         // --------------------------------------------------- step k (swarm.hpp:138-174)
-        const uint64_t base = 2ull * uint64_t(R) * uint64_t(D) + uint64_t(k - 1) * 3ull * uint64_t(R);
-        for (int t = tid; t < 3 * c.P; t += nthr) {     // draw_step_randoms (swarm.hpp:59-70)
-            const int j = t / c.P, pl = t - j * c.P;
-            const int row = c.row0 + pl, g = row / N;
-            const T u = unit_from_word<T>(philox_word(seed, base + uint64_t(j) * R + row));
-            c.coef[j * c.P + pl] = A::mul(c.hyp[g * 6 + j], u);   // a_j = c_j * r_j
-        }
-        __syncthreads();
         {
             const T frac = T(double(k) / double(p.cap));           // inertia_at (swarm.hpp:81-84)
-            for (int e = tid; e < c.P * D; e += nthr) {
-                const int pl = e / D, d = e - pl * D;
-                const int g = (c.row0 + pl) / N;
+            ElemWalk w(c.fD, tid, nthr, D);
+            int g = int(c.fN.div(uint32_t(c.row0 + w.pl)));
+            for (int e = tid; e < c.P * D; e += nthr, w.next()) {
+                const int pl = w.pl, d = w.col;
+                while ((g + 1) * N <= c.row0 + pl) ++g;
                 const T* h = c.hyp + g * 6;
-                const T w = A::sub(h[3], A::mul(A::sub(h[3], h[4]), frac));
+                const T wt = A::sub(h[3], A::mul(A::sub(h[3], h[4]), frac));
                 const T lo = c.lo[d], hi = c.hi[d];
                 const T vmax = A::mul(h[5], A::sub(hi, lo));
                 const T xv = c.x[e];
-                T nv = A::add(A::add(A::add(A::mul(w, c.v[e]), A::mul(c.coef[pl], A::sub(c.pb[e], xv))),
+                T nv = A::add(A::add(A::add(A::mul(wt, c.v[e]), A::mul(c.coef[pl], A::sub(c.pb[e], xv))),
                                      A::mul(c.coef[c.P + pl], A::sub(c.gbx[g * D + d], xv))),
                               A::mul(c.coef[2 * c.P + pl], A::sub(c.tbx[d], xv)));
                 nv = clampT(nv, T(-vmax), vmax);

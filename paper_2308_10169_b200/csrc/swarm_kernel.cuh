@@ -84,7 +84,7 @@ struct SwarmParams {
 
 struct SmemLayout {
     size_t x, v, pb, pbf, pbq, q, fit, imp, seglen, coef, lo, hi, hyp, gbx, gbf, gbq, chg, tbx,
-        win, pf, prow, pq, px, allf, allrow, allq, obb, ooff, vert, edge, list, misc, total;
+        win, pf, prow, pq, px, allf, allrow, allq, obb, ooff, ofl, vert, edge, list, misc, total;
 };
 
 #ifdef __CUDACC__
@@ -132,6 +132,7 @@ SEPSO_LHD SmemLayout smem_layout(const SwarmParams& p, size_t tsz, bool path) {
     L.allq = take(C * LG * 4);
     L.obb = take(O * 4 * tsz);
     L.ooff = take((O + 1) * 4);
+    L.ofl = take(O * 4);
     L.vert = take(V * 2 * tsz);
     L.edge = take(V * 4 * tsz);
     L.list = take(path ? size_t(p.entry_cap) * 4 : 0);
