@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <limits>
 
@@ -231,7 +232,34 @@ FusedPlan plan_fused(sf_ctx* ctx, int problem, int n_swarms, int G, int N, int D
 int launch_fused(sf_ctx* ctx, FusedPlan& fp, int problem) {
     if (ctx->timing) cudaEventRecord(ctx->ev0, ctx->stream);
     size_t smem = 0;
+    static const bool phase_prof = std::getenv("SEPSO_PHASE_PROF") != nullptr;
+    long long* prof = nullptr;
+    if (phase_prof && fp.p.cap > 0) {
+        cudaMalloc(&prof, sizeof(long long) * kProfPhases * fp.p.cap);
+        cudaMemsetAsync(prof, 0, sizeof(long long) * kProfPhases * fp.p.cap, ctx->stream);
+        fp.p.prof = prof;
+    }
     const int e = launch_swarms(fp.p, problem, ctx->precision == SF_FP64, ctx->stream, &smem);
+    if (prof) {
+        std::vector<long long> h(size_t(kProfPhases) * fp.p.cap);
+        cudaMemcpyAsync(h.data(), prof, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream);
+        cudaStreamSynchronize(ctx->stream);
+        cudaFree(prof);
+        fp.p.prof = nullptr;
+        static const char* names[] = {"A1", "A2", "A3+", "pbest", "part", "csync", "gath", "B1", "B2", "step"};
+        double acc[10] = {0};
+        int iters = 0;
+        for (int k = 0; k < fp.p.cap; ++k) {
+            const long long* r = h.data() + size_t(k) * kProfPhases;
+            if (r[0] == 0) break;
+            ++iters;
+            const long long t[11] = {r[0], r[1], r[2], r[4], r[5], r[6], r[7], r[8], r[9], r[10], r[11]};
+            for (int i = 0; i < 10; ++i) if (t[i + 1] > t[i]) acc[i] += double(t[i + 1] - t[i]);
+        }
+        std::fprintf(stderr, "[phase] C=%d T=%d iters=%d cycles/iter:", fp.p.C, fp.p.nthreads, iters);
+        for (int i = 0; i < 10; ++i) std::fprintf(stderr, " %s=%.0f", names[i], iters ? acc[i] / iters : 0.0);
+        std::fprintf(stderr, " entries(it1)=%lld\n", h[3]);
+    }
     if (e != 0) return cuda_fail(cudaError_t(e), "fused swarm launch");
     if (ctx->timing) {
         cudaEventRecord(ctx->ev1, ctx->stream);

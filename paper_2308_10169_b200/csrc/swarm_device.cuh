@@ -269,15 +269,45 @@ inline __device__ int pair_count<float>(const Ctx<float>& c, int pl, int s, int 
     return cnt;
 }
 
-// First waypoint strictly inside obstacle o (geometry.hpp:217-218), FP64 always.
+// First waypoint strictly inside obstacle o (geometry.hpp:217-218).
 template <class T>
-__device__ int contain_count(const Ctx<T>& c, int pl, int o) {
+__device__ int contain_count_ref(const Ctx<T>& c, int pl, int o) {
     const double px = double(c.x[pl * c.D]), py = double(c.x[pl * c.D + c.W]);
     const int v0 = c.ooff[o], n = c.ooff[o + 1] - v0;
     const T* vb = c.vert + 2 * v0;
     return point_strictly_inside_ref(
         px, py, n, [vb](int i) { return double(vb[2 * i]); },
         [vb](int i) { return double(vb[2 * i + 1]); });
+}
+
+template <class T> __device__ int contain_count(const Ctx<T>& c, int pl, int o);
+template <> inline __device__ int contain_count<double>(const Ctx<double>& c, int pl, int o) {
+    return contain_count_ref(c, pl, o);
+}
+// FP32 engine: per edge one filtered cross c = orientation(a, b, p).  Certain
+// (|c| > B) on every edge means p is off every edge line (no boundary exit) and
+// the reference's rounded crossing test p.x < a.x + (b.x-a.x)(p.y-a.y)/(b.y-a.y)
+// equals the exact one, i.e. (c > 0) == (b.y > a.y); B also covers the FP64
+// rounding of that quotient (1e-13 M L term).  Otherwise: FP64 reference.
+template <> inline __device__ int contain_count<float>(const Ctx<float>& c, int pl, int o) {
+    const float px = c.x[pl * c.D], py = c.x[pl * c.D + c.W];
+    const float* bb = c.obb + 4 * o;
+    const float L = fmaxf(fmaxf(px, bb[2]) - fminf(px, bb[0]), fmaxf(py, bb[3]) - fminf(py, bb[1]));
+    const float M = fmaxf(fmaxf(fabsf(px), fabsf(py)), fmaxf(fmaxf(fabsf(bb[0]), fabsf(bb[2])),
+                                                             fmaxf(fabsf(bb[1]), fabsf(bb[3]))));
+    const float B = 2.9e-6f * L * L + 1e-13f * M * L + 4e-12f;
+    const int v0 = c.ooff[o], v1 = c.ooff[o + 1];
+    const float4* E = reinterpret_cast<const float4*>(c.edge);
+    bool inside = false;
+    for (int i = v0; i < v1; ++i) {
+        const float4 e = E[i];                       // a = (e.x, e.y), b - a = (e.z, e.w)
+        const float cr = fmaf(e.z, py - e.y, -(e.w * (px - e.x)));
+        if (!(fabsf(cr) > B)) return contain_count_ref(c, pl, o);
+        const int j = (i + 1 == v1) ? v0 : i + 1;
+        const float ay = e.y, by = c.vert[2 * j + 1];
+        if ((ay > py) != (by > py) && ((cr > 0.f) == (by > ay))) inside = !inside;
+    }
+    return inside ? 1 : 0;
 }
 
 template <class T>
@@ -344,7 +374,8 @@ __device__ void load_world(Ctx<T>& c, const unsigned char* wrec, int off_offsets
 //   A3  fitness = sum of lengths in chain order + alpha * Q^beta.
 // Entries beyond the list capacity are evaluated in place (correct, divergent).
 template <class T>
-__device__ void path_fitness_phase(const SwarmParams& p, Ctx<T>& c) {
+__device__ void path_fitness_phase(const SwarmParams& p, Ctx<T>& c, long long* prof = nullptr,
+                                   int k = 0) {
     const int tid = threadIdx.x, lane = tid & 31, nthr = blockDim.x;
     const int S = c.S, items = c.P * S, O = c.O;
     const int cap = p.entry_cap;
@@ -410,6 +441,7 @@ __device__ void path_fitness_phase(const SwarmParams& p, Ctx<T>& c) {
         }
     }
     __syncthreads();
+    if (prof) prof[(k - 1) * kProfPhases + 1] = clock64();
     // ---- A2
     const int np = min(c.m->n_pair, cap);
     for (int e = tid; e < np; e += nthr) {
@@ -419,6 +451,10 @@ __device__ void path_fitness_phase(const SwarmParams& p, Ctx<T>& c) {
         if (k) atomicAdd(&c.q[pl], k);
     }
     __syncthreads();
+    if (prof) {
+        prof[(k - 1) * kProfPhases + 2] = clock64();
+        prof[(k - 1) * kProfPhases + 3] = np;
+    }
     if (tid == 0) c.m->n_pair = 0;
     // ---- A3
     for (int pl = tid; pl < c.P; pl += nthr) {

@@ -66,6 +66,8 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
         p.roots ? splitmix64(splitmix64(p.roots[swarm] ^ p.tag_hash) + uint64_t(p.frame_index))
                 : p.seeds[swarm];
     const int G = c.G, N = c.N, D = c.D, R = c.R;
+    long long* const prof = (p.prof != nullptr && swarm == 0 && c.crank == 0 && tid == 0) ? p.prof : nullptr;
+#define SEPSO_MARK(ph) do { if (prof) prof[(k - 1) * kProfPhases + (ph)] = clock64(); } while (0)
 
     // ---------------------------------------------------------- constants
     const double* hyp_src = p.hypers + size_t(swarm) * size_t(p.hypers_stride);
@@ -128,9 +130,11 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
     int k = 1;
     for (; k <= p.cap; ++k) {
         const int buf = k & 1;
+        SEPSO_MARK(0);
         // fitness (geometry.hpp:262-267 / benchmarks.hpp:45-53)
-        if (PATH) path_fitness_phase(p, c);
+        if (PATH) path_fitness_phase(p, c, prof, k);
         else bench_fitness_phase(problem, c);
+        SEPSO_MARK(4);
         // pbest (runner.hpp:73-80) incl. the x -> pbest_x row copy; non-finite
         // detection (runner.hpp:56-61).  Same thread owns fit[pl] (A3 above).
         for (int pl = tid; pl < c.P; pl += nthr) {
@@ -146,6 +150,7 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
             if (PATH) c.q[pl] = 0;
         }
         __syncthreads();
+        SEPSO_MARK(5);
         // per-CTA group partials: (pbest_f, row) lexicographic min, one warp per group
         for (int lg = warp; lg < c.LG; lg += nthr >> 5) {
             const int g = gfirst + lg;
@@ -171,7 +176,9 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
             if (br != INT_MAX)
                 for (int d = lane; d < D; d += 32) c.px[(buf * LGM + lg) * D + d] = c.pb[br * D + d];
         }
+        SEPSO_MARK(6);
         cluster.sync();   // partials of every CTA visible cluster-wide
+        SEPSO_MARK(7);
 
         // gather partials (one DSMEM round trip, all threads in parallel)
         for (int t = tid; t < c.C * LGM + c.C; t += nthr) {
@@ -190,6 +197,7 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
             }
         }
         __syncthreads();
+        SEPSO_MARK(8);
         if (tid == 0) {
             Misc<T>* m = c.m;
             int bad = INT_MAX;
@@ -255,6 +263,7 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
             }
         }
         __syncthreads();
+        SEPSO_MARK(9);
         if (c.m->status) break;
         // copy improved group bests (and the new tbest) from their owners' partials
         {
@@ -272,6 +281,7 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
             }
         }
         __syncthreads();
+        SEPSO_MARK(10);
         if (c.m->stop) break;
         if (k == p.cap) break;        // plan_frame: no step after the last iteration
         // --------------------------------------------------- step k (swarm.hpp:138-174)
@@ -296,6 +306,7 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
             }
         }
         __syncthreads();
+        SEPSO_MARK(11);
     }
 
     // ---------------------------------------------------------------- results

@@ -80,7 +80,10 @@ struct SwarmParams {
     double* win_vals; int* win_len;
     // outputs
     SwarmOut* out; double* best_x; double* trace;
+    // debug: per-iteration phase timestamps of swarm 0 / CTA 0 (SEPSO_PHASE_PROF)
+    long long* prof;
 };
+constexpr int kProfPhases = 12;
 
 struct SmemLayout {
     size_t x, v, pb, pbf, pbq, q, fit, imp, seglen, coef, lo, hi, hyp, gbx, gbf, gbq, chg, tbx,

@@ -297,3 +297,32 @@ def test_invalid_arguments_raise(eng32):
         eng32.plan_frame(w, None, EVOLVED_PATH_HYPERS[:3], pe.PlannerConfig(), 1)
     with pytest.raises(ValueError):
         eng32.run_dtpso("BF1", DEFAULT_GROUP_HYPERS, 8, 10, 0, 1)
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_general_polygons_q(prec, eng32, eng64):
+    """Non-rectangular, concave and sliver polygons (the FP32 filtered paths:
+    vertex-cross early exit, containment) agree with the oracle on Q."""
+    eng = eng64 if prec == "fp64" else eng32
+    rng = np.random.default_rng(9)
+    for trial in range(40):
+        polys = []
+        for _ in range(int(rng.integers(1, 9))):
+            cx, cy = rng.uniform(20, 180, 2)
+            n = int(rng.integers(3, 9))
+            ang = np.sort(rng.uniform(0, 2 * np.pi, n))
+            rad = rng.uniform(3, 25, n) * (rng.uniform(0.2, 1.0, n) if trial % 2 else 1.0)
+            poly = np.stack([cx + rad * np.cos(ang), cy + rad * np.sin(ang)], 1)
+            if trial % 5 == 0:          # a near-degenerate sliver edge
+                poly = np.vstack([poly, poly[-1] + 1e-4])
+            polys.append(np.clip(poly, 0, 200))
+        w = pe.PolygonWorld(200, 200, rng.uniform(0, 200, 2), rng.uniform(0, 200, 2), polys)
+        if prec == "fp32":
+            w = float_world(w)
+        D = 2 * int(rng.integers(1, 9))
+        xs = rng.uniform(0, 200, (256, D))
+        if prec == "fp32":
+            xs = xs.astype(np.float32).astype(np.float64)
+        f, q = eng.eval_path_rows(w, xs, D)
+        fo, qo = oracle_eval(w, xs, D)
+        assert np.array_equal(q, qo), trial

@@ -1,0 +1,14 @@
+"""Per-phase cycle breakdown of the fused kernel (SEPSO_PHASE_PROF=1)."""
+import os, sys
+os.environ["SEPSO_PHASE_PROF"] = "1"
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2308_10169_b200 as pe
+eng = pe.Engine(0, sys.argv[1] if len(sys.argv) > 1 else "fp32")
+planner = pe.PlannerConfig(max_iters_per_frame=30, window_carryover=True)
+for C, T in ((8, 512), (16, 256), (16, 512)):
+    eng.set_launch(C, T)
+    sb = pe.SceneBatch(eng, [pe.ScenarioConfig(root_seed=3)], planner, pe.EVOLVED_PATH_HYPERS, 6)
+    sb.run(6)
+    sb.records(0, 6)
+    sb.close()
