@@ -169,8 +169,9 @@ template <class T> struct Ctx {
     int G, N, D, W, S, R, P, row0, LG, O, C, crank;
     FastDiv fS, fD, fN;
     // shared arrays
-    T *x, *v, *pb, *pbf, *fit, *seglen, *coef, *lo, *hi, *hyp, *gbx, *gbf, *tbx, *pf, *px, *allf;
-    int *pbq, *q, *imp, *gbq, *chg, *prow, *pq, *allrow, *allq, *ooff, *ofl;
+    T *x, *v, *pb, *pbf, *fit, *seglen, *coef, *lo, *hi, *hyp, *gbx, *gbf, *tbx, *px;
+    int *pbq, *q, *imp, *gbq, *chg, *ooff, *ofl, *allbad, *gtab, *ctab;
+    Part *part, *allpart;
     T *obb, *vert, *edge;
     double* win;
     uint32_t* list;
@@ -314,6 +315,19 @@ template <class T>
 __device__ __forceinline__ bool box_overlap(T lx, T ly, T hx, T hy, const T* bb, T m) {
     return lx <= bb[2] + m && bb[0] <= hx + m && ly <= bb[3] + m && bb[1] <= hy + m;
 }
+template <>
+__device__ __forceinline__ bool box_overlap<float>(float lx, float ly, float hx, float hy,
+                                                   const float* bb, float m) {
+    const float4 b = *reinterpret_cast<const float4*>(bb);      // one LDS.128
+    return lx <= b.z + m && b.x <= hx + m && ly <= b.w + m && b.y <= hy + m;
+}
+
+// Total order key for a fitness value: orderable bits (+0 canonical), so the
+// group argmin can use 32-bit warp reductions (REDUX).
+__device__ __forceinline__ uint32_t order_key(float f) {
+    const uint32_t u = __float_as_uint(f == 0.f ? 0.f : f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
 
 // Stage one world record (double) into shared memory as T: vertices, edge
 // records (b1, b2 - b1), obstacle boxes (geometry.hpp:167-177) and the
@@ -397,6 +411,7 @@ __device__ void path_fitness_phase(const SwarmParams& p, Ctx<T>& c, long long* p
                 uint32_t mask = 0;
                 if (act) {
                     const int oe = min(32, O - o0);
+#pragma unroll 8
                     for (int j = 0; j < oe; ++j)
                         if (box_overlap(lx, ly, hx, hy, c.obb + 4 * (o0 + j), c.margin)) mask |= 1u << j;
                 }

@@ -56,11 +56,10 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
     c.seglen = (T*)S8(L.seglen); c.coef = (T*)S8(L.coef); c.lo = (T*)S8(L.lo); c.hi = (T*)S8(L.hi);
     c.hyp = (T*)S8(L.hyp); c.gbx = (T*)S8(L.gbx); c.gbf = (T*)S8(L.gbf); c.gbq = (int*)S8(L.gbq);
     c.chg = (int*)S8(L.chg); c.tbx = (T*)S8(L.tbx); c.win = (double*)S8(L.win);
-    c.pf = (T*)S8(L.pf); c.prow = (int*)S8(L.prow); c.pq = (int*)S8(L.pq); c.px = (T*)S8(L.px);
-    c.allf = (T*)S8(L.allf); c.allrow = (int*)S8(L.allrow); c.allq = (int*)S8(L.allq);
+    c.part = (Part*)S8(L.part); c.px = (T*)S8(L.px); c.allpart = (Part*)S8(L.allpart);
+    c.allbad = (int*)S8(L.allbad); c.gtab = (int*)S8(L.gtab); c.ctab = (int*)S8(L.ctab);
     c.obb = (T*)S8(L.obb); c.ooff = (int*)S8(L.ooff); c.ofl = (int*)S8(L.ofl); c.vert = (T*)S8(L.vert);
     c.edge = (T*)S8(L.edge); c.list = (uint32_t*)S8(L.list); c.m = (Misc<T>*)S8(L.misc);
-    int* allbad = c.allrow + c.C * p.max_local_groups;
     const int LGM = p.max_local_groups;
     const uint64_t seed =
         p.roots ? splitmix64(splitmix64(p.roots[swarm] ^ p.tag_hash) + uint64_t(p.frame_index))
@@ -90,7 +89,12 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
     }
     if (p.carry)
         for (int i = tid; i < p.tw; i += nthr) c.win[i] = p.win_vals[size_t(swarm) * p.tw + i];
-    for (int g = tid; g < G; g += nthr) { c.gbf[g] = A::inf(); c.gbq[g] = 0; c.chg[g] = -1; }
+    for (int g = tid; g < G; g += nthr) {
+        c.gbf[g] = A::inf(); c.gbq[g] = 0; c.chg[g] = -1;
+        c.gtab[2 * g] = (g * N) / p.rows_per_cta;               // CTAs owning group g
+        c.gtab[2 * g + 1] = ((g + 1) * N - 1) / p.rows_per_cta;
+    }
+    for (int cc = tid; cc < c.C; cc += nthr) c.ctab[cc] = (cc * p.rows_per_cta) / N;
     for (int pl = tid; pl < c.P; pl += nthr) { c.pbf[pl] = A::inf(); c.pbq[pl] = 0; c.q[pl] = 0; }
     __syncthreads();
 
@@ -145,7 +149,12 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
                 c.pbq[pl] = c.q[pl];
                 const T* xs = c.x + pl * D;
                 T* ps = c.pb + pl * D;
-                for (int d = 0; d < D; ++d) ps[d] = xs[d];
+                if (sizeof(T) == 4 && (D & 3) == 0) {
+                    for (int d = 0; d < D; d += 4)
+                        *reinterpret_cast<float4*>(ps + d) = *reinterpret_cast<const float4*>(xs + d);
+                } else {
+                    for (int d = 0; d < D; ++d) ps[d] = xs[d];
+                }
             }
             if (PATH) c.q[pl] = 0;
         }
@@ -156,22 +165,29 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
             const int g = gfirst + lg;
             const int l0 = max(c.row0, g * N) - c.row0, l1 = min(row1, (g + 1) * N) - c.row0;
             T bf = A::inf();
-            int br = INT_MAX, bq = 0;
+            int br = INT_MAX;
             for (int pl = l0 + lane; pl < l1; pl += 32) {
                 const T f = c.pbf[pl];
-                if (f < bf) { bf = f; br = pl; bq = c.pbq[pl]; }   // lanes scan ascending
+                if (f < bf) { bf = f; br = pl; }                    // lanes scan ascending
             }
-            for (int off = 16; off; off >>= 1) {
-                const T of = __shfl_down_sync(0xffffffffu, bf, off);
-                const int orow = __shfl_down_sync(0xffffffffu, br, off);
-                const int oq = __shfl_down_sync(0xffffffffu, bq, off);
-                if (of < bf || (of == bf && orow < br)) { bf = of; br = orow; bq = oq; }
+            if (sizeof(T) == 4) {
+                const uint32_t key = order_key(float(bf));
+                const uint32_t kmin = __reduce_min_sync(0xffffffffu, key);
+                br = int(__reduce_min_sync(0xffffffffu, key == kmin ? uint32_t(br) : 0xffffffffu));
+            } else {
+                for (int off = 16; off; off >>= 1) {
+                    const T of = __shfl_xor_sync(0xffffffffu, bf, off);
+                    const int orow = __shfl_xor_sync(0xffffffffu, br, off);
+                    if (of < bf || (of == bf && orow < br)) { bf = of; br = orow; }
+                }
             }
             br = __shfl_sync(0xffffffffu, br, 0);
             if (lane == 0) {
-                c.pf[buf * LGM + lg] = bf;
-                c.prow[buf * LGM + lg] = br == INT_MAX ? INT_MAX : br + c.row0;
-                c.pq[buf * LGM + lg] = bq;
+                Part pt;
+                pt.f = br == INT_MAX ? double(A::inf()) : double(c.pbf[br]);
+                pt.row = br == INT_MAX ? INT_MAX : br + c.row0;
+                pt.q = br == INT_MAX ? 0 : c.pbq[br];
+                c.part[buf * LGM + lg] = pt;
             }
             if (br != INT_MAX)
                 for (int d = lane; d < D; d += 32) c.px[(buf * LGM + lg) * D + d] = c.pb[br * D + d];
@@ -184,82 +200,106 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
         for (int t = tid; t < c.C * LGM + c.C; t += nthr) {
             if (t < c.C * LGM) {
                 const int cc = t / LGM, lg = t - cc * LGM;
-                const T* rpf = cluster.map_shared_rank(c.pf, cc);
-                const int* rrow = cluster.map_shared_rank(c.prow, cc);
-                const int* rq = cluster.map_shared_rank(c.pq, cc);
-                c.allf[t] = rpf[buf * LGM + lg];
-                c.allrow[t] = rrow[buf * LGM + lg];
-                c.allq[t] = rq[buf * LGM + lg];
+                const Part* rp = cluster.map_shared_rank(c.part, cc);
+                c.allpart[t] = rp[buf * LGM + lg];
             } else {
                 const int cc = t - c.C * LGM;
                 const Misc<T>* rm = cluster.map_shared_rank(c.m, cc);
-                allbad[cc] = rm->bad_row;
+                c.allbad[cc] = rm->bad_row;
             }
         }
         __syncthreads();
         SEPSO_MARK(8);
-        if (tid == 0) {
+        if (warp == 0) {
+            // gbest, one lane per group: scan the owning CTAs in row order,
+            // strict '<' vs the incumbent (runner.hpp:81-87)
             Misc<T>* m = c.m;
             int bad = INT_MAX;
-            for (int cc = 0; cc < c.C; ++cc) bad = min(bad, allbad[cc]);
+            for (int cc = lane; cc < c.C; cc += 32) bad = min(bad, c.allbad[cc]);
+            bad = int(__reduce_min_sync(0xffffffffu, uint32_t(bad)));
             if (bad != INT_MAX) {
-                m->status = 2; m->bad_min = bad; m->stop = 1;
+                if (lane == 0) { m->status = 2; m->bad_min = bad; m->stop = 1; }
             } else {
-                // gbest: scan n ascending, strict '<' vs the incumbent (runner.hpp:81-87)
-                const int Rc = p.rows_per_cta;
-                for (int g = 0; g < G; ++g) {
-                    const int cf = (g * N) / Rc, cl = ((g + 1) * N - 1) / Rc;
-                    T bf = A::inf();
+                T tv = A::inf();
+                int tg = INT_MAX;
+                for (int g = lane; g < G; g += 32) {
+                    const int cf = c.gtab[2 * g], cl = c.gtab[2 * g + 1];
+                    double bf = double(A::inf());
                     int bslot = -1, bq = 0;
                     for (int cc = cf; cc <= cl; ++cc) {
-                        const int lg = g - (cc * Rc) / N;
-                        const int slot = cc * LGM + lg;
-                        if (c.allf[slot] < bf) { bf = c.allf[slot]; bslot = slot; bq = c.allq[slot]; }
+                        const int slot = cc * LGM + (g - c.ctab[cc]);
+                        const Part pt = c.allpart[slot];
+                        if (pt.f < bf) { bf = pt.f; bslot = slot; bq = pt.q; }
                     }
-                    if (bf < c.gbf[g]) { c.gbf[g] = bf; c.gbq[g] = bq; c.chg[g] = bslot; }
+                    if (T(bf) < c.gbf[g]) { c.gbf[g] = T(bf); c.gbq[g] = bq; c.chg[g] = bslot; }
                     else c.chg[g] = -1;
+                    if (c.gbf[g] < tv) { tv = c.gbf[g]; tg = g; }       // per-lane, g ascending
                 }
-                // tbest: scan g ascending, strict '<' (runner.hpp:88-91)
-                int tg = -1;
-                for (int g = 0; g < G; ++g)
-                    if (c.gbf[g] < m->tbf) { m->tbf = c.gbf[g]; m->tbq = c.gbq[g]; tg = g; }
-                m->tsrc_slot = tg >= 0 ? tg : -1;
-                if (c.crank == 0) p.trace[size_t(swarm) * p.cap + (k - 1)] = double(m->tbf);
-                // window push + trim to tw (planner.hpp:179-180)
-                const double tv = double(m->tbf);
-                if (p.tw <= 0) {
-                } else if (m->win_len < p.tw) {
-                    c.win[(m->win_head + m->win_len) % p.tw] = tv;
-                    ++m->win_len;
-                } else {
-                    c.win[m->win_head] = tv;
-                    m->win_head = (m->win_head + 1) % p.tw;
+                // tbest: (gbest_f, g) lexicographic min over groups, strict '<'
+                // vs the incumbent (runner.hpp:88-91)
+                for (int off = 16; off; off >>= 1) {
+                    const T ov = __shfl_xor_sync(0xffffffffu, tv, off);
+                    const int og = __shfl_xor_sync(0xffffffffu, tg, off);
+                    if (ov < tv || (ov == tv && og < tg)) { tv = ov; tg = og; }
                 }
-                // auto truncation (planner.hpp:181-187, 138-149), Q(tbest) tracked;
-                // the std is only needed when the cheap conjuncts hold
-                if (p.auto_truncate && m->win_len >= p.tw && m->tbq == 0) {
-                    double mean = 0.0;
-                    for (int i = 0; i < p.tw; ++i) mean = __dadd_rn(mean, c.win[(m->win_head + i) % p.tw]);
-                    mean = __ddiv_rn(mean, double(p.tw));
-                    double var = 0.0;
-                    for (int i = 0; i < p.tw; ++i) {
-                        const double dv = __dsub_rn(c.win[(m->win_head + i) % p.tw], mean);
-                        var = __dadd_rn(var, __dmul_rn(dv, dv));
+                if (lane == 0) {
+                    if (tv < m->tbf) { m->tbf = tv; m->tbq = c.gbq[tg]; m->tsrc_slot = tg; }
+                    else m->tsrc_slot = -1;
+                    if (c.crank == 0) p.trace[size_t(swarm) * p.cap + (k - 1)] = double(m->tbf);
+                    // window push + trim to tw (planner.hpp:179-180)
+                    const double wv = double(m->tbf);
+                    int wl = m->win_len, wh = m->win_head;
+                    if (p.tw <= 0) {
+                    } else if (wl < p.tw) {
+                        int at = wh + wl;
+                        if (at >= p.tw) at -= p.tw;
+                        c.win[at] = wv;
+                        ++wl;
+                    } else {
+                        c.win[wh] = wv;
+                        if (++wh == p.tw) wh = 0;
                     }
-                    var = __ddiv_rn(var, double(p.tw));
-                    if (__dsqrt_rn(var) < p.delta) { m->truncated = 1; m->stop = 1; }
+                    m->win_len = wl;
+                    m->win_head = wh;
+                    // auto truncation (planner.hpp:181-187, 138-149) with Q(tbest)
+                    // tracked; the std only when the cheap conjuncts hold
+                    if (p.auto_truncate && wl >= p.tw && m->tbq == 0) {
+                        double mean = 0.0;
+                        for (int i = 0, at = wh; i < p.tw; ++i) {
+                            mean = __dadd_rn(mean, c.win[at]);
+                            if (++at == p.tw) at = 0;
+                        }
+                        mean = __ddiv_rn(mean, double(p.tw));
+                        double var = 0.0;
+                        for (int i = 0, at = wh; i < p.tw; ++i) {
+                            const double dv = __dsub_rn(c.win[at], mean);
+                            var = __dadd_rn(var, __dmul_rn(dv, dv));
+                            if (++at == p.tw) at = 0;
+                        }
+                        var = __ddiv_rn(var, double(p.tw));
+                        if (__dsqrt_rn(var) < p.delta) { m->truncated = 1; m->stop = 1; }
+                    }
                 }
             }
-            m->k_done = k;
+            if (lane == 0) m->k_done = k;
         } else if (k < p.cap) {
             // meanwhile: this step's draws (draw_step_randoms, swarm.hpp:59-70) --
             // they depend only on (seed, k, row), not on the bests
             const uint64_t base = 2ull * uint64_t(R) * uint64_t(D) + uint64_t(k - 1) * 3ull * uint64_t(R);
-            for (int t = tid - 1; t < 3 * c.P; t += nthr - 1) {
+            for (int t = tid - 32; t < 3 * c.P; t += nthr - 32) {
                 const int j = t >= 2 * c.P ? 2 : (t >= c.P ? 1 : 0), pl = t - j * c.P;
                 const int row = c.row0 + pl, g = int(c.fN.div(uint32_t(row)));
                 const T u = unit_from_word<T>(philox_word(seed, base + uint64_t(j) * R + row));
                 c.coef[j * c.P + pl] = A::mul(c.hyp[g * 6 + j], u);   // a_j = c_j * r_j
+            }
+        }
+        if (nthr == 32 && k < p.cap) {   // single-warp CTA: draws after the bests
+            const uint64_t base = 2ull * uint64_t(R) * uint64_t(D) + uint64_t(k - 1) * 3ull * uint64_t(R);
+            for (int t = tid; t < 3 * c.P; t += 32) {
+                const int j = t >= 2 * c.P ? 2 : (t >= c.P ? 1 : 0), pl = t - j * c.P;
+                const int row = c.row0 + pl, g = int(c.fN.div(uint32_t(row)));
+                const T u = unit_from_word<T>(philox_word(seed, base + uint64_t(j) * R + row));
+                c.coef[j * c.P + pl] = A::mul(c.hyp[g * 6 + j], u);
             }
         }
         __syncthreads();
@@ -354,12 +394,18 @@ static int launch_t(const SwarmParams& p, int problem, cudaStream_t st, size_t* 
     const SmemLayout L = smem_layout(p, sizeof(T), PATH);
     if (smem_out) *smem_out = L.total;
     auto kern = swarm_kernel<T, PATH>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(L.total));
-    if (e != cudaSuccess) return int(e);
-    if (p.C > 8) {
+    cudaError_t e = cudaSuccess;
+    static thread_local size_t smem_set = 0;     // attributes are sticky per function
+    static thread_local bool nonportable = false;
+    if (L.total > smem_set) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.total));
+        if (e != cudaSuccess) return int(e);
+        smem_set = L.total;
+    }
+    if (p.C > 8 && !nonportable) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return int(e);
+        nonportable = true;
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(p.n_swarms * p.C));

@@ -85,9 +85,16 @@ struct SwarmParams {
 };
 constexpr int kProfPhases = 12;
 
+// One CTA's best (pbest_f, row) of one group, read by its peers over DSMEM in
+// a single 16-byte load.
+struct Part {
+    double f;
+    int row, q;
+};
+
 struct SmemLayout {
     size_t x, v, pb, pbf, pbq, q, fit, imp, seglen, coef, lo, hi, hyp, gbx, gbf, gbq, chg, tbx,
-        win, pf, prow, pq, px, allf, allrow, allq, obb, ooff, ofl, vert, edge, list, misc, total;
+        win, part, px, allpart, allbad, gtab, ctab, obb, ooff, ofl, vert, edge, list, misc, total;
 };
 
 #ifdef __CUDACC__
@@ -126,13 +133,12 @@ SEPSO_LHD SmemLayout smem_layout(const SwarmParams& p, size_t tsz, bool path) {
     L.chg = take(G * 4);
     L.tbx = take(D * tsz);
     L.win = take(size_t(p.tw) * 8);
-    L.pf = take(2 * LG * tsz);
-    L.prow = take(2 * LG * 4);
-    L.pq = take(2 * LG * 4);
+    L.part = take(2 * LG * 16);            // double-buffered group partials (Part)
     L.px = take(2 * LG * D * tsz);
-    L.allf = take(C * LG * tsz);
-    L.allrow = take(C * LG * 4 + C * 4);   // + per-CTA bad row
-    L.allq = take(C * LG * 4);
+    L.allpart = take(C * LG * 16);         // gathered partials of the cluster
+    L.allbad = take(C * 4);                // per-CTA first non-finite row
+    L.gtab = take(G * 8);                  // per group: first / last owning CTA
+    L.ctab = take(C * 4);                  // per CTA: first group
     L.obb = take(O * 4 * tsz);
     L.ooff = take((O + 1) * 4);
     L.ofl = take(O * 4);
