@@ -201,7 +201,11 @@ FusedPlan plan_fused(sf_ctx* ctx, int problem, int n_swarms, int G, int N, int D
     const int want_c = ctx->force_cluster ? ctx->force_cluster : env_int("SEPSO_CLUSTER", 0);
     const int want_t = ctx->force_threads ? ctx->force_threads : env_int("SEPSO_THREADS", 0);
     // latency-oriented default: ~192 particle rows per CTA, up to 16 CTAs per cluster
-    int C = want_c > 0 ? want_c : std::max(1, std::min(16, (R + 191) / 192));
+    // latency mode (few swarms): spread one swarm over up to 16 SMs (~96 rows per
+    // CTA); throughput mode (many swarms): ~384 rows per CTA, fewer cluster syncs
+    const bool latency = n_swarms * 16 <= 2 * 148;
+    const int rows_target = latency ? 96 : 384;
+    int C = want_c > 0 ? want_c : std::max(1, std::min(16, (R + rows_target - 1) / rows_target));
     for (;; C *= 2) {
         if (C > 16) C = 16;
         const int Rc = (R + C - 1) / C;
@@ -214,8 +218,9 @@ FusedPlan plan_fused(sf_ctx* ctx, int problem, int n_swarms, int G, int N, int D
         }
         p.max_local_groups = lgm;
         if (path) {
-            p.entry_cap = std::min(std::max(1024, Rc * S * 2), 6144);
-            p.nthreads = std::min(512, std::max(128, ((Rc * S / 3) + 31) / 32 * 32));
+            // worst case Rc*S*O entries; beyond the capacity entries are evaluated in place
+            p.entry_cap = std::min(std::max(1024, Rc * S * std::max(max_obs, 1)), 8192);
+            p.nthreads = std::min(512, std::max(128, ((Rc * S) + 31) / 32 * 32));
         } else {
             p.entry_cap = 0;
             p.nthreads = std::min(512, std::max(32, (Rc + 31) / 32 * 32));
