@@ -226,6 +226,10 @@ int sf_scene_batch_destroy(sf_scene_batch* b);
 /* FP32 FFMA throughput of the device (TFLOP/s): roofline denominator probe. */
 int sf_measure_fp32_peak(sf_ctx* ctx, double* tflops);
 
+/* Benchmark hygiene: when bytes > 0, sf_run_scenario writes a device buffer of
+ * that size (flushing L2) before each frame, outside the frame's wall time. */
+int sf_ctx_set_l2_flush(sf_ctx* ctx, uint64_t bytes);
+
 /* Bytes moved host->device and device->host by the last host-buffer call. */
 int sf_ctx_last_io_bytes(sf_ctx* ctx, uint64_t* h2d, uint64_t* d2h);
 

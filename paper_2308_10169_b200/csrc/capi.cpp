@@ -291,6 +291,7 @@ int sf_ctx_destroy(sf_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     ctx->io.release();
     ctx->scratch.release();
+    ctx->flush.release();
     ctx->hio.release();
     cudaEventDestroy(ctx->ev0);
     cudaEventDestroy(ctx->ev1);
@@ -991,7 +992,15 @@ int sf_run_scenario(sf_ctx* ctx, const sf_scenario_config* c, int variant, uint3
     std::vector<double> prev(cfg.dim), win(std::max<uint32_t>(cfg.tw, 1) + 1);
     uint32_t wl = 0;
     bool have_prev = false;
+    if (ctx->l2_flush) {
+        const cudaError_t fe = ctx->flush.ensure(ctx->l2_flush);
+        if (fe != cudaSuccess) return cuda_fail(fe, "l2 flush buffer");
+    }
     for (uint32_t f = 0; f < frames; ++f) {
+        if (ctx->l2_flush) {
+            cudaMemsetAsync(ctx->flush.p, int(f & 0xff), ctx->l2_flush, ctx->stream);
+            cudaStreamSynchronize(ctx->stream);
+        }
         std::vector<double> bp(cfg.dim);
         st = sf_plan_frame(ctx, &w, have_prev ? prev.data() : nullptr, hyp.data(), &cfg,
                            derive_seed(c->root_seed, "plan", f), win.data(), &wl, uint32_t(win.size()),
@@ -1002,6 +1011,12 @@ int sf_run_scenario(sf_ctx* ctx, const sf_scenario_config* c, int variant, uint3
         if (best) std::copy(bp.begin(), bp.end(), best + size_t(f) * cfg.dim);
         if ((st = sf_step_world(&w, verts.data(), vel.data(), c->dt))) return st;
     }
+    return SF_OK;
+}
+
+int sf_ctx_set_l2_flush(sf_ctx* ctx, uint64_t bytes) {
+    if (!ctx) return fail(SF_INVALID_ARGUMENT, "ctx is null");
+    ctx->l2_flush = bytes;
     return SF_OK;
 }
 

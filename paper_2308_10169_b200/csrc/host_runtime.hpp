@@ -46,7 +46,8 @@ struct sf_ctx {
     uint64_t launches = 0;
     int force_cluster = 0, force_threads = 0;
     uint64_t last_h2d = 0, last_d2h = 0;
-    sepso::DevBuf io, scratch;
+    uint64_t l2_flush = 0;
+    sepso::DevBuf io, scratch, flush;
     sepso::PinnedBuf hio;
 };
 

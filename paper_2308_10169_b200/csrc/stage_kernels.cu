@@ -479,7 +479,11 @@ __global__ void k_finish(int D, const unsigned char* __restrict__ cands, int n_c
                     win[st->win_head] = tv;
                     st->win_head = (st->win_head + 1) % tw;
                 }
-                if (auto_truncate && st->win_len >= tw) {
+                int newest = st->win_head + st->win_len - 1;
+                if (newest >= tw) newest -= tw;
+                const double gap = fabs(win[newest] - win[st->win_head]);
+                const bool may_fire = !(gap >= delta * sqrt(2.0 * tw) * (1.0 + 1e-9));
+                if (auto_truncate && st->win_len >= tw && st->tbest_q == 0 && may_fire) {
                     double mean = 0.0;
                     for (int i = 0; i < tw; ++i) mean = __dadd_rn(mean, win[(st->win_head + i) % tw]);
                     mean = __ddiv_rn(mean, double(tw));
@@ -489,7 +493,7 @@ __global__ void k_finish(int D, const unsigned char* __restrict__ cands, int n_c
                         var = __dadd_rn(var, __dmul_rn(dv, dv));
                     }
                     var = __ddiv_rn(var, double(tw));
-                    if (__dsqrt_rn(var) < delta && st->tbest_q == 0) {
+                    if (__dsqrt_rn(var) < delta) {
                         st->truncated = 1;
                         st->stop = 1;
                     }

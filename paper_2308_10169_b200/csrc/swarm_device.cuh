@@ -444,15 +444,20 @@ __device__ void path_fitness_phase(const SwarmParams& p, Ctx<T>& c, long long* p
             s += step_s;
             if (s >= S) { s -= S; ++pl; }
         }
-        // first waypoint strictly inside an obstacle (geometry.hpp:217-218)
-        for (int q = tid; q < c.P; q += nthr) {
-            const T wx = c.x[q * c.D], wy = c.x[q * c.D + c.W];
+        // first waypoint strictly inside an obstacle (geometry.hpp:217-218):
+        // particle tasks continue the item index space so they land on the
+        // threads with the fewest items
+        for (int t = tid - (items % nthr); t < c.P; t += nthr) {
+            if (t < 0) continue;
+            const T wx = c.x[t * c.D], wy = c.x[t * c.D + c.W];
+            int hits = 0;
             for (int o = 0; o < O; ++o) {
                 const T* bb = c.obb + 4 * o;
                 if (wx >= bb[0] - c.margin && wx <= bb[2] + c.margin && wy >= bb[1] - c.margin &&
-                    wy <= bb[3] + c.margin && contain_count(c, q, o))
-                    atomicAdd(&c.q[q], 1);
+                    wy <= bb[3] + c.margin)
+                    hits += contain_count(c, t, o);
             }
+            if (hits) atomicAdd(&c.q[t], hits);
         }
     }
     __syncthreads();
@@ -462,8 +467,8 @@ __device__ void path_fitness_phase(const SwarmParams& p, Ctx<T>& c, long long* p
     for (int e = tid; e < np; e += nthr) {
         const uint32_t w = c.list[e];
         const int pl = int(w >> 19), s = int((w >> 11) & 0xffu), o = int(w & 0x7ffu);
-        const int k = pair_count(c, pl, s, o);
-        if (k) atomicAdd(&c.q[pl], k);
+        const int hits = pair_count(c, pl, s, o);
+        if (hits) atomicAdd(&c.q[pl], hits);
     }
     __syncthreads();
     if (prof) {

@@ -263,7 +263,14 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
                     m->win_head = wh;
                     // auto truncation (planner.hpp:181-187, 138-149) with Q(tbest)
                     // tracked; the std only when the cheap conjuncts hold
-                    if (p.auto_truncate && wl >= p.tw && m->tbq == 0) {
+                    // Exact skip: a window of n values with range r has population
+                    // std >= r / sqrt(2n); the newest-oldest gap bounds r from below.
+                    int oldest = wh;
+                    int newest = wh + wl - 1;
+                    if (newest >= p.tw) newest -= p.tw;
+                    const double gap = fabs(c.win[newest] - c.win[oldest]);
+                    const bool may_fire = !(gap >= p.delta * sqrt(2.0 * p.tw) * (1.0 + 1e-9));
+                    if (p.auto_truncate && wl >= p.tw && m->tbq == 0 && may_fire) {
                         double mean = 0.0;
                         for (int i = 0, at = wh; i < p.tw; ++i) {
                             mean = __dadd_rn(mean, c.win[at]);

@@ -37,7 +37,7 @@ ABI_SYMBOLS = [
     "sf_update_bests", "sf_eval_path_rows", "sf_eval_bench_rows", "sf_should_truncate",
     "sf_generate_world", "sf_step_world", "sf_run_scenario", "sf_scene_batch_create",
     "sf_scene_batch_run", "sf_scene_batch_records", "sf_scene_batch_destroy",
-    "sf_ctx_last_io_bytes", "sf_measure_fp32_peak",
+    "sf_ctx_last_io_bytes", "sf_measure_fp32_peak", "sf_ctx_set_l2_flush",
 ]
 
 
@@ -165,6 +165,7 @@ def lib():
         "sf_scene_batch_destroy": (C.c_int, [C.c_void_p]),
         "sf_ctx_last_io_bytes": (C.c_int, [C.c_void_p, _u64p, _u64p]),
         "sf_measure_fp32_peak": (C.c_int, [C.c_void_p, _dp]),
+        "sf_ctx_set_l2_flush": (C.c_int, [C.c_void_p, C.c_uint64]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -410,6 +411,9 @@ class Engine:
 
     def enable_timing(self, on=True):
         _check(self._L.sf_ctx_enable_timing(self._h, int(on)))
+
+    def set_l2_flush(self, nbytes: int):
+        _check(self._L.sf_ctx_set_l2_flush(self._h, nbytes))
 
     def measure_fp32_peak(self):
         t = C.c_double(0)
