@@ -207,6 +207,7 @@ int run_batch(sf_ctx* ctx, const BatchIn& b, BatchOut& r) {
     p.alpha = b.alpha;
     p.beta = b.beta;
     p.beta_int = beta_integer(b.beta);
+    p.at_gap = b.delta * std::sqrt(2.0 * double(b.tw)) * (1.0 + 1e-9);
     p.delta = b.delta;
     p.pi_radius = b.pi_radius;
     p.warm = b.warm;
@@ -1112,6 +1113,7 @@ int sf_scene_batch_create(sf_ctx* ctx, uint32_t n, const sf_scenario_config* cfg
     p.alpha = cfg->alpha;
     p.beta = cfg->beta;
     p.beta_int = beta_integer(cfg->beta);
+    p.at_gap = cfg->delta * std::sqrt(2.0 * double(cfg->tw)) * (1.0 + 1e-9);
     p.delta = cfg->delta;
     p.pi_radius = cfg->pi_radius;
     p.warm = int(cfg->gamma * double(cfg->per_group));

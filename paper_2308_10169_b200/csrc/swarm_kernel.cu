@@ -182,40 +182,40 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
                 }
             }
             br = __shfl_sync(0xffffffffu, br, 0);
-            if (lane == 0) {
-                Part pt;
-                pt.f = br == INT_MAX ? double(A::inf()) : double(c.pbf[br]);
-                pt.row = br == INT_MAX ? INT_MAX : br + c.row0;
-                pt.q = br == INT_MAX ? 0 : c.pbq[br];
-                c.part[buf * LGM + lg] = pt;
+            // push (value, row, q) and the row itself into every peer's slot
+            // (crank, lg) of buffer buf: after the cluster barrier all reads are local
+            const int slot = c.crank * LGM + lg;
+            Part pt;
+            pt.f = br == INT_MAX ? double(A::inf()) : double(c.pbf[br]);
+            pt.row = br == INT_MAX ? INT_MAX : br + c.row0;
+            pt.q = br == INT_MAX ? 0 : c.pbq[br];
+            for (int r = lane; r < c.C; r += 32) {
+                Part* rp = cluster.map_shared_rank(c.part, r);
+                rp[buf * c.C * LGM + slot] = pt;
             }
             if (br != INT_MAX)
-                for (int d = lane; d < D; d += 32) c.px[(buf * LGM + lg) * D + d] = c.pb[br * D + d];
+                for (int t = lane; t < c.C * D; t += 32) {
+                    const int r = int(c.fD.div(uint32_t(t))), d = t - r * D;
+                    T* rx = cluster.map_shared_rank(c.px, r);
+                    rx[(buf * c.C * LGM + slot) * D + d] = c.pb[br * D + d];
+                }
+        }
+        if (tid < c.C) {
+            int* rb = cluster.map_shared_rank(c.allbad, tid);
+            rb[buf * c.C + c.crank] = c.m->bad_row;
         }
         SEPSO_MARK(6);
         cluster.sync();   // partials of every CTA visible cluster-wide
         SEPSO_MARK(7);
 
-        // gather partials (one DSMEM round trip, all threads in parallel)
-        for (int t = tid; t < c.C * LGM + c.C; t += nthr) {
-            if (t < c.C * LGM) {
-                const int cc = t / LGM, lg = t - cc * LGM;
-                const Part* rp = cluster.map_shared_rank(c.part, cc);
-                c.allpart[t] = rp[buf * LGM + lg];
-            } else {
-                const int cc = t - c.C * LGM;
-                const Misc<T>* rm = cluster.map_shared_rank(c.m, cc);
-                c.allbad[cc] = rm->bad_row;
-            }
-        }
-        __syncthreads();
+        // partials were pushed before the barrier: nothing to gather
         SEPSO_MARK(8);
         if (warp == 0) {
             // gbest, one lane per group: scan the owning CTAs in row order,
             // strict '<' vs the incumbent (runner.hpp:81-87)
             Misc<T>* m = c.m;
             int bad = INT_MAX;
-            for (int cc = lane; cc < c.C; cc += 32) bad = min(bad, c.allbad[cc]);
+            for (int cc = lane; cc < c.C; cc += 32) bad = min(bad, c.allbad[buf * c.C + cc]);
             bad = int(__reduce_min_sync(0xffffffffu, uint32_t(bad)));
             if (bad != INT_MAX) {
                 if (lane == 0) { m->status = 2; m->bad_min = bad; m->stop = 1; }
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
                     int bslot = -1, bq = 0;
                     for (int cc = cf; cc <= cl; ++cc) {
                         const int slot = cc * LGM + (g - c.ctab[cc]);
-                        const Part pt = c.allpart[slot];
+                        const Part pt = c.part[buf * c.C * LGM + slot];
                         if (pt.f < bf) { bf = pt.f; bslot = slot; bq = pt.q; }
                     }
                     if (T(bf) < c.gbf[g]) { c.gbf[g] = T(bf); c.gbq[g] = bq; c.chg[g] = bslot; }
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
                     int newest = wh + wl - 1;
                     if (newest >= p.tw) newest -= p.tw;
                     const double gap = fabs(c.win[newest] - c.win[oldest]);
-                    const bool may_fire = !(gap >= p.delta * sqrt(2.0 * p.tw) * (1.0 + 1e-9));
+                    const bool may_fire = !(gap >= p.at_gap);
                     if (p.auto_truncate && wl >= p.tw && m->tbq == 0 && may_fire) {
                         double mean = 0.0;
                         for (int i = 0, at = wh; i < p.tw; ++i) {
@@ -312,16 +312,14 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
         __syncthreads();
         SEPSO_MARK(9);
         if (c.m->status) break;
-        // copy improved group bests (and the new tbest) from their owners' partials
+        // copy improved group bests (and the new tbest) from the pushed rows
         {
             const int tg = c.m->tsrc_slot;
             for (int t = tid; t < G * D; t += nthr) {
                 const int g = int(c.fD.div(uint32_t(t))), d = t - g * D;
                 const int slot = c.chg[g];
                 if (slot >= 0) {
-                    const int cc = slot / LGM, lg = slot - cc * LGM;
-                    const T* rpx = cluster.map_shared_rank(c.px, cc);
-                    const T val = rpx[(buf * LGM + lg) * D + d];
+                    const T val = c.px[(buf * c.C * LGM + slot) * D + d];
                     c.gbx[g * D + d] = val;
                     if (g == tg) c.tbx[d] = val;
                 }

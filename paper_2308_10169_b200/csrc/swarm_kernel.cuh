@@ -66,6 +66,7 @@ struct SwarmParams {
     int auto_truncate, carry, tw, warm;
     double alpha, beta, delta, pi_radius;
     int beta_int;            // >= 1: beta is this small integer (exact repeated product)
+    double at_gap;           // delta * sqrt(2 tw) * (1 + 1e-9): exact AT pre-test bound
     // inputs
     const double* hypers;  long long hypers_stride;   // doubles between swarms (0 = shared)
     const unsigned long long* seeds;
@@ -133,10 +134,10 @@ SEPSO_LHD SmemLayout smem_layout(const SwarmParams& p, size_t tsz, bool path) {
     L.chg = take(G * 4);
     L.tbx = take(D * tsz);
     L.win = take(size_t(p.tw) * 8);
-    L.part = take(2 * LG * 16);            // double-buffered group partials (Part)
-    L.px = take(2 * LG * D * tsz);
-    L.allpart = take(C * LG * 16);         // gathered partials of the cluster
-    L.allbad = take(C * 4);                // per-CTA first non-finite row
+    L.part = take(2 * C * LG * 16);        // pushed partials of every CTA, double-buffered
+    L.px = take(2 * C * LG * D * tsz);     // and the matching pbest rows
+    L.allpart = take(0);
+    L.allbad = take(2 * C * 4);            // per-CTA first non-finite row, double-buffered
     L.gtab = take(G * 8);                  // per group: first / last owning CTA
     L.ctab = take(C * 4);                  // per CTA: first group
     L.obb = take(O * 4 * tsz);
