@@ -150,18 +150,19 @@ int sf_lfv_batch(sf_ctx* ctx, const sf_problem* problem, uint32_t m, const doubl
 /* evolve (hsef.hpp:125-171): outer PSO on the host, each evolution's
  * outer_groups*outer_per_group inner runs batched in one sf_lfv_batch launch.
  * best_trace/round_trace: E values; best_hypers: inner_groups*6. */
+typedef void (*sf_evolution_cb)(uint32_t evolution, double best_lfv, void* user);
 int sf_evolve(sf_ctx* ctx, const sf_problem* problem, uint32_t inner_groups,
               uint32_t inner_per_group, uint32_t inner_iterations, uint32_t outer_groups,
               uint32_t outer_per_group, uint32_t evolutions, uint64_t seed,
               const double* outer_hypers, double* best_trace, double* round_trace,
-              double* best_hypers);
+              double* best_hypers, sf_evolution_cb on_evolution, void* user);
 
 /* ---- stage entry points (parity) ---------------------------------------- */
 /* init_swarm (swarm.hpp:94-132) / priori_init (planner.hpp:77-133 when prev != NULL) */
 int sf_init_swarm(sf_ctx* ctx, const double* hypers, const double* lo, const double* hi,
                   uint32_t groups, uint32_t per_group, uint32_t dim, uint64_t seed,
-                  const double* prev_particle, uint32_t warm, double pi_radius, double* x,
-                  double* v);
+                  uint64_t first_draw, const double* prev_particle, uint32_t warm,
+                  double pi_radius, double* x, double* v);
 /* step (swarm.hpp:138-174) with the stream positioned at draw `first_draw` */
 int sf_step(sf_ctx* ctx, const double* hypers, const double* lo, const double* hi,
             uint32_t groups, uint32_t per_group, uint32_t dim, double* x, double* v,

@@ -560,7 +560,8 @@ int sf_lfv_batch(sf_ctx* ctx, const sf_problem* pr, uint32_t m, const double* ca
 // hsef.hpp:125-171: outer PSO on the host, inner runs batched on the device
 int sf_evolve(sf_ctx* ctx, const sf_problem* pr, uint32_t iG, uint32_t iN, uint32_t iT,
               uint32_t oG, uint32_t oN, uint32_t E, uint64_t seed, const double* outer_hypers,
-              double* best_trace, double* round_trace, double* best_hypers) {
+              double* best_trace, double* round_trace, double* best_hypers, sf_evolution_cb cb,
+              void* user) {
     if (!ctx || !outer_hypers) return fail(SF_INVALID_ARGUMENT, "null argument");
     if (E < 1) return fail(SF_INVALID_ARGUMENT, "evolve: evolution count must be >= 1");
     if (iT < 1) return fail(SF_INVALID_ARGUMENT, "evolve: inner iteration count must be >= 1");
@@ -592,6 +593,7 @@ int sf_evolve(sf_ctx* ctx, const sf_problem* pr, uint32_t iG, uint32_t iN, uint3
         host_update_bests(s, fit.data());
         if (best_trace) best_trace[e - 1] = s.tbf;
         if (round_trace) round_trace[e - 1] = round_best;
+        if (cb) cb(e, s.tbf, user);                                   // hsef.hpp:163
         host_step(s, outer_hypers, lo.data(), hi.data(), rng, e, E);
     }
     if (best_hypers) unflatten_hypers(s.tbx.data(), iG, best_hypers);
@@ -639,8 +641,8 @@ int sync(sf_ctx* ctx) {
 }  // namespace
 
 int sf_init_swarm(sf_ctx* ctx, const double* hypers, const double* lo, const double* hi,
-                  uint32_t G, uint32_t N, uint32_t D, uint64_t seed, const double* prev,
-                  uint32_t warm, double pi_radius, double* x, double* v) {
+                  uint32_t G, uint32_t N, uint32_t D, uint64_t seed, uint64_t first_draw,
+                  const double* prev, uint32_t warm, double pi_radius, double* x, double* v) {
     if (!ctx || !x || !v) return fail(SF_INVALID_ARGUMENT, "null argument");
     DeviceGuard guard(ctx->device);
     int st = validate_hypers(hypers, G);
@@ -661,7 +663,7 @@ int sf_init_swarm(sf_ctx* ctx, const double* hypers, const double* lo, const dou
     if (prev) up(ctx, a.at(op), prev, size_t(D) * 8);
     const StageShape s{int(G), int(N), int(D), 0, int(G * N)};
     const int e = stage_init(ctx->precision == SF_FP64, s, reinterpret_cast<double*>(a.at(oh)), a.at(olo),
-                             a.at(ohi), seed, prev ? reinterpret_cast<double*>(a.at(op)) : nullptr,
+                             a.at(ohi), seed, first_draw, prev ? reinterpret_cast<double*>(a.at(op)) : nullptr,
                              prev ? int(warm) : 0, pi_radius, a.at(ox), a.at(ov), a.at(opb), ctx->stream);
     if (e) return cuda_fail(cudaError_t(e), "stage_init");
     std::vector<unsigned char> hx(E * ts), hv(E * ts);

@@ -359,7 +359,7 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
     if (ctx->timing) cudaEventRecord(ctx->ev0, st);
     const StageShape s{G, N, D, 0, R};
     IterState* dst = reinterpret_cast<IterState*>(dev + o_st);
-    int e = stage_init(fp64, s, reinterpret_cast<double*>(dev + o_hyp), dev + o_lo, dev + o_hi, r.seed,
+    int e = stage_init(fp64, s, reinterpret_cast<double*>(dev + o_hyp), dev + o_lo, dev + o_hi, r.seed, 0,
                        r.prev ? reinterpret_cast<double*>(dev + o_prev) : nullptr, r.warm, r.pi_radius,
                        dev + o_x, dev + o_v, dev + o_pb, st);
     if (e) return cuda_fail(cudaError_t(e), "stage_init");

@@ -28,8 +28,9 @@ static inline unsigned grid_for(long long work, int block) {
 // swarm.hpp:94-132 / planner.hpp:77-133 (draws indexed by global row)
 template <class T>
 __global__ void k_init(StageShape s, const double* __restrict__ hypers, const T* __restrict__ lo,
-                       const T* __restrict__ hi, uint64_t seed, const double* __restrict__ prev,
-                       int warm, double pi_radius, T* x, T* v, T* pb) {
+                       const T* __restrict__ hi, uint64_t seed, uint64_t first,
+                       const double* __restrict__ prev, int warm, double pi_radius, T* x, T* v,
+                       T* pb) {
     using A = Ar<T>;
     const long long total = (long long)s.rows * s.D;
     const int R = s.G * s.N;
@@ -38,7 +39,7 @@ __global__ void k_init(StageShape s, const double* __restrict__ hypers, const T*
          e += (long long)gridDim.x * blockDim.x) {
         const int rl = int(e / s.D), d = int(e - (long long)rl * s.D);
         const int row = s.row_begin + rl, g = row / s.N, n = row - g * s.N;
-        const uint64_t ix = uint64_t(row) * uint64_t(s.D) + uint64_t(d);
+        const uint64_t ix = first + uint64_t(row) * uint64_t(s.D) + uint64_t(d);
         const T ux = unit_from_word<T>(philox_word(seed, ix));
         const T l0 = lo[d], h0 = hi[d];
         T xv;
@@ -60,17 +61,18 @@ __global__ void k_init(StageShape s, const double* __restrict__ hypers, const T*
 }
 
 int stage_init(bool fp64, const StageShape& s, const double* hypers, const void* lo,
-               const void* hi, uint64_t seed, const double* prev, int warm, double pi_radius,
-               void* x, void* v, void* pb, void* stream) {
+               const void* hi, uint64_t seed, uint64_t first, const double* prev, int warm,
+               double pi_radius, void* x, void* v, void* pb, void* stream) {
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     const unsigned grid = grid_for((long long)s.rows * s.D, 256);
     if (fp64)
         k_init<double><<<grid, 256, 0, st>>>(s, hypers, (const double*)lo, (const double*)hi, seed,
-                                              prev, warm, pi_radius, (double*)x, (double*)v,
+                                              first, prev, warm, pi_radius, (double*)x, (double*)v,
                                               (double*)pb);
     else
         k_init<float><<<grid, 256, 0, st>>>(s, hypers, (const float*)lo, (const float*)hi, seed,
-                                             prev, warm, pi_radius, (float*)x, (float*)v, (float*)pb);
+                                             first, prev, warm, pi_radius, (float*)x, (float*)v,
+                                             (float*)pb);
     return int(cudaGetLastError());
 }
 

@@ -34,8 +34,8 @@ struct IterState {
 };
 
 int stage_init(bool fp64, const StageShape& s, const double* hypers, const void* lo,
-               const void* hi, uint64_t seed, const double* prev, int warm, double pi_radius,
-               void* x, void* v, void* pbest_x, void* stream);
+               const void* hi, uint64_t seed, uint64_t first_draw, const double* prev, int warm,
+               double pi_radius, void* x, void* v, void* pbest_x, void* stream);
 
 int stage_step(bool fp64, const StageShape& s, const double* hypers, const void* lo,
                const void* hi, void* x, void* v, const void* pbest_x, const void* gbest_x,

@@ -142,9 +142,10 @@ def lib():
                                    C.c_uint32, C.c_uint32, C.c_uint32, _dp]),
         "sf_evolve": (C.c_int, [C.c_void_p, C.POINTER(_Problem), C.c_uint32, C.c_uint32,
                                 C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, _dp,
-                                _dp, _dp, _dp]),
+                                _dp, _dp, _dp, C.c_void_p, C.c_void_p]),
         "sf_init_swarm": (C.c_int, [C.c_void_p, _dp, _dp, _dp, C.c_uint32, C.c_uint32,
-                                    C.c_uint32, C.c_uint64, _dp, C.c_uint32, C.c_double, _dp, _dp]),
+                                    C.c_uint32, C.c_uint64, C.c_uint64, _dp, C.c_uint32, C.c_double,
+                                    _dp, _dp]),
         "sf_step": (C.c_int, [C.c_void_p, _dp, _dp, _dp, C.c_uint32, C.c_uint32, C.c_uint32, _dp,
                               _dp, _dp, _dp, _dp, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32]),
         "sf_update_bests": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, _dp, _dp,
@@ -545,12 +546,14 @@ class Engine:
         bt, rt = np.zeros(E), np.zeros(E)
         best = np.zeros(6 * inner[0])
         _check(self._L.sf_evolve(self._h, C.byref(pr), inner[0], inner[1], inner[2], outer[0],
-                                 outer[1], E, C.c_uint64(seed), _p(oh), _p(bt), _p(rt), _p(best)))
+                                 outer[1], E, C.c_uint64(seed), _p(oh), _p(bt), _p(rt), _p(best),
+                                 None, None))
         return dict(best_lfv_trace=bt, evolution_lfv_trace=rt, best=best.reshape(-1, 6),
                     evolutions=E, lfv_evaluations=outer[0] * outer[1] * E)
 
     # -- stages
-    def init_swarm(self, hypers, lo, hi, G, N, D, seed, prev=None, warm=0, pi_radius=20.0):
+    def init_swarm(self, hypers, lo, hi, G, N, D, seed, prev=None, warm=0, pi_radius=20.0,
+                   first_draw=0):
         x = np.zeros(G * N * D)
         v = np.zeros(G * N * D)
         hyp = np.ascontiguousarray(hypers, dtype=np.float64)
@@ -558,7 +561,7 @@ class Engine:
         hi = np.ascontiguousarray(hi, dtype=np.float64)
         pv = None if prev is None else np.ascontiguousarray(prev, dtype=np.float64)
         _check(self._L.sf_init_swarm(self._h, _p(hyp), _p(lo), _p(hi), G, N, D, C.c_uint64(seed),
-                                     _p(pv), warm, pi_radius, _p(x), _p(v)))
+                                     C.c_uint64(first_draw), _p(pv), warm, pi_radius, _p(x), _p(v)))
         return x, v
 
     def step(self, hypers, lo, hi, G, N, D, x, v, pbest_x, gbest_x, tbest_x, seed, first_draw,

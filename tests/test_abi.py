@@ -135,3 +135,10 @@ def test_invalid_scenario_config_rejected():
         pe.generate_world(pe.ScenarioConfig(max_side=400.0), 1)
     with pytest.raises(ValueError):
         pe.generate_world(pe.ScenarioConfig(max_speed=0.0), 1)
+
+
+def test_dropin_headers_compile_as_cpp20():
+    """A reference user's program compiles against include/swarmforge/*.hpp."""
+    for ex in ("plan_route.cpp", "minimize_rastrigin.cpp"):
+        subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "examples", ex)], check=True)
