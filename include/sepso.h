@@ -227,6 +227,23 @@ int sf_scene_batch_destroy(sf_scene_batch* b);
 /* FP32 FFMA throughput of the device (TFLOP/s): roofline denominator probe. */
 int sf_measure_fp32_peak(sf_ctx* ctx, double* tflops);
 
+/* ---- multi-GPU: one large swarm sharded by group (BASELINE config 4) ------ */
+/* NCCL communicator owned by the context (one process per GPU).  Rank 0 makes
+ * the id, the caller broadcasts it, every rank attaches.  */
+int sf_comm_unique_id(uint8_t id[128]);
+int sf_ctx_init_comm(sf_ctx* ctx, const uint8_t id[128], int nranks, int rank);
+/* plan_frame (planner.hpp:156-199) for one large swarm whose groups are split
+ * across the communicator's ranks: rank r evaluates and updates groups
+ * [r*G/n, (r+1)*G/n) in HBM with the stage kernels; per iteration the ranks
+ * all-gather one population-best candidate each (~16 + 4*dim bytes) and reduce
+ * it identically (group order, strict '<'), so the AT decision, the trace and
+ * the record are identical on every rank and equal the unsharded run.  With no
+ * communicator it runs the same HBM path on one GPU. */
+int sf_plan_frame_sharded(sf_ctx* ctx, const sf_world* world, const double* prev_particle,
+                          const double* hypers, const sf_planner_config* cfg, uint64_t seed,
+                          double* window, uint32_t* window_len, uint32_t window_cap,
+                          sf_plan_record* record, double* best_particle, uint64_t* bad);
+
 /* Benchmark hygiene: when bytes > 0, sf_run_scenario writes a device buffer of
  * that size (flushing L2) before each frame, outside the frame's wall time. */
 int sf_ctx_set_l2_flush(sf_ctx* ctx, uint64_t bytes);

@@ -293,6 +293,7 @@ int sf_ctx_destroy(sf_ctx* ctx) {
     ctx->io.release();
     ctx->scratch.release();
     ctx->flush.release();
+    comm_destroy(ctx->comm);
     ctx->hio.release();
     cudaEventDestroy(ctx->ev0);
     cudaEventDestroy(ctx->ev1);
@@ -1014,6 +1015,72 @@ int sf_run_scenario(sf_ctx* ctx, const sf_scenario_config* c, int variant, uint3
         if (best) std::copy(bp.begin(), bp.end(), best + size_t(f) * cfg.dim);
         if ((st = sf_step_world(&w, verts.data(), vel.data(), c->dt))) return st;
     }
+    return SF_OK;
+}
+
+int sf_comm_unique_id(uint8_t id[128]) {
+    if (!id) return fail(SF_INVALID_ARGUMENT, "id is null");
+    return comm_unique_id(id);
+}
+
+int sf_ctx_init_comm(sf_ctx* ctx, const uint8_t id[128], int nranks, int rank) {
+    if (!ctx || !id) return fail(SF_INVALID_ARGUMENT, "null argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(SF_INVALID_ARGUMENT, "bad rank / world size");
+    DeviceGuard guard(ctx->device);
+    if (ctx->comm) comm_destroy(ctx->comm);
+    ctx->comm = nullptr;
+    const int st = comm_init(&ctx->comm, id, nranks, rank);
+    if (st) return st;
+    ctx->rank = rank;
+    ctx->nranks = nranks;
+    return SF_OK;
+}
+
+int sf_plan_frame_sharded(sf_ctx* ctx, const sf_world* world, const double* prev, const double* hypers,
+                          const sf_planner_config* cfg, uint64_t seed, double* window, uint32_t* window_len,
+                          uint32_t window_cap, sf_plan_record* record, double* best, uint64_t* bad) {
+    const double t0 = now_seconds();
+    if (!ctx || !record) return fail(SF_INVALID_ARGUMENT, "ctx/record is null");
+    DeviceGuard guard(ctx->device);
+    int st = validate_planner(cfg);
+    if (st) return st;
+    if ((st = validate_world(world))) return st;
+    if (!hypers) return fail(SF_INVALID_ARGUMENT, "hypers is null");
+    if ((st = validate_hypers(hypers, cfg->groups))) return st;
+    if (int(cfg->groups) < ctx->nranks) return fail(SF_INVALID_ARGUMENT, "sharded swarm: fewer groups than ranks");
+    const bool carry = cfg->window_carryover && window && window_len;
+    StagedRun sr;
+    sr.problem = kPath;
+    sr.G = int(cfg->groups); sr.N = int(cfg->per_group); sr.D = int(cfg->dim); sr.cap = int(cfg->max_iters_per_frame);
+    sr.world = world;
+    sr.alpha = cfg->alpha; sr.beta = cfg->beta;
+    sr.hypers = hypers;
+    sr.seed = seed;
+    sr.prev = prev;
+    sr.warm = prev ? int(cfg->gamma * double(cfg->per_group)) : 0;
+    sr.pi_radius = cfg->pi_radius;
+    sr.auto_truncate = cfg->auto_truncate;
+    sr.tw = int(cfg->tw);
+    sr.delta = cfg->delta;
+    std::vector<double> wtail;
+    if (carry) {
+        const uint32_t keep = std::min(*window_len, cfg->tw);
+        wtail.assign(window + (*window_len - keep), window + *window_len);
+        sr.win_in = wtail.data();
+        sr.win_len_in = int(keep);
+    }
+    sr.rank = ctx->rank;
+    sr.nranks = ctx->nranks;
+    sr.comm = ctx->comm;
+    if ((st = run_staged(ctx, sr))) return st;
+    if (sr.out.status == 2) {
+        if (bad) { bad[0] = sr.out.bad_g; bad[1] = sr.out.bad_n; bad[2] = sr.out.bad_k; }
+        return fail(SF_NON_FINITE, nonfinite_msg(sr.out.bad_g, sr.out.bad_n, sr.out.bad_k));
+    }
+    if (carry && (st = carry_window(window, window_len, window_cap, cfg->tw, sr.trace.data(), sr.out.iterations)))
+        return st;
+    if (best) std::copy(sr.best.begin(), sr.best.end(), best);
+    fill_record(sr.out, now_seconds() - t0, record);
     return SF_OK;
 }
 

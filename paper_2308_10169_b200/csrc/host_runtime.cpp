@@ -282,6 +282,11 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
     const bool fp64 = ctx->precision == SF_FP64;
     const size_t tsz = fp64 ? 8 : 4;
     const int G = r.G, N = r.N, D = r.D, R = G * N;
+    // this device's shard: whole groups [g0, g1) (rows [g0*N, g1*N))
+    const int nranks = std::max(1, r.nranks);
+    const int g0 = int((long long)r.rank * G / nranks), g1 = int((long long)(r.rank + 1) * G / nranks);
+    const int RL = (g1 - g0) * N, row_begin = g0 * N;
+    if (RL <= 0) return fail(SF_INVALID_ARGUMENT, "sharded swarm: more ranks than groups");
     const bool path = r.problem == kPath;
     cudaStream_t st = ctx->stream;
     // host-side staging of constants
@@ -304,14 +309,15 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
     const size_t o_hyp = take(size_t(G) * 6 * 8);
     const size_t o_lo = take(size_t(D) * tsz), o_hi = take(size_t(D) * tsz);
     const size_t o_prev = take(size_t(D) * 8);
-    const size_t o_x = take(size_t(R) * D * tsz), o_v = take(size_t(R) * D * tsz);
-    const size_t o_pb = take(size_t(R) * D * tsz);
-    const size_t o_fit = take(size_t(R) * tsz), o_pbf = take(size_t(R) * tsz);
-    const size_t o_q = take(size_t(R) * 4), o_pbq = take(size_t(R) * 4);
+    const size_t o_x = take(size_t(RL) * D * tsz), o_v = take(size_t(RL) * D * tsz);
+    const size_t o_pb = take(size_t(RL) * D * tsz);
+    const size_t o_fit = take(size_t(RL) * tsz), o_pbf = take(size_t(RL) * tsz);
+    const size_t o_q = take(size_t(RL) * 4), o_pbq = take(size_t(RL) * 4);
     const size_t o_pf = take(size_t(G) * tsz), o_prow = take(size_t(G) * 4), o_pq = take(size_t(G) * 4);
     const size_t o_gbx = take(size_t(G) * D * tsz), o_gbf = take(size_t(G) * tsz), o_gbq = take(size_t(G) * 4);
     const size_t o_tbx = take(size_t(D) * tsz);
-    const size_t o_cand = take(cand_bytes(fp64, D));
+    const size_t cstride = cand_bytes(fp64, D);
+    const size_t o_cand = take(cstride * size_t(nranks));
     const size_t o_st = take(sizeof(IterState));
     const size_t o_win = take(size_t(std::max(r.tw, 1)) * 8);
     const size_t o_trace = take(size_t(r.cap) * 8);
@@ -335,14 +341,14 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
     ce = cudaMemcpyAsync(dev, h.data(), o_x, cudaMemcpyHostToDevice, st);
     if (ce != cudaSuccess) return cuda_fail(ce, "staged upload");
     // bests start at +inf (swarm.hpp:113-116)
-    std::vector<unsigned char> inf_f(size_t(std::max(R, G)) * tsz);
-    for (int i = 0; i < std::max(R, G); ++i) {
+    std::vector<unsigned char> inf_f(size_t(std::max(RL, G)) * tsz);
+    for (int i = 0; i < std::max(RL, G); ++i) {
         if (fp64) reinterpret_cast<double*>(inf_f.data())[i] = std::numeric_limits<double>::infinity();
         else reinterpret_cast<float*>(inf_f.data())[i] = std::numeric_limits<float>::infinity();
     }
-    cudaMemcpyAsync(dev + o_pbf, inf_f.data(), size_t(R) * tsz, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(dev + o_pbf, inf_f.data(), size_t(RL) * tsz, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(dev + o_gbf, inf_f.data(), size_t(G) * tsz, cudaMemcpyHostToDevice, st);
-    cudaMemsetAsync(dev + o_pbq, 0, size_t(R) * 4, st);
+    cudaMemsetAsync(dev + o_pbq, 0, size_t(RL) * 4, st);
     cudaMemsetAsync(dev + o_gbq, 0, size_t(G) * 4, st);
     cudaMemsetAsync(dev + o_gbx, 0, size_t(G) * D * tsz, st);
     cudaMemsetAsync(dev + o_tbx, 0, size_t(D) * tsz, st);
@@ -357,7 +363,7 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
         cudaMemcpyAsync(dev + o_win, r.win_in, size_t(is.win_len) * 8, cudaMemcpyHostToDevice, st);
 
     if (ctx->timing) cudaEventRecord(ctx->ev0, st);
-    const StageShape s{G, N, D, 0, R};
+    const StageShape s{G, N, D, row_begin, RL};
     IterState* dst = reinterpret_cast<IterState*>(dev + o_st);
     int e = stage_init(fp64, s, reinterpret_cast<double*>(dev + o_hyp), dev + o_lo, dev + o_hi, r.seed, 0,
                        r.prev ? reinterpret_cast<double*>(dev + o_prev) : nullptr, r.warm, r.pi_radius,
@@ -367,10 +373,10 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
     for (int k = 1; k <= r.cap; ++k) {
         if (path)
             e = stage_eval_path(fp64, dev + o_world, wl.max_obs, wl.max_verts, int(wl.off_offsets),
-                                int(wl.off_verts), D, R, dev + o_x, r.alpha, r.beta, dev + o_fit,
+                                int(wl.off_verts), D, RL, dev + o_x, r.alpha, r.beta, dev + o_fit,
                                 reinterpret_cast<int*>(dev + o_q), dst, st);
         else
-            e = stage_eval_bench(fp64, r.problem, D, R, dev + o_x, dev + o_fit,
+            e = stage_eval_bench(fp64, r.problem, D, RL, dev + o_x, dev + o_fit,
                                  reinterpret_cast<int*>(dev + o_q), dst, st);
         if (e) return cuda_fail(cudaError_t(e), "stage_eval");
         e = stage_pbest_partials(fp64, s, dev + o_x, dev + o_fit, reinterpret_cast<int*>(dev + o_q),
@@ -380,9 +386,13 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
         if (e) return cuda_fail(cudaError_t(e), "stage_pbest");
         e = stage_group_bests(fp64, s, dev + o_pf, reinterpret_cast<int*>(dev + o_prow),
                               reinterpret_cast<int*>(dev + o_pq), dev + o_pb, dev + o_gbx, dev + o_gbf,
-                              reinterpret_cast<int*>(dev + o_gbq), dev + o_cand, dst, st);
+                              reinterpret_cast<int*>(dev + o_gbq), dev + o_cand + cstride * r.rank, dst, st, dst);
         if (e) return cuda_fail(cudaError_t(e), "stage_group_bests");
-        e = stage_finish(fp64, D, dev + o_cand, 1, dev + o_tbx, dst,
+        if (nranks > 1) {   // the only cross-GPU traffic: each rank's tbest candidate
+            e = comm_allgather(r.comm, dev + o_cand + cstride * r.rank, dev + o_cand, cstride, st);
+            if (e) return fail(SF_CUDA_ERROR, "ncclAllGather of tbest candidates failed");
+        }
+        e = stage_finish(fp64, D, dev + o_cand, nranks, dev + o_tbx, dst,
                          r.tw > 0 ? reinterpret_cast<double*>(dev + o_win) : nullptr, r.tw,
                          r.auto_truncate, r.delta, k, r.cap, reinterpret_cast<double*>(dev + o_trace), st);
         if (e) return cuda_fail(cudaError_t(e), "stage_finish");

@@ -47,6 +47,8 @@ struct sf_ctx {
     int force_cluster = 0, force_threads = 0;
     uint64_t last_h2d = 0, last_d2h = 0;
     uint64_t l2_flush = 0;
+    void* comm = nullptr;
+    int rank = 0, nranks = 1;
     sepso::DevBuf io, scratch, flush;
     sepso::PinnedBuf hio;
 };
@@ -100,11 +102,20 @@ struct StagedRun {
     double delta = 10.0;
     const double* win_in = nullptr;   // last min(len, tw) values
     int win_len_in = 0;
+    // sharding (BASELINE config 4): this rank's groups, the communicator
+    int rank = 0, nranks = 1;
+    void* comm = nullptr;
     // outputs
     SwarmOut out{};
     std::vector<double> best, trace, win_out;
 };
 int run_staged(sf_ctx* ctx, StagedRun& r);
+
+// NCCL (dlopen'ed; the process's already-loaded libnccl is reused)
+int comm_unique_id(unsigned char id[128]);
+int comm_init(void** comm, const unsigned char id[128], int nranks, int rank);
+int comm_allgather(void* comm, const void* send, void* recv, size_t bytes, cudaStream_t st);
+void comm_destroy(void* comm);
 
 bool force_staged();
 

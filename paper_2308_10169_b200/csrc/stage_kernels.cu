@@ -12,6 +12,8 @@ struct CandHdr {        // one device's population-best candidate (runner.hpp:88
     double f;
     int q;
     int g;
+    int bad;            // first non-finite global row on that device (INT_MAX: none)
+    int pad;
 };
 
 size_t cand_bytes(bool fp64, int D) {
@@ -192,7 +194,7 @@ struct EvalSmem {
 };
 
 SEPSO_LHD EvalSmem eval_smem(int rows_tile, int D, int max_obs, int max_verts, int entry_cap,
-                          size_t tsz) {
+                          size_t tsz, bool edges = true) {
     EvalSmem L{};
     size_t o = 0;
     auto take = [&](size_t b) { const size_t at = o; o = sm_align(o + b); return at; };
@@ -204,7 +206,7 @@ SEPSO_LHD EvalSmem eval_smem(int rows_tile, int D, int max_obs, int max_verts, i
     L.ooff = take(size_t(max_obs + 1) * 4);
     L.ofl = take(size_t(max_obs) * 4);
     L.vert = take(size_t(max_verts) * 2 * tsz);
-    L.edge = take(size_t(max_verts) * 4 * tsz);
+    L.edge = take(edges ? size_t(max_verts) * 4 * tsz : 0);
     L.seglen = take(size_t(rows_tile) * S * tsz);
     L.q = take(size_t(rows_tile) * 4);
     L.list = take(size_t(entry_cap) * 4);
@@ -246,6 +248,66 @@ __global__ void __launch_bounds__(256) k_eval_path(const unsigned char* __restri
     for (int i = threadIdx.x; i < c.P; i += blockDim.x) qout[r0 + i] = c.q[i];
 }
 
+
+// K2 for wide worlds (many obstacles, config 4): one warp per (particle,
+// segment) item, its lanes sweep the obstacles 32 at a time -- box cull and
+// the pair test of every overlapping obstacle run side by side in SIMT, no
+// work list.  The world is staged in shared memory once per CTA.
+template <class T>
+__global__ void __launch_bounds__(256) k_eval_path_wide(const unsigned char* __restrict__ world,
+                                                        SwarmParams pp, int rows, int rows_tile,
+                                                        const T* x, T* fit, int* qout,
+                                                        const IterState* gate) {
+    if (gate != nullptr && gate->stop) return;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const EvalSmem L = eval_smem(rows_tile, pp.D, pp.max_obs, pp.max_verts, 0, sizeof(T), sizeof(T) == 4);
+    const int r0 = blockIdx.x * rows_tile;
+    Ctx<T> c{};
+    c.D = pp.D; c.W = pp.D / 2; c.S = c.W + 1;
+    c.fS.init(uint32_t(c.S));
+    c.P = min(rows_tile, rows - r0);
+    if (c.P <= 0) return;
+    c.x = const_cast<T*>(x) + size_t(r0) * pp.D;
+    c.lo = (T*)(smem + L.lo); c.hi = (T*)(smem + L.hi);
+    c.obb = (T*)(smem + L.obb); c.ooff = (int*)(smem + L.ooff); c.ofl = (int*)(smem + L.ofl);
+    c.vert = (T*)(smem + L.vert);
+    c.edge = sizeof(T) == 4 ? (T*)(smem + L.edge) : nullptr;
+    c.seglen = (T*)(smem + L.seglen); c.q = (int*)(smem + L.q);
+    load_world(c, world, pp.off_offsets, pp.off_verts);
+    for (int i = threadIdx.x; i < c.P; i += blockDim.x) c.q[i] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int S = c.S, items = c.P * S, O = c.O;
+    for (int it = warp; it < items; it += nw) {
+        const int pl = int(c.fS.div(uint32_t(it))), s = it - pl * S;
+        T a1x, a1y, a2x, a2y;
+        chain_pt(c, pl, s, a1x, a1y);
+        chain_pt(c, pl, s + 1, a2x, a2y);
+        if (lane == 0) c.seglen[it] = seg_length<T>(Ar<T>::sub(a2x, a1x), Ar<T>::sub(a2y, a1y));
+        const T lx = a1x < a2x ? a1x : a2x, hx = a1x < a2x ? a2x : a1x;
+        const T ly = a1y < a2y ? a1y : a2y, hy = a1y < a2y ? a2y : a1y;
+        int cnt = 0;
+        for (int o = lane; o < O; o += 32)
+            if (box_overlap(lx, ly, hx, hy, c.obb + 4 * o, c.margin)) cnt += pair_count_pts(c, a1x, a1y, a2x, a2y, o);
+        if (s == 0)   // first waypoint (the segment's end) strictly inside (geometry.hpp:217-218)
+            for (int o = lane; o < O; o += 32) {
+                const T* bb = c.obb + 4 * o;
+                if (a2x >= bb[0] - c.margin && a2x <= bb[2] + c.margin && a2y >= bb[1] - c.margin &&
+                    a2y <= bb[3] + c.margin)
+                    cnt += contain_count(c, pl, o);
+            }
+        cnt = int(__reduce_add_sync(0xffffffffu, uint32_t(cnt)));
+        if (lane == 0 && cnt) atomicAdd(&c.q[pl], cnt);
+    }
+    __syncthreads();
+    for (int pl = threadIdx.x; pl < c.P; pl += blockDim.x) {
+        T len = T(0);
+        for (int s = 0; s < S; ++s) len = Ar<T>::add(len, c.seglen[pl * S + s]);
+        fit[r0 + pl] = Ar<T>::add(len, T(penalty(pp.alpha, pp.beta, pp.beta_int, c.q[pl])));
+        qout[r0 + pl] = c.q[pl];
+    }
+}
+
 int stage_eval_path(bool fp64, const unsigned char* world, int max_obs, int max_verts,
                     int off_offsets, int off_verts, int D, int rows, const void* x, double alpha,
                     double beta, void* fit, int* q, const IterState* gate, void* stream) {
@@ -259,8 +321,29 @@ int stage_eval_path(bool fp64, const unsigned char* world, int max_obs, int max_
     pp.alpha = alpha;
     pp.beta = beta;
     pp.beta_int = (beta == double(int(beta)) && beta >= 1.0 && beta <= 64.0) ? int(beta) : 0;
-    const int rows_tile = 64;
     const int S = D / 2 + 1;
+    if (max_obs >= 48) {   // wide worlds: lanes over obstacles
+        const int rows_tile = 16;
+        pp.entry_cap = 0;
+        // FP64 reads the vertices only (no edge records)
+        const EvalSmem L = eval_smem(rows_tile, D, max_obs, max_verts, 0, fp64 ? 8 : 4, !fp64);
+        const unsigned grid = unsigned((rows + rows_tile - 1) / rows_tile);
+        if (grid == 0) return 0;
+        cudaError_t e;
+        if (fp64) {
+            e = cudaFuncSetAttribute(k_eval_path_wide<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.total));
+            if (e != cudaSuccess) return int(e);
+            k_eval_path_wide<double><<<grid, 256, L.total, st>>>(world, pp, rows, rows_tile, (const double*)x,
+                                                                 (double*)fit, q, gate);
+        } else {
+            e = cudaFuncSetAttribute(k_eval_path_wide<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.total));
+            if (e != cudaSuccess) return int(e);
+            k_eval_path_wide<float><<<grid, 256, L.total, st>>>(world, pp, rows, rows_tile, (const float*)x,
+                                                                (float*)fit, q, gate);
+        }
+        return int(cudaGetLastError());
+    }
+    const int rows_tile = 64;
     pp.entry_cap = std::max(1024, std::min(rows_tile * (S + 1) * std::max(max_obs, 1), 8192));
     const size_t tsz = fp64 ? 8 : 4;
     const EvalSmem L = eval_smem(rows_tile, D, max_obs, max_verts, pp.entry_cap, tsz);
@@ -382,7 +465,7 @@ template <class T>
 __global__ void k_group_bests(StageShape s, const T* __restrict__ part_f,
                               const int* __restrict__ part_row, const int* __restrict__ part_q,
                               const T* __restrict__ pb, T* gbx, T* gbf, int* gbq,
-                              unsigned char* cand, const IterState* gate) {
+                              unsigned char* cand, const IterState* gate, const IterState* st) {
     if (gate != nullptr && gate->stop) return;
     extern __shared__ int chg[];
     const int g0 = s.row_begin / s.N;
@@ -404,7 +487,7 @@ __global__ void k_group_bests(StageShape s, const T* __restrict__ part_f,
     }
     __shared__ int best_g;
     if (threadIdx.x == 0) {
-        CandHdr h{__longlong_as_double(0x7ff0000000000000ll), 0, -1};
+        CandHdr h{__longlong_as_double(0x7ff0000000000000ll), 0, -1, st ? st->nonfinite_row : INT_MAX, 0};
         for (int lg = 0; lg < ng; ++lg) {
             const double f = double(gbf[g0 + lg]);
             if (f < h.f) { h.f = f; h.q = gbq[g0 + lg]; h.g = g0 + lg; }
@@ -420,18 +503,18 @@ __global__ void k_group_bests(StageShape s, const T* __restrict__ part_f,
 
 int stage_group_bests(bool fp64, const StageShape& s, const void* part_f, const int* part_row,
                       const int* part_q, const void* pb, void* gbx, void* gbf, int* gbq,
-                      void* cand, const IterState* gate, void* stream) {
+                      void* cand, const IterState* gate, void* stream, const IterState* stt) {
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int ng = (s.row_begin + s.rows - 1) / s.N - s.row_begin / s.N + 1;
     const size_t sm = size_t(ng) * 4;
     if (fp64)
         k_group_bests<double><<<1, 256, sm, st>>>(s, (const double*)part_f, part_row, part_q,
                                                   (const double*)pb, (double*)gbx, (double*)gbf,
-                                                  gbq, (unsigned char*)cand, gate);
+                                                  gbq, (unsigned char*)cand, gate, stt);
     else
         k_group_bests<float><<<1, 256, sm, st>>>(s, (const float*)part_f, part_row, part_q,
                                                  (const float*)pb, (float*)gbx, (float*)gbf, gbq,
-                                                 (unsigned char*)cand, gate);
+                                                 (unsigned char*)cand, gate, stt);
     return int(cudaGetLastError());
 }
 
@@ -444,7 +527,11 @@ __global__ void k_finish(int D, const unsigned char* __restrict__ cands, int n_c
     __shared__ int src;
     if (threadIdx.x == 0) {
         src = -1;
-        if (st->nonfinite_row != INT_MAX) {
+        int bad = INT_MAX;
+        for (int i = 0; i < n_cand; ++i)
+            bad = min(bad, reinterpret_cast<const CandHdr*>(cands + i * cstride)->bad);
+        if (bad != INT_MAX) {
+            st->nonfinite_row = bad;
             st->status = 2;
             st->stop = 1;
         } else {

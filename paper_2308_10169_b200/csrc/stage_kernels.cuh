@@ -61,7 +61,7 @@ int stage_pbest_partials(bool fp64, const StageShape& s, const void* x, const vo
 int stage_group_bests(bool fp64, const StageShape& s, const void* part_f, const int* part_row,
                       const int* part_q, const void* pbest_x, void* gbest_x, void* gbest_f,
                       int* gbest_q, void* cand /*packed candidate*/, const IterState* gate,
-                      void* stream);
+                      void* stream, const IterState* st = nullptr);
 
 // Scan n_cand candidates (ascending group order) for tbest, push the window,
 // evaluate AT; trace[k-1] = tbest_f.  cand layout: see big_swarm.cu.

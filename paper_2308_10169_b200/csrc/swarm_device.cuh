@@ -208,11 +208,8 @@ template <class T>
 __device__ int pair_count(const Ctx<T>& c, int pl, int s, int o);
 
 // FP64 engine: the reference predicate on every edge, bit for bit.
-template <>
-inline __device__ int pair_count<double>(const Ctx<double>& c, int pl, int s, int o) {
-    double a1x, a1y, a2x, a2y;
-    chain_pt(c, pl, s, a1x, a1y);
-    chain_pt(c, pl, s + 1, a2x, a2y);
+inline __device__ int pair_count_pts(const Ctx<double>& c, double a1x, double a1y, double a2x,
+                                     double a2y, int o) {
     const int v0 = c.ooff[o], v1 = c.ooff[o + 1];
     int cnt = 0;
     for (int i = v0; i < v1; ++i) {
@@ -223,6 +220,14 @@ inline __device__ int pair_count<double>(const Ctx<double>& c, int pl, int s, in
     return cnt;
 }
 
+template <>
+inline __device__ int pair_count<double>(const Ctx<double>& c, int pl, int s, int o) {
+    double a1x, a1y, a2x, a2y;
+    chain_pt(c, pl, s, a1x, a1y);
+    chain_pt(c, pl, s + 1, a2x, a2y);
+    return pair_count_pts(c, a1x, a1y, a2x, a2y, o);
+}
+
 // FP32 engine: filtered orientation signs.
 // Vertex crosses cv_i = d x (v_i - a1) are shared by the two edges meeting at
 // v_i (o1 of edge i is o2 of edge i-1).  With every |cv| above the bound B and
@@ -231,11 +236,8 @@ inline __device__ int pair_count<double>(const Ctx<double>& c, int pl, int s, in
 // segment on an edge and therefore opposite vertex signs -- provided the
 // obstacle has no edge shorter than 1e-3 (ofl[o]); otherwise every edge takes
 // the per-pair test.  Uncertain signs fall back to the FP64 reference.
-template <>
-inline __device__ int pair_count<float>(const Ctx<float>& c, int pl, int s, int o) {
-    float a1x, a1y, a2x, a2y;
-    chain_pt(c, pl, s, a1x, a1y);
-    chain_pt(c, pl, s + 1, a2x, a2y);
+inline __device__ int pair_count_pts(const Ctx<float>& c, float a1x, float a1y, float a2x, float a2y,
+                                     int o) {
     const float dx = a2x - a1x, dy = a2y - a1y;
     const float* bb = c.obb + 4 * o;
     const float ux = fmaxf(fmaxf(a1x, a2x), bb[2]) - fminf(fminf(a1x, a2x), bb[0]);
@@ -268,6 +270,14 @@ inline __device__ int pair_count<float>(const Ctx<float>& c, int pl, int s, int 
         cnt += r;
     }
     return cnt;
+}
+
+template <>
+inline __device__ int pair_count<float>(const Ctx<float>& c, int pl, int s, int o) {
+    float a1x, a1y, a2x, a2y;
+    chain_pt(c, pl, s, a1x, a1y);
+    chain_pt(c, pl, s + 1, a2x, a2y);
+    return pair_count_pts(c, a1x, a1y, a2x, a2y, o);
 }
 
 // First waypoint strictly inside obstacle o (geometry.hpp:217-218).
@@ -365,12 +375,15 @@ __device__ void load_world(Ctx<T>& c, const unsigned char* wrec, int off_offsets
             bx1 = bx1 < vx ? vx : bx1;
             by1 = by1 < vy ? vy : by1;
             const int j = (i + 1 == v1) ? v0 : i + 1;
-            T* e = c.edge + 4 * i;
-            e[0] = vx;
-            e[1] = vy;
-            e[2] = A::sub(c.vert[2 * j], vx);
-            e[3] = A::sub(c.vert[2 * j + 1], vy);
-            const T ax = e[2] < T(0) ? -e[2] : e[2], ay = e[3] < T(0) ? -e[3] : e[3];
+            const T ex = A::sub(c.vert[2 * j], vx), ey = A::sub(c.vert[2 * j + 1], vy);
+            if (c.edge != nullptr) {
+                T* e = c.edge + 4 * i;
+                e[0] = vx;
+                e[1] = vy;
+                e[2] = ex;
+                e[3] = ey;
+            }
+            const T ax = ex < T(0) ? -ex : ex, ay = ey < T(0) ? -ey : ey;
             long_edges &= (ax > ay ? ax : ay) >= T(1e-3);
         }
         T* bb = c.obb + 4 * o;

@@ -38,6 +38,7 @@ ABI_SYMBOLS = [
     "sf_generate_world", "sf_step_world", "sf_run_scenario", "sf_scene_batch_create",
     "sf_scene_batch_run", "sf_scene_batch_records", "sf_scene_batch_destroy",
     "sf_ctx_last_io_bytes", "sf_measure_fp32_peak", "sf_ctx_set_l2_flush",
+    "sf_comm_unique_id", "sf_ctx_init_comm", "sf_plan_frame_sharded",
 ]
 
 
@@ -167,6 +168,10 @@ def lib():
         "sf_ctx_last_io_bytes": (C.c_int, [C.c_void_p, _u64p, _u64p]),
         "sf_measure_fp32_peak": (C.c_int, [C.c_void_p, _dp]),
         "sf_ctx_set_l2_flush": (C.c_int, [C.c_void_p, C.c_uint64]),
+        "sf_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+        "sf_ctx_init_comm": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8), C.c_int, C.c_int]),
+        "sf_plan_frame_sharded": (C.c_int, [C.c_void_p, W, _dp, _dp, P, C.c_uint64, _dp, _u32p,
+                                            C.c_uint32, Pr, _dp, _u64p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -412,6 +417,41 @@ class Engine:
 
     def enable_timing(self, on=True):
         _check(self._L.sf_ctx_enable_timing(self._h, int(on)))
+
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _check(lib().sf_comm_unique_id(buf))
+        return bytes(buf)
+
+    def init_comm(self, uid: bytes, nranks: int, rank: int):
+        buf = (C.c_uint8 * 128)(*uid)
+        _check(self._L.sf_ctx_init_comm(self._h, buf, nranks, rank))
+
+    def plan_frame_sharded(self, world: PolygonWorld, prev_best, hypers, config: PlannerConfig,
+                           seed: int, carried_window: Optional[list] = None):
+        """plan_frame for one large swarm split by group over the communicator."""
+        hyp = _hyper_rows(hypers, config.groups, "priori_init")
+        prev = None if prev_best is None else np.ascontiguousarray(
+            encode_path(prev_best) if np.ndim(prev_best) == 2 else prev_best, dtype=np.float64)
+        best = np.zeros(config.dim)
+        rec = _PlanRecord()
+        bad = (C.c_uint64 * 3)()
+        win = wl = None
+        cap = 0
+        if carried_window is not None:
+            cap = max(len(carried_window), config.tw) + 1
+            win = np.zeros(cap)
+            win[:len(carried_window)] = carried_window
+            wl = C.c_uint32(len(carried_window))
+        st = self._L.sf_plan_frame_sharded(self._h, C.byref(world._c()), _p(prev), _p(hyp),
+                                           C.byref(config._c()), C.c_uint64(seed), _p(win),
+                                           C.byref(wl) if wl is not None else None, cap,
+                                           C.byref(rec), _p(best), bad)
+        _check(st, bad)
+        if carried_window is not None and config.window_carryover:
+            carried_window[:] = list(win[:wl.value])
+        return PlanRecord._from(rec, best)
 
     def set_l2_flush(self, nbytes: int):
         _check(self._L.sf_ctx_set_l2_flush(self._h, nbytes))
