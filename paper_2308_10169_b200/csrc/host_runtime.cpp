@@ -219,7 +219,7 @@ FusedPlan plan_fused(sf_ctx* ctx, int problem, int n_swarms, int G, int N, int D
         p.max_local_groups = lgm;
         if (path) {
             // worst case Rc*S*O entries; beyond the capacity entries are evaluated in place
-            p.entry_cap = std::min(std::max(1024, Rc * S * std::max(max_obs, 1)), 8192);
+            p.entry_cap = 0;   // overlapping obstacles are evaluated in place (no work list)
             p.nthreads = std::min(512, std::max(128, ((Rc * S) + 31) / 32 * 32));
         } else {
             p.entry_cap = 0;

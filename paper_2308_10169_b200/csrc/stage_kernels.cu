@@ -344,7 +344,7 @@ int stage_eval_path(bool fp64, const unsigned char* world, int max_obs, int max_
         return int(cudaGetLastError());
     }
     const int rows_tile = 64;
-    pp.entry_cap = std::max(1024, std::min(rows_tile * (S + 1) * std::max(max_obs, 1), 8192));
+    pp.entry_cap = 0;
     const size_t tsz = fp64 ? 8 : 4;
     const EvalSmem L = eval_smem(rows_tile, D, max_obs, max_verts, pp.entry_cap, tsz);
     const unsigned grid = unsigned((rows + rows_tile - 1) / rows_tile);

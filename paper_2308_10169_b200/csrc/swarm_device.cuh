@@ -394,65 +394,40 @@ __device__ void load_world(Ctx<T>& c, const unsigned char* wrec, int off_offsets
 
 // Path fitness of the CTA's particles into c.fit (before pbest logic).
 //   A1  one thread per (particle, segment): segment length, obstacle-box cull
-//       into a bit mask, warp-aggregated append of (particle, segment, obstacle)
-//       work entries (one shared atomic per warp and 32-obstacle chunk);
-//       first-waypoint containment per particle (FP64, rare).
-//   A2  the compacted entries, densely: pair_count per entry.
+//       into a 32-bit mask per obstacle chunk, then every overlapping obstacle
+//       evaluated in place (vertex-cross early exit, filtered pair test, FP64
+//       fallback); first-waypoint containment tasks continue the item space.
 //   A3  fitness = sum of lengths in chain order + alpha * Q^beta.
-// Entries beyond the list capacity are evaluated in place (correct, divergent).
 template <class T>
 __device__ void path_fitness_phase(const SwarmParams& p, Ctx<T>& c, long long* prof = nullptr,
                                    int k = 0) {
-    const int tid = threadIdx.x, lane = tid & 31, nthr = blockDim.x;
+    const int tid = threadIdx.x, nthr = blockDim.x;
     const int S = c.S, items = c.P * S, O = c.O;
-    const int cap = p.entry_cap;
     // ---- A1
     {
         const int step_pl = int(c.fS.div(uint32_t(nthr))), step_s = nthr - step_pl * S;
         int pl = int(c.fS.div(uint32_t(tid))), s = tid - pl * S;
-        for (int base = 0; base < items; base += nthr) {
-            const bool act = base + tid < items;
-            T a1x = 0, a1y = 0, a2x = 0, a2y = 0;
-            if (act) {
-                chain_pt(c, pl, s, a1x, a1y);
-                chain_pt(c, pl, s + 1, a2x, a2y);
-                c.seglen[pl * S + s] = seg_length<T>(Ar<T>::sub(a2x, a1x), Ar<T>::sub(a2y, a1y));
-            }
+        for (int it = tid; it < items; it += nthr) {
+            T a1x, a1y, a2x, a2y;
+            chain_pt(c, pl, s, a1x, a1y);
+            chain_pt(c, pl, s + 1, a2x, a2y);
+            c.seglen[pl * S + s] = seg_length<T>(Ar<T>::sub(a2x, a1x), Ar<T>::sub(a2y, a1y));
             const T lx = a1x < a2x ? a1x : a2x, hx = a1x < a2x ? a2x : a1x;
             const T ly = a1y < a2y ? a1y : a2y, hy = a1y < a2y ? a2y : a1y;
+            int cnt = 0;
             for (int o0 = 0; o0 < O; o0 += 32) {
                 uint32_t mask = 0;
-                if (act) {
-                    const int oe = min(32, O - o0);
+                const int oe = min(32, O - o0);
 #pragma unroll 8
-                    for (int j = 0; j < oe; ++j)
-                        if (box_overlap(lx, ly, hx, hy, c.obb + 4 * (o0 + j), c.margin)) mask |= 1u << j;
-                }
-                const int n = __popc(mask);
-                int incl = n;
-#pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const int t = __shfl_up_sync(0xffffffffu, incl, off);
-                    if (lane >= off) incl += t;
-                }
-                const int total = __shfl_sync(0xffffffffu, incl, 31);
-                if (total == 0) continue;
-                int wbase = 0;
-                if (lane == 31) wbase = atomicAdd(&c.m->n_pair, total);
-                wbase = __shfl_sync(0xffffffffu, wbase, 31);
-                int idx = wbase + incl - n;
+                for (int j = 0; j < oe; ++j)
+                    if (box_overlap(lx, ly, hx, hy, c.obb + 4 * (o0 + j), c.margin)) mask |= 1u << j;
                 while (mask) {
                     const int j = __ffs(mask) - 1;
                     mask &= mask - 1;
-                    if (idx < cap) {
-                        c.list[idx] = pack_entry(pl, s, o0 + j);
-                    } else {
-                        const int k = pair_count(c, pl, s, o0 + j);
-                        if (k) atomicAdd(&c.q[pl], k);
-                    }
-                    ++idx;
+                    cnt += pair_count_pts(c, a1x, a1y, a2x, a2y, o0 + j);
                 }
             }
+            if (cnt) atomicAdd(&c.q[pl], cnt);
             pl += step_pl;
             s += step_s;
             if (s >= S) { s -= S; ++pl; }
@@ -474,21 +449,11 @@ __device__ void path_fitness_phase(const SwarmParams& p, Ctx<T>& c, long long* p
         }
     }
     __syncthreads();
-    if (prof) prof[(k - 1) * kProfPhases + 1] = clock64();
-    // ---- A2
-    const int np = min(c.m->n_pair, cap);
-    for (int e = tid; e < np; e += nthr) {
-        const uint32_t w = c.list[e];
-        const int pl = int(w >> 19), s = int((w >> 11) & 0xffu), o = int(w & 0x7ffu);
-        const int hits = pair_count(c, pl, s, o);
-        if (hits) atomicAdd(&c.q[pl], hits);
-    }
-    __syncthreads();
     if (prof) {
+        prof[(k - 1) * kProfPhases + 1] = clock64();
         prof[(k - 1) * kProfPhases + 2] = clock64();
-        prof[(k - 1) * kProfPhases + 3] = np;
+        prof[(k - 1) * kProfPhases + 3] = 0;
     }
-    if (tid == 0) c.m->n_pair = 0;
     // ---- A3
     for (int pl = tid; pl < c.P; pl += nthr) {
         T len = T(0);

@@ -193,12 +193,23 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
                 Part* rp = cluster.map_shared_rank(c.part, r);
                 rp[buf * c.C * LGM + slot] = pt;
             }
-            if (br != INT_MAX)
-                for (int t = lane; t < c.C * D; t += 32) {
-                    const int r = int(c.fD.div(uint32_t(t))), d = t - r * D;
-                    T* rx = cluster.map_shared_rank(c.px, r);
-                    rx[(buf * c.C * LGM + slot) * D + d] = c.pb[br * D + d];
+            if (br != INT_MAX) {
+                if (sizeof(T) == 4 && (D & 3) == 0) {          // 16-byte remote stores
+                    const int D4 = D >> 2;
+                    for (int t = lane; t < c.C * D4; t += 32) {
+                        const int r = t / D4, d4 = t - r * D4;
+                        float4* rx = reinterpret_cast<float4*>(cluster.map_shared_rank(c.px, r));
+                        rx[(buf * c.C * LGM + slot) * D4 + d4] =
+                            reinterpret_cast<const float4*>(c.pb + br * D)[d4];
+                    }
+                } else {
+                    for (int t = lane; t < c.C * D; t += 32) {
+                        const int r = int(c.fD.div(uint32_t(t))), d = t - r * D;
+                        T* rx = cluster.map_shared_rank(c.px, r);
+                        rx[(buf * c.C * LGM + slot) * D + d] = c.pb[br * D + d];
+                    }
                 }
+            }
         }
         if (tid < c.C) {
             int* rb = cluster.map_shared_rank(c.allbad, tid);
@@ -242,50 +253,75 @@ __global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ S
                     const int og = __shfl_xor_sync(0xffffffffu, tg, off);
                     if (ov < tv || (ov == tv && og < tg)) { tv = ov; tg = og; }
                 }
+                // tbest update, trace, window push + trim to tw (planner.hpp:179-180)
+                const bool tnew = tv < m->tbf;
+                const double tb = double(tnew ? tv : m->tbf);
+                const int tbq = tnew ? c.gbq[tg] : m->tbq;
+                const int wl0 = m->win_len, wh0 = m->win_head;
+                int wl = wl0, wh = wh0;
+                if (p.tw > 0) {
+                    if (wl < p.tw) ++wl;
+                    else if (++wh == p.tw) wh = 0;
+                }
+                __syncwarp();      // every lane has read m before lane 0 updates it
                 if (lane == 0) {
-                    if (tv < m->tbf) { m->tbf = tv; m->tbq = c.gbq[tg]; m->tsrc_slot = tg; }
+                    if (tnew) { m->tbf = tv; m->tbq = tbq; m->tsrc_slot = tg; }
                     else m->tsrc_slot = -1;
-                    if (c.crank == 0) p.trace[size_t(swarm) * p.cap + (k - 1)] = double(m->tbf);
-                    // window push + trim to tw (planner.hpp:179-180)
-                    const double wv = double(m->tbf);
-                    int wl = m->win_len, wh = m->win_head;
-                    if (p.tw <= 0) {
-                    } else if (wl < p.tw) {
-                        int at = wh + wl;
-                        if (at >= p.tw) at -= p.tw;
-                        c.win[at] = wv;
-                        ++wl;
-                    } else {
-                        c.win[wh] = wv;
-                        if (++wh == p.tw) wh = 0;
+                    if (c.crank == 0) p.trace[size_t(swarm) * p.cap + (k - 1)] = tb;
+                    if (p.tw > 0) {
+                        int at = wh0 + wl0;                       // slot of the new value
+                        if (wl0 == p.tw) at = wh0;
+                        else if (at >= p.tw) at -= p.tw;
+                        c.win[at] = tb;
                     }
                     m->win_len = wl;
                     m->win_head = wh;
-                    // auto truncation (planner.hpp:181-187, 138-149) with Q(tbest)
-                    // tracked; the std only when the cheap conjuncts hold
-                    // Exact skip: a window of n values with range r has population
-                    // std >= r / sqrt(2n); the newest-oldest gap bounds r from below.
-                    int oldest = wh;
-                    int newest = wh + wl - 1;
-                    if (newest >= p.tw) newest -= p.tw;
-                    const double gap = fabs(c.win[newest] - c.win[oldest]);
-                    const bool may_fire = !(gap >= p.at_gap);
-                    if (p.auto_truncate && wl >= p.tw && m->tbq == 0 && may_fire) {
+                }
+                __syncwarp();
+                // auto truncation (planner.hpp:181-187, 138-149) with Q(tbest)
+                // tracked.  Lane i holds window value i (oldest first); the sums
+                // stay sequential in that order, as in the reference.  The exact
+                // pre-test (std >= range / sqrt(2 tw)) skips hopeless windows.
+                if (p.auto_truncate && p.tw <= 32 && wl >= p.tw && tbq == 0) {
+                    int at = wh + lane;
+                    if (at >= p.tw) at -= p.tw;
+                    const double wv = lane < p.tw ? c.win[at] : 0.0;
+                    const double oldest = __shfl_sync(0xffffffffu, wv, 0);
+                    const double newest = __shfl_sync(0xffffffffu, wv, p.tw - 1);
+                    if (!(fabs(newest - oldest) >= p.at_gap)) {
                         double mean = 0.0;
-                        for (int i = 0, at = wh; i < p.tw; ++i) {
-                            mean = __dadd_rn(mean, c.win[at]);
-                            if (++at == p.tw) at = 0;
+#pragma unroll 4
+                        for (int i = 0; i < 32; ++i) {
+                            const double vi = __shfl_sync(0xffffffffu, wv, i);
+                            if (i < p.tw) mean = __dadd_rn(mean, vi);
                         }
                         mean = __ddiv_rn(mean, double(p.tw));
+                        const double dv = __dsub_rn(wv, mean);
+                        const double sq = __dmul_rn(dv, dv);
                         double var = 0.0;
-                        for (int i = 0, at = wh; i < p.tw; ++i) {
-                            const double dv = __dsub_rn(c.win[at], mean);
-                            var = __dadd_rn(var, __dmul_rn(dv, dv));
-                            if (++at == p.tw) at = 0;
+#pragma unroll 4
+                        for (int i = 0; i < 32; ++i) {
+                            const double si = __shfl_sync(0xffffffffu, sq, i);
+                            if (i < p.tw) var = __dadd_rn(var, si);
                         }
                         var = __ddiv_rn(var, double(p.tw));
-                        if (__dsqrt_rn(var) < p.delta) { m->truncated = 1; m->stop = 1; }
+                        if (lane == 0 && __dsqrt_rn(var) < p.delta) { m->truncated = 1; m->stop = 1; }
                     }
+                } else if (p.auto_truncate && p.tw > 32 && wl >= p.tw && tbq == 0 && lane == 0) {
+                    double mean = 0.0;
+                    for (int i = 0, at = wh; i < p.tw; ++i) {
+                        mean = __dadd_rn(mean, c.win[at]);
+                        if (++at == p.tw) at = 0;
+                    }
+                    mean = __ddiv_rn(mean, double(p.tw));
+                    double var = 0.0;
+                    for (int i = 0, at = wh; i < p.tw; ++i) {
+                        const double dv = __dsub_rn(c.win[at], mean);
+                        var = __dadd_rn(var, __dmul_rn(dv, dv));
+                        if (++at == p.tw) at = 0;
+                    }
+                    var = __ddiv_rn(var, double(p.tw));
+                    if (__dsqrt_rn(var) < p.delta) { m->truncated = 1; m->stop = 1; }
                 }
             }
             if (lane == 0) m->k_done = k;
