@@ -314,7 +314,7 @@ int sf_ctx_synchronize(sf_ctx* ctx) {
 int sf_ctx_set_launch(sf_ctx* ctx, int cluster, int threads) {
     if (!ctx) return fail(SF_INVALID_ARGUMENT, "ctx is null");
     if (cluster < 0 || cluster > 16) return fail(SF_INVALID_ARGUMENT, "cluster must be 0..16");
-    if (threads < 0 || threads > 512) return fail(SF_INVALID_ARGUMENT, "threads must be 0..512");
+    if (threads < 0 || threads > 1024) return fail(SF_INVALID_ARGUMENT, "threads must be 0..1024");
     ctx->force_cluster = cluster;
     ctx->force_threads = threads;
     return SF_OK;

@@ -220,12 +220,12 @@ FusedPlan plan_fused(sf_ctx* ctx, int problem, int n_swarms, int G, int N, int D
         if (path) {
             // worst case Rc*S*O entries; beyond the capacity entries are evaluated in place
             p.entry_cap = 0;   // overlapping obstacles are evaluated in place (no work list)
-            p.nthreads = std::min(512, std::max(128, ((Rc * S) + 31) / 32 * 32));
+            p.nthreads = std::min(1024, std::max(128, ((Rc * S) + 31) / 32 * 32));
         } else {
             p.entry_cap = 0;
             p.nthreads = std::min(512, std::max(32, (Rc + 31) / 32 * 32));
         }
-        if (want_t > 0) p.nthreads = std::min(512, std::max(32, want_t / 32 * 32));
+        if (want_t > 0) p.nthreads = std::min(1024, std::max(32, want_t / 32 * 32));
         fp.smem = smem_layout(p, fp64 ? 8 : 4, path).total;
         if (int(fp.smem) <= smem_max) { fp.fits = true; break; }
         if (C >= 16 || want_c > 0) break;

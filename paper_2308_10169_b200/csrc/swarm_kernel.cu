@@ -30,7 +30,7 @@ struct ElemWalk {
 };
 
 template <class T, bool PATH>
-__global__ void __launch_bounds__(512, 1) swarm_kernel(const __grid_constant__ SwarmParams p,
+__global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ SwarmParams p,
                                                         int problem) {
     using A = Ar<T>;
     cg::cluster_group cluster = cg::this_cluster();

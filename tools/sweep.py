@@ -12,7 +12,7 @@ planner = pe.PlannerConfig(max_iters_per_frame=30, window_carryover=True)
 cold = pe.PlannerConfig(max_iters_per_frame=30)
 res = []
 for C in (4, 8, 16):
-    for T in (256, 512):
+    for T in (256, 512, 1024):
         eng.set_launch(C, T)
         try:
             # latency: one scenario, 40 frames
