@@ -44,7 +44,7 @@ __device__ __forceinline__ bool on_segment_ref(double ax, double ay, double bx, 
 }
 
 // geometry.hpp:120-132
-static __device__ __noinline__ bool segments_intersect_ref(double a1x, double a1y, double a2x,
+static __device__ __forceinline__ bool segments_intersect_ref(double a1x, double a1y, double a2x,
                                                     double a2y, double b1x, double b1y,
                                                     double b2x, double b2y) {
     const int o1 = orient_ref(a1x, a1y, a2x, a2y, b1x, b1y);
@@ -62,7 +62,7 @@ static __device__ __noinline__ bool segments_intersect_ref(double a1x, double a1
 // geometry.hpp:135-152 -- strict even-odd containment.  `vx`/`vy` fetch vertex
 // i of the polygon (any storage type, widened to double).
 template <class VX, class VY>
-__device__ __noinline__ bool point_strictly_inside_ref(double px, double py, int n, VX vx, VY vy) {
+__device__ __forceinline__ bool point_strictly_inside_ref(double px, double py, int n, VX vx, VY vy) {
     for (int i = 0; i < n; ++i) {
         const int j = (i + 1 == n) ? 0 : i + 1;
         const double ax = vx(i), ay = vy(i), bx = vx(j), by = vy(j);

@@ -251,19 +251,20 @@ int launch_fused(sf_ctx* ctx, FusedPlan& fp, int problem) {
         cudaStreamSynchronize(ctx->stream);
         cudaFree(prof);
         fp.p.prof = nullptr;
-        static const char* names[] = {"A1", "A2", "A3+", "pbest", "part", "csync", "gath", "B1", "B2", "step"};
-        double acc[10] = {0};
+        static const char* names[] = {"prelude", "mask+pairs", "cont", "A1sync+A3", "pbest", "part",
+                                      "csync", "gath", "B1", "B2", "step"};
+        double acc[11] = {0};
         int iters = 0;
         for (int k = 0; k < fp.p.cap; ++k) {
             const long long* r = h.data() + size_t(k) * kProfPhases;
             if (r[0] == 0) break;
             ++iters;
-            const long long t[11] = {r[0], r[1], r[2], r[4], r[5], r[6], r[7], r[8], r[9], r[10], r[11]};
-            for (int i = 0; i < 10; ++i) if (t[i + 1] > t[i]) acc[i] += double(t[i + 1] - t[i]);
+            const long long t[12] = {r[0], r[1], r[2], r[3], r[4], r[5], r[6], r[7], r[8], r[9], r[10], r[11]};
+            for (int i = 0; i < 11; ++i) if (t[i + 1] > t[i]) acc[i] += double(t[i + 1] - t[i]);
         }
         std::fprintf(stderr, "[phase] C=%d T=%d iters=%d cycles/iter:", fp.p.C, fp.p.nthreads, iters);
-        for (int i = 0; i < 10; ++i) std::fprintf(stderr, " %s=%.0f", names[i], iters ? acc[i] / iters : 0.0);
-        std::fprintf(stderr, " entries(it1)=%lld\n", h[3]);
+        for (int i = 0; i < 11; ++i) std::fprintf(stderr, " %s=%.0f", names[i], iters ? acc[i] / iters : 0.0);
+        std::fprintf(stderr, "\n");
     }
     if (e != 0) return cuda_fail(cudaError_t(e), "fused swarm launch");
     if (ctx->timing) {

@@ -248,6 +248,32 @@ inline __device__ int pair_count_pts(const Ctx<float>& c, float a1x, float a1y, 
     const float B = 2.9e-6f * L * L + 4e-12f;
     const int v0 = c.ooff[o], v1 = c.ooff[o + 1];
     const float4* E = reinterpret_cast<const float4*>(c.edge);
+    if (v1 - v0 == 4) {
+        // quadrilaterals (every obstacle of the paper's scenes): all loads and
+        // crosses issue together -- no loop-carried latency chain
+        const float4 e0 = E[v0], e1 = E[v0 + 1], e2 = E[v0 + 2], e3 = E[v0 + 3];
+        const float cv0 = fmaf(dx, e0.y - a1y, -(dy * (e0.x - a1x)));
+        const float cv1 = fmaf(dx, e1.y - a1y, -(dy * (e1.x - a1x)));
+        const float cv2 = fmaf(dx, e2.y - a1y, -(dy * (e2.x - a1x)));
+        const float cv3 = fmaf(dx, e3.y - a1y, -(dy * (e3.x - a1x)));
+        if (c.ofl[o]) {
+            const float mn = fminf(fminf(cv0, cv1), fminf(cv2, cv3));
+            const float mx = fmaxf(fmaxf(cv0, cv1), fmaxf(cv2, cv3));
+            if (mn > B || mx < -B) return 0;          // vertex-cross early exit
+        }
+        int r0 = fast_pair(a1x, a1y, dx, dy, e0.x, e0.y, e0.z, e0.w, B);
+        int r1 = fast_pair(a1x, a1y, dx, dy, e1.x, e1.y, e1.z, e1.w, B);
+        int r2 = fast_pair(a1x, a1y, dx, dy, e2.x, e2.y, e2.z, e2.w, B);
+        int r3 = fast_pair(a1x, a1y, dx, dy, e3.x, e3.y, e3.z, e3.w, B);
+        if ((r0 | r1 | r2 | r3) < 0) {                 // some sign uncertain: FP64 reference
+            const float* vv = c.vert + 2 * v0;
+            if (r0 < 0) r0 = segments_intersect_ref(a1x, a1y, a2x, a2y, vv[0], vv[1], vv[2], vv[3]);
+            if (r1 < 0) r1 = segments_intersect_ref(a1x, a1y, a2x, a2y, vv[2], vv[3], vv[4], vv[5]);
+            if (r2 < 0) r2 = segments_intersect_ref(a1x, a1y, a2x, a2y, vv[4], vv[5], vv[6], vv[7]);
+            if (r3 < 0) r3 = segments_intersect_ref(a1x, a1y, a2x, a2y, vv[6], vv[7], vv[0], vv[1]);
+        }
+        return r0 + r1 + r2 + r3;
+    }
     if (c.ofl[o]) {
         bool pos = true, neg = true;
         for (int i = v0; i < v1; ++i) {
@@ -263,6 +289,9 @@ inline __device__ int pair_count_pts(const Ctx<float>& c, float a1x, float a1y, 
         const float4 e = E[i];
         int r = fast_pair(a1x, a1y, dx, dy, e.x, e.y, e.z, e.w, B);
         if (r < 0) {
+#ifdef SEPSO_COUNT_FALLBACKS
+            atomicAdd(&c.m->n_cont, 1);
+#endif
             const int j = (i + 1 == v1) ? v0 : i + 1;
             r = segments_intersect_ref(a1x, a1y, a2x, a2y, c.vert[2 * i], c.vert[2 * i + 1],
                                        c.vert[2 * j], c.vert[2 * j + 1]);
@@ -310,6 +339,20 @@ template <> inline __device__ int contain_count<float>(const Ctx<float>& c, int 
     const int v0 = c.ooff[o], v1 = c.ooff[o + 1];
     const float4* E = reinterpret_cast<const float4*>(c.edge);
     bool inside = false;
+    if (v1 - v0 == 4) {
+        const float4 e[4] = {E[v0], E[v0 + 1], E[v0 + 2], E[v0 + 3]};
+        float cr[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cr[i] = fmaf(e[i].z, py - e[i].y, -(e[i].w * (px - e[i].x)));
+        if (!(fminf(fminf(fabsf(cr[0]), fabsf(cr[1])), fminf(fabsf(cr[2]), fabsf(cr[3]))) > B))
+            return contain_count_ref(c, pl, o);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float ay = e[i].y, by = e[(i + 1) & 3].y;
+            if ((ay > py) != (by > py) && ((cr[i] > 0.f) == (by > ay))) inside = !inside;
+        }
+        return inside ? 1 : 0;
+    }
     for (int i = v0; i < v1; ++i) {
         const float4 e = E[i];                       // a = (e.x, e.y), b - a = (e.z, e.w)
         const float cr = fmaf(e.z, py - e.y, -(e.w * (px - e.x)));
@@ -414,6 +457,7 @@ __device__ void path_fitness_phase(const SwarmParams& p, Ctx<T>& c, long long* p
             c.seglen[pl * S + s] = seg_length<T>(Ar<T>::sub(a2x, a1x), Ar<T>::sub(a2y, a1y));
             const T lx = a1x < a2x ? a1x : a2x, hx = a1x < a2x ? a2x : a1x;
             const T ly = a1y < a2y ? a1y : a2y, hy = a1y < a2y ? a2y : a1y;
+            if (prof && it == tid) prof[(k - 1) * kProfPhases + 1] = clock64();
             int cnt = 0;
             for (int o0 = 0; o0 < O; o0 += 32) {
                 uint32_t mask = 0;
@@ -427,6 +471,7 @@ __device__ void path_fitness_phase(const SwarmParams& p, Ctx<T>& c, long long* p
                     cnt += pair_count_pts(c, a1x, a1y, a2x, a2y, o0 + j);
                 }
             }
+            if (prof && it == tid) prof[(k - 1) * kProfPhases + 2] = clock64();
             if (cnt) atomicAdd(&c.q[pl], cnt);
             pl += step_pl;
             s += step_s;
@@ -447,13 +492,9 @@ __device__ void path_fitness_phase(const SwarmParams& p, Ctx<T>& c, long long* p
             }
             if (hits) atomicAdd(&c.q[t], hits);
         }
+        if (prof) prof[(k - 1) * kProfPhases + 3] = clock64();
     }
     __syncthreads();
-    if (prof) {
-        prof[(k - 1) * kProfPhases + 1] = clock64();
-        prof[(k - 1) * kProfPhases + 2] = clock64();
-        prof[(k - 1) * kProfPhases + 3] = 0;
-    }
     // ---- A3
     for (int pl = tid; pl < c.P; pl += nthr) {
         T len = T(0);

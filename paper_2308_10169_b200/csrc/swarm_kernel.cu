@@ -348,24 +348,21 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
         __syncthreads();
         SEPSO_MARK(9);
         if (c.m->status) break;
-        // copy improved group bests (and the new tbest) from the pushed rows
-        {
-            const int tg = c.m->tsrc_slot;
-            for (int t = tid; t < G * D; t += nthr) {
-                const int g = int(c.fD.div(uint32_t(t))), d = t - g * D;
-                const int slot = c.chg[g];
-                if (slot >= 0) {
-                    const T val = c.px[(buf * c.C * LGM + slot) * D + d];
-                    c.gbx[g * D + d] = val;
-                    if (g == tg) c.tbx[d] = val;
-                }
-            }
-        }
-        __syncthreads();
         SEPSO_MARK(10);
-        if (c.m->stop) break;
-        if (k == p.cap) break;        // plan_frame: no step after the last iteration
+        const int tg = c.m->tsrc_slot;                     // new tbest's group or -1
+        const int tslot = tg >= 0 ? c.chg[tg] : -1;
+        const T* pxb = c.px + size_t(buf) * c.C * LGM * D;  // this iteration's pushed rows
+        if (c.m->stop || k == p.cap) {                       // no step after the last iteration
+            if (tslot >= 0)
+                for (int d = tid; d < D; d += nthr) c.tbx[d] = pxb[tslot * D + d];
+            __syncthreads();
+            break;
+        }
         // --------------------------------------------------- step k (swarm.hpp:138-174)
+        // Improved group bests / the new tbest are read straight from the pushed
+        // rows; the first local particle of each group (and particle 0 for tbest)
+        // persists them for the next iteration.  Readers of gbx / tbx only read
+        // when the entry did not change, so the in-loop writes cannot race.
         {
             const T frac = T(double(k) / double(p.cap));           // inertia_at (swarm.hpp:81-84)
             ElemWalk w(c.fD, tid, nthr, D);
@@ -377,10 +374,15 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
                 const T wt = A::sub(h[3], A::mul(A::sub(h[3], h[4]), frac));
                 const T lo = c.lo[d], hi = c.hi[d];
                 const T vmax = A::mul(h[5], A::sub(hi, lo));
+                const int gslot = c.chg[g];
+                const T gv = gslot >= 0 ? pxb[gslot * D + d] : c.gbx[g * D + d];
+                const T tv = tslot >= 0 ? pxb[tslot * D + d] : c.tbx[d];
+                if (gslot >= 0 && c.row0 + pl == max(g * N, c.row0)) c.gbx[g * D + d] = gv;
+                if (tslot >= 0 && pl == 0) c.tbx[d] = tv;
                 const T xv = c.x[e];
                 T nv = A::add(A::add(A::add(A::mul(wt, c.v[e]), A::mul(c.coef[pl], A::sub(c.pb[e], xv))),
-                                     A::mul(c.coef[c.P + pl], A::sub(c.gbx[g * D + d], xv))),
-                              A::mul(c.coef[2 * c.P + pl], A::sub(c.tbx[d], xv)));
+                                     A::mul(c.coef[c.P + pl], A::sub(gv, xv))),
+                              A::mul(c.coef[2 * c.P + pl], A::sub(tv, xv)));
                 nv = clampT(nv, T(-vmax), vmax);
                 c.v[e] = nv;
                 c.x[e] = clampT(A::add(xv, nv), lo, hi);
