@@ -362,7 +362,7 @@ def main():
             "scaling": "weak",
             "vs_baseline": value / PUBLISHED_PLANS_PER_S if a.workload == "scene" else None,
             "dtype": a.precision,
-            "data": "synthetic (seeded generate_world scenes, Philox draw stream)",
+            "data": "synthetic (seeded generate_world scenes; the reference's mt19937_64 draw stream, generated on the device)",
             "config": {
                 "workload": ("config2: paper dynamic scene (366 cm, 6 dynamic + 2 static obstacles), "
                              "SEPSO evolved hypers + PI + AT, G=8 N=170 D=16, cap 30, window carryover, "

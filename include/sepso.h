@@ -44,6 +44,14 @@ typedef enum sf_status {
 
 typedef enum sf_precision { SF_FP32 = 0, SF_FP64 = 1 } sf_precision;
 
+/* Random stream.  SF_RNG_MT19937 is the reference's own
+ * std::mt19937_64 stream (rng.hpp:13-28), generated on the device in the
+ * reference's draw order: with SF_FP64 the engine reproduces the UNMODIFIED
+ * reference bit for bit.  SF_RNG_PHILOX is the counter-based stream (random
+ * access, no sequential generator) shared with the harness build
+ * oracle/_ref/libsfref_philox.so.  Default: SF_RNG_MT19937. */
+typedef enum sf_rng { SF_RNG_PHILOX = 0, SF_RNG_MT19937 = 1 } sf_rng;
+
 typedef enum sf_problem_kind {   /* FitnessProblem implementations (problem.hpp:14-31) */
     SF_PROBLEM_PATH = 0,         /* PathPlanningProblem (geometry.hpp:245-279) */
     SF_PROBLEM_SPHERE = 1,       /* BenchmarkProblem BF1 (benchmarks.hpp:16-95) */
@@ -100,6 +108,8 @@ void* sf_ctx_stream(sf_ctx* ctx);                            /* cudaStream_t of 
 int sf_ctx_synchronize(sf_ctx* ctx);
 /* Launch tuning (0 = heuristic): cluster size, threads per CTA. */
 int sf_ctx_set_launch(sf_ctx* ctx, int cluster, int threads);
+int sf_ctx_set_rng(sf_ctx* ctx, int rng);
+int sf_ctx_rng(const sf_ctx* ctx);
 /* Device time of the engine kernels, bracketed by CUDA events on the context
  * stream while enabled: total milliseconds and launch count since enable. */
 int sf_ctx_enable_timing(sf_ctx* ctx, int enable);
@@ -194,7 +204,7 @@ typedef struct sf_scenario_config {                          /* ScenarioConfig, 
 
 /* generate_world (simenv.hpp:83-132) with the engine stream: rectangles.
  * offsets (n+1), vertices (4n), velocities (n) out; n = dynamic + static. */
-int sf_generate_world(const sf_scenario_config* cfg, uint64_t seed, sf_world* world_out,
+int sf_generate_world(const sf_scenario_config* cfg, uint64_t seed, int rng, sf_world* world_out,
                       uint32_t* offsets, sf_point* vertices, sf_point* velocities);
 /* step_world (simenv.hpp:155-184), in place on caller-owned buffers */
 int sf_step_world(sf_world* world, sf_point* vertices, sf_point* velocities, double dt);

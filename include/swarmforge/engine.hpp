@@ -36,6 +36,12 @@ private:
 
 namespace engine {
 
+/// SEPSO_RNG=philox selects the counter-based stream; default: the reference's mt19937_64.
+inline int rng_kind() {
+    const char* r = std::getenv("SEPSO_RNG");
+    return (r && std::strcmp(r, "philox") == 0) ? SF_RNG_PHILOX : SF_RNG_MT19937;
+}
+
 inline void check(int status, const std::uint64_t* bad = nullptr) {
     if (status == SF_OK) return;
     const std::string msg = sf_last_error();
@@ -51,6 +57,7 @@ struct Context {
         const char* prec = std::getenv("SEPSO_PRECISION");
         const int precision = (prec && std::strcmp(prec, "fp64") == 0) ? SF_FP64 : SF_FP32;
         check(sf_ctx_create(dev ? std::atoi(dev) : 0, precision, &ctx));
+        check(sf_ctx_set_rng(ctx, rng_kind()));
     }
     ~Context() { sf_ctx_destroy(ctx); }
     Context(const Context&) = delete;

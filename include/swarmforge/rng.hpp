@@ -1,14 +1,17 @@
 // swarmforge/rng.hpp -- drop-in for the reference's rng.hpp:1-61.
 //
 // Same interface (RngStream{uniform(), uniform(lo, hi), seed()}, derive_seed)
-// and the same seed derivation (splitmix64 of root ^ FNV-1a(tag)); the words
-// come from the engine's counter-based stream instead of mt19937_64: word i is
-// half (i & 1) of Philox4x32-10 block i >> 1 keyed by the seed (DESIGN.md "RNG
-// contract").  Every engine kernel computes the index of the draw it needs, so
-// host and device consume the identical sequence in the reference's order.
+// and seed derivation.  The stream is the engine context's: std::mt19937_64
+// (the reference's, default) or the counter-based Philox stream (SEPSO_RNG=
+// philox; word i = half (i & 1) of Philox4x32-10 block i >> 1).  drawn() is the
+// stream position the device resumes from, so host and device consume the
+// identical sequence in the reference's order.
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <random>
 #include <string_view>
 
 namespace swarmforge {
@@ -35,17 +38,30 @@ inline std::uint64_t philox_word(std::uint64_t seed, std::uint64_t index) {
 
 class RngStream {
 public:
-    explicit RngStream(std::uint64_t seed) : seed_(seed) {}
-    double uniform() { return double(rng_detail::philox_word(seed_, drawn_++) >> 11) * 0x1.0p-53; }
+    explicit RngStream(std::uint64_t seed) : seed_(seed), engine_(seed) {
+        const char* r = std::getenv("SEPSO_RNG");
+        philox_ = r && std::strcmp(r, "philox") == 0;
+    }
+    double uniform() { return double(next() >> 11) * 0x1.0p-53; }
     double uniform(double lo, double hi) { return lo + uniform() * (hi - lo); }
     std::uint64_t seed() const { return seed_; }
-    /// Draws consumed so far: the counter the engine's index algebra starts from.
+    /// Draws consumed so far: the position the engine's index algebra resumes at.
     std::uint64_t drawn() const { return drawn_; }
-    void skip(std::uint64_t n) { drawn_ += n; }
+    /// Advance past n draws the device consumed.
+    void skip(std::uint64_t n) {
+        if (!philox_) engine_.discard(n);
+        drawn_ += n;
+    }
 
 private:
+    std::uint64_t next() {
+        const std::uint64_t i = drawn_++;
+        return philox_ ? rng_detail::philox_word(seed_, i) : engine_();
+    }
     std::uint64_t seed_;
     std::uint64_t drawn_ = 0;
+    bool philox_ = false;
+    std::mt19937_64 engine_;
 };
 
 namespace detail {

@@ -320,6 +320,15 @@ int sf_ctx_set_launch(sf_ctx* ctx, int cluster, int threads) {
     return SF_OK;
 }
 
+int sf_ctx_set_rng(sf_ctx* ctx, int rng) {
+    if (!ctx) return fail(SF_INVALID_ARGUMENT, "ctx is null");
+    if (rng != SF_RNG_PHILOX && rng != SF_RNG_MT19937) return fail(SF_INVALID_ARGUMENT, "unknown rng");
+    ctx->rng = rng;
+    return SF_OK;
+}
+
+int sf_ctx_rng(const sf_ctx* ctx) { return ctx ? ctx->rng : -1; }
+
 int sf_ctx_enable_timing(sf_ctx* ctx, int enable) {
     if (!ctx) return fail(SF_INVALID_ARGUMENT, "ctx is null");
     ctx->timing = enable != 0;
@@ -578,7 +587,7 @@ int sf_evolve(sf_ctx* ctx, const sf_problem* pr, uint32_t iG, uint32_t iN, uint3
         for (int f = 0; f < 6; ++f) { lo[6 * g + f] = flo[f]; hi[6 * g + f] = fhi[f]; }
     const uint64_t outer_seed = derive_seed(seed, "outer");
     const uint64_t lfv_root = derive_seed(seed, "lfv");
-    HostStream rng(outer_seed);
+    HostStream rng(outer_seed, ctx->rng);
     HostSwarm s;
     host_init_swarm(s, outer_hypers, lo.data(), hi.data(), oG, oN, dim, rng);
     const uint32_t cand = oG * oN;
@@ -663,9 +672,22 @@ int sf_init_swarm(sf_ctx* ctx, const double* hypers, const double* lo, const dou
     up(ctx, a.at(ohi), bhi.data(), bhi.size());
     if (prev) up(ctx, a.at(op), prev, size_t(D) * 8);
     const StageShape s{int(G), int(N), int(D), 0, int(G * N)};
+    unsigned long long* words = nullptr;
+    if (ctx->rng == SF_RNG_MT19937) {   // the window [first_draw, first_draw + 2RD) of the reference stream
+        DevBuf& wb = ctx->flush;
+        const size_t n = 2 * E;
+        cudaError_t ce = wb.ensure(n * 8 + sizeof(MtPersist));
+        if (ce != cudaSuccess) return cuda_fail(ce, "mt window");
+        words = static_cast<unsigned long long*>(wb.p);
+        MtPersist* g = reinterpret_cast<MtPersist*>(static_cast<unsigned char*>(wb.p) + n * 8);
+        const int fe = stage_mt_fill(g, seed, true, (long long)first_draw, (long long)(first_draw + n), words,
+                                     ctx->stream);
+        if (fe) return cuda_fail(cudaError_t(fe), "stage_mt_fill");
+    }
     const int e = stage_init(ctx->precision == SF_FP64, s, reinterpret_cast<double*>(a.at(oh)), a.at(olo),
                              a.at(ohi), seed, first_draw, prev ? reinterpret_cast<double*>(a.at(op)) : nullptr,
-                             prev ? int(warm) : 0, pi_radius, a.at(ox), a.at(ov), a.at(opb), ctx->stream);
+                             prev ? int(warm) : 0, pi_radius, a.at(ox), a.at(ov), a.at(opb), ctx->stream, words,
+                             (long long)first_draw);
     if (e) return cuda_fail(cudaError_t(e), "stage_init");
     std::vector<unsigned char> hx(E * ts), hv(E * ts);
     down(ctx, hx.data(), a.at(ox), hx.size());
@@ -701,9 +723,21 @@ int sf_step(sf_ctx* ctx, const double* hypers, const double* lo, const double* h
     to_dev_type(ctx, gbx, size_t(G) * D, b); up(ctx, a.at(og), b.data(), b.size()); sync(ctx);
     to_dev_type(ctx, tbx, D, b); up(ctx, a.at(ot), b.data(), b.size()); sync(ctx);
     const StageShape s{int(G), int(N), int(D), 0, int(G * N)};
+    unsigned long long* words = nullptr;
+    if (ctx->rng == SF_RNG_MT19937) {   // draws [first_draw, first_draw + 3R) of the reference stream
+        DevBuf& wb = ctx->flush;
+        const size_t n = 3 * size_t(G) * N;
+        cudaError_t ce = wb.ensure(n * 8 + sizeof(MtPersist));
+        if (ce != cudaSuccess) return cuda_fail(ce, "mt window");
+        words = static_cast<unsigned long long*>(wb.p);
+        MtPersist* g = reinterpret_cast<MtPersist*>(static_cast<unsigned char*>(wb.p) + n * 8);
+        const int fe = stage_mt_fill(g, seed, true, (long long)first_draw, (long long)(first_draw + n), words,
+                                     ctx->stream);
+        if (fe) return cuda_fail(cudaError_t(fe), "stage_mt_fill");
+    }
     const int e = stage_step(ctx->precision == SF_FP64, s, reinterpret_cast<double*>(a.at(oh)), a.at(olo),
-                             a.at(ohi), a.at(ox), a.at(ov), a.at(opb), a.at(og), a.at(ot), seed,
-                             first_draw, int(k), int(T), nullptr, ctx->stream);
+                             a.at(ohi), a.at(ox), a.at(ov), a.at(opb), a.at(og), a.at(ot), seed, first_draw,
+                             int(k), int(T), nullptr, ctx->stream, words, (long long)first_draw);
     if (e) return cuda_fail(cudaError_t(e), "stage_step");
     std::vector<unsigned char> hx(E * ts), hv(E * ts);
     down(ctx, hx.data(), a.at(ox), hx.size());
@@ -860,8 +894,8 @@ int sf_should_truncate(const double* window, uint32_t len, int cf, const sf_plan
 
 // ------------------------------------------------------------- scene state
 // simenv.hpp:83-132 over the engine stream (RngStream = Philox contract)
-int sf_generate_world(const sf_scenario_config* c, uint64_t seed, sf_world* w, uint32_t* offsets,
-                      sf_point* verts, sf_point* vel) {
+int sf_generate_world(const sf_scenario_config* c, uint64_t seed, int rng_kind, sf_world* w,
+                      uint32_t* offsets, sf_point* verts, sf_point* vel) {
     if (!c || !w || !offsets || !verts || !vel) return fail(SF_INVALID_ARGUMENT, "null argument");
     if (!(c->map_size > 0.0)) return fail(SF_INVALID_ARGUMENT, "scenario: map size must be positive");
     if (!(c->min_side > 0.0) || c->min_side > c->max_side || c->max_side >= c->map_size)
@@ -869,7 +903,7 @@ int sf_generate_world(const sf_scenario_config* c, uint64_t seed, sf_world* w, u
     if (!(c->max_speed > 0.0)) return fail(SF_INVALID_ARGUMENT, "scenario: max speed must be positive");
     if (c->frames < 1) return fail(SF_INVALID_ARGUMENT, "scenario: frame count must be >= 1");
     if (!(c->dt > 0.0)) return fail(SF_INVALID_ARGUMENT, "scenario: dt must be positive");
-    HostStream rng(seed);
+    HostStream rng(seed, rng_kind);
     const double M = c->map_size;
     w->width = M;
     w->height = M;
@@ -991,7 +1025,8 @@ int sf_run_scenario(sf_ctx* ctx, const sf_scenario_config* c, int variant, uint3
     std::vector<uint32_t> off(n + 1);
     std::vector<sf_point> verts(4 * size_t(n)), vel(n);
     sf_world w{};
-    int st = sf_generate_world(&sc, derive_seed(c->root_seed, "world"), &w, off.data(), verts.data(), vel.data());
+    int st = sf_generate_world(&sc, derive_seed(c->root_seed, "world"), ctx->rng, &w, off.data(), verts.data(),
+                               vel.data());
     if (st) return st;
     std::vector<double> prev(cfg.dim), win(std::max<uint32_t>(cfg.tw, 1) + 1);
     uint32_t wl = 0;
@@ -1130,8 +1165,8 @@ int sf_scene_batch_create(sf_ctx* ctx, uint32_t n, const sf_scenario_config* cfg
         off[s].resize(k + 1);
         verts[s].resize(4 * size_t(k) + 1);
         vel[s].resize(size_t(k) + 1);
-        if ((st = sf_generate_world(&cfgs[s], derive_seed(cfgs[s].root_seed, "world"), &ws[s], off[s].data(),
-                                    verts[s].data(), vel[s].data())))
+        if ((st = sf_generate_world(&cfgs[s], derive_seed(cfgs[s].root_seed, "world"), ctx->rng, &ws[s],
+                                    off[s].data(), verts[s].data(), vel[s].data())))
             return st;
     }
     WorldPack wp;

@@ -226,6 +226,8 @@ FusedPlan plan_fused(sf_ctx* ctx, int problem, int n_swarms, int G, int N, int D
             p.nthreads = std::min(512, std::max(32, (Rc + 31) / 32 * 32));
         }
         if (want_t > 0) p.nthreads = std::min(1024, std::max(32, want_t / 32 * 32));
+        p.rng = ctx->rng;
+        if (p.rng == SF_RNG_MT19937) p.nthreads = std::max(p.nthreads, 320);   // one 312-word block per pass
         fp.smem = smem_layout(p, fp64 ? 8 : 4, path).total;
         if (int(fp.smem) <= smem_max) { fp.fits = true; break; }
         if (C >= 16 || want_c > 0) break;
@@ -322,6 +324,9 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
     const size_t o_st = take(sizeof(IterState));
     const size_t o_win = take(size_t(std::max(r.tw, 1)) * 8);
     const size_t o_trace = take(size_t(r.cap) * 8);
+    const bool mt = ctx->rng == SF_RNG_MT19937;
+    const size_t o_mt = take(mt ? sizeof(MtPersist) : 0);
+    const size_t o_words = take(mt ? size_t(2) * R * D * 8 : 0);   // init window; steps reuse it
     cudaError_t ce = ctx->scratch.ensure(off);
     if (ce != cudaSuccess) return cuda_fail(ce, "staged arena");
     unsigned char* dev = static_cast<unsigned char*>(ctx->scratch.p);
@@ -366,9 +371,15 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
     if (ctx->timing) cudaEventRecord(ctx->ev0, st);
     const StageShape s{G, N, D, row_begin, RL};
     IterState* dst = reinterpret_cast<IterState*>(dev + o_st);
+    unsigned long long* words = mt ? reinterpret_cast<unsigned long long*>(dev + o_words) : nullptr;
+    MtPersist* mtg = mt ? reinterpret_cast<MtPersist*>(dev + o_mt) : nullptr;
+    if (mt) {   // the reference stream, sequential: init words [0, 2RD)
+        const int fe = stage_mt_fill(mtg, r.seed, true, 0, 2ll * R * D, words, st);
+        if (fe) return cuda_fail(cudaError_t(fe), "stage_mt_fill");
+    }
     int e = stage_init(fp64, s, reinterpret_cast<double*>(dev + o_hyp), dev + o_lo, dev + o_hi, r.seed, 0,
                        r.prev ? reinterpret_cast<double*>(dev + o_prev) : nullptr, r.warm, r.pi_radius,
-                       dev + o_x, dev + o_v, dev + o_pb, st);
+                       dev + o_x, dev + o_v, dev + o_pb, st, words, 0);
     if (e) return cuda_fail(cudaError_t(e), "stage_init");
     const WorldLayout& wl = wp.lay;
     for (int k = 1; k <= r.cap; ++k) {
@@ -399,9 +410,13 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
         if (e) return cuda_fail(cudaError_t(e), "stage_finish");
         if (k < r.cap) {
             const uint64_t first = 2ull * uint64_t(R) * D + uint64_t(k - 1) * 3ull * R;
+            if (mt) {   // draws of step k (the generator persists across iterations)
+                const int fe = stage_mt_fill(mtg, r.seed, false, (long long)first, (long long)first + 3ll * R, words, st);
+                if (fe) return cuda_fail(cudaError_t(fe), "stage_mt_fill");
+            }
             e = stage_step(fp64, s, reinterpret_cast<double*>(dev + o_hyp), dev + o_lo, dev + o_hi,
                            dev + o_x, dev + o_v, dev + o_pb, dev + o_gbx, dev + o_tbx, r.seed, first,
-                           k, r.cap, dst, st);
+                           k, r.cap, dst, st, words, (long long)first);
             if (e) return cuda_fail(cudaError_t(e), "stage_step");
         }
     }

@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -39,6 +40,7 @@ struct PinnedBuf {
 struct sf_ctx {
     int device = 0;
     int precision = SF_FP32;
+    int rng = SF_RNG_MT19937;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool timing = false;
@@ -123,10 +125,16 @@ bool force_staged();
 // The HSEF outer swarm lives on the host (hsef.hpp:144-165); this is the
 // reference's batched update restated in C++ over the engine's Philox stream
 // (sequential draw counter), compiled with -ffp-contract=off.
-struct HostStream {
+struct HostStream {            // RngStream (rng.hpp:13-28) over either engine stream
     uint64_t seed, drawn = 0;
-    explicit HostStream(uint64_t s) : seed(s) {}
-    double uniform() { return double(philox_word(seed, drawn++) >> 11) * 0x1.0p-53; }
+    bool mt;
+    std::mt19937_64 eng;
+    HostStream(uint64_t s, int rng) : seed(s), mt(rng == SF_RNG_MT19937), eng(s) {}
+    uint64_t next() {
+        const uint64_t i = drawn++;
+        return mt ? eng() : philox_word(seed, i);
+    }
+    double uniform() { return double(next() >> 11) * 0x1.0p-53; }
     double uniform(double lo, double hi) { return lo + uniform() * (hi - lo); }
 };
 

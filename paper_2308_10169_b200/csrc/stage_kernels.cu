@@ -3,6 +3,7 @@
 
 #include <algorithm>
 
+#include "mt19937.cuh"
 #include "stage_kernels.cuh"
 #include "swarm_device.cuh"
 
@@ -26,13 +27,47 @@ static inline unsigned grid_for(long long work, int block) {
     return unsigned(g < 1 ? 1 : g);
 }
 
+// word i of the stream: Philox by index, or a pre-generated mt19937_64 window
+__device__ __forceinline__ uint64_t stream_word(uint64_t seed, uint64_t i, const unsigned long long* words,
+                                                long long base) {
+    return words ? words[(long long)i - base] : philox_word(seed, i);
+}
+
+// Advance a persisted mt19937_64 generator (one CTA, 320+ threads) and write
+// words [from, upto) to out[w - from]; words before `from` are skipped.
+__global__ void __launch_bounds__(320) k_mt_fill(MtPersist* g, unsigned long long seed, int reseed,
+                                                 long long from, long long upto,
+                                                 unsigned long long* out) {
+    __shared__ unsigned long long buf[2 * 312];
+    MtState s{buf, 0, 0};
+    if (reseed) {
+        mt_seed(s, seed);
+    } else {
+        for (int i = threadIdx.x; i < 312; i += blockDim.x) buf[i] = g->st[i];
+        s.blocks = g->blocks;
+        __syncthreads();
+    }
+    const long long base = from;
+    mt_deliver(s, from < 0 ? 0 : from, upto, [&](long long w, unsigned long long word) {
+        if (out) out[w - base] = word;
+    });
+    for (int i = threadIdx.x; i < 312; i += blockDim.x) g->st[i] = buf[s.cur * 312 + i];
+    if (threadIdx.x == 0) g->blocks = s.blocks;
+}
+
+int stage_mt_fill(MtPersist* g, unsigned long long seed, bool reseed, long long from, long long upto,
+                  unsigned long long* out, void* stream) {
+    k_mt_fill<<<1, 320, 0, static_cast<cudaStream_t>(stream)>>>(g, seed, reseed ? 1 : 0, from, upto, out);
+    return int(cudaGetLastError());
+}
+
 // --------------------------------------------------------------------- init
 // swarm.hpp:94-132 / planner.hpp:77-133 (draws indexed by global row)
 template <class T>
 __global__ void k_init(StageShape s, const double* __restrict__ hypers, const T* __restrict__ lo,
                        const T* __restrict__ hi, uint64_t seed, uint64_t first,
                        const double* __restrict__ prev, int warm, double pi_radius, T* x, T* v,
-                       T* pb) {
+                       T* pb, const unsigned long long* words, long long wbase) {
     using A = Ar<T>;
     const long long total = (long long)s.rows * s.D;
     const int R = s.G * s.N;
@@ -42,7 +77,7 @@ __global__ void k_init(StageShape s, const double* __restrict__ hypers, const T*
         const int rl = int(e / s.D), d = int(e - (long long)rl * s.D);
         const int row = s.row_begin + rl, g = row / s.N, n = row - g * s.N;
         const uint64_t ix = first + uint64_t(row) * uint64_t(s.D) + uint64_t(d);
-        const T ux = unit_from_word<T>(philox_word(seed, ix));
+        const T ux = unit_from_word<T>(stream_word(seed, ix, words, wbase));
         const T l0 = lo[d], h0 = hi[d];
         T xv;
         if (prev != nullptr && n < warm) {
@@ -53,7 +88,7 @@ __global__ void k_init(StageShape s, const double* __restrict__ hypers, const T*
         } else {
             xv = A::add(l0, A::mul(ux, A::sub(h0, l0)));
         }
-        const T uv = unit_from_word<T>(philox_word(seed, uint64_t(R) * s.D + ix));
+        const T uv = unit_from_word<T>(stream_word(seed, uint64_t(R) * s.D + ix, words, wbase));
         const T vmax = A::mul(T(hypers[g * 6 + 5]), A::sub(h0, l0));
         const T vlo = -vmax;
         x[e] = xv;
@@ -64,17 +99,18 @@ __global__ void k_init(StageShape s, const double* __restrict__ hypers, const T*
 
 int stage_init(bool fp64, const StageShape& s, const double* hypers, const void* lo,
                const void* hi, uint64_t seed, uint64_t first, const double* prev, int warm,
-               double pi_radius, void* x, void* v, void* pb, void* stream) {
+               double pi_radius, void* x, void* v, void* pb, void* stream,
+               const unsigned long long* words, long long wbase) {
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     const unsigned grid = grid_for((long long)s.rows * s.D, 256);
     if (fp64)
         k_init<double><<<grid, 256, 0, st>>>(s, hypers, (const double*)lo, (const double*)hi, seed,
                                               first, prev, warm, pi_radius, (double*)x, (double*)v,
-                                              (double*)pb);
+                                              (double*)pb, words, wbase);
     else
         k_init<float><<<grid, 256, 0, st>>>(s, hypers, (const float*)lo, (const float*)hi, seed,
                                              first, prev, warm, pi_radius, (float*)x, (float*)v,
-                                             (float*)pb);
+                                             (float*)pb, words, wbase);
     return int(cudaGetLastError());
 }
 
@@ -93,7 +129,8 @@ __global__ void __launch_bounds__(256) k_step(StageShape s, const double* __rest
                                               const T* __restrict__ pb, const T* __restrict__ gbx,
                                               const T* __restrict__ tbx, uint64_t seed,
                                               uint64_t first_draw, int k, int total,
-                                              const IterState* gate) {
+                                              const IterState* gate,
+                                              const unsigned long long* words, long long wbase) {
     using A = Ar<T>;
     if (gate != nullptr && gate->stop) return;
     __shared__ T coef[3 * kStepRows];
@@ -112,7 +149,7 @@ __global__ void __launch_bounds__(256) k_step(StageShape s, const double* __rest
     for (int t = threadIdx.x; t < 3 * nr; t += blockDim.x) {
         const int j = t / nr, rl = t - j * nr;
         const int row = s.row_begin + r0 + rl, g = row / s.N;
-        const T u = unit_from_word<T>(philox_word(seed, first_draw + uint64_t(j) * R + row));
+        const T u = unit_from_word<T>(stream_word(seed, first_draw + uint64_t(j) * R + row, words, wbase));
         coef[j * kStepRows + rl] = A::mul(T(hypers[g * 6 + j]), u);
     }
     __syncthreads();
@@ -164,7 +201,8 @@ __global__ void __launch_bounds__(256) k_step(StageShape s, const double* __rest
 int stage_step(bool fp64, const StageShape& s, const double* hypers, const void* lo,
                const void* hi, void* x, void* v, const void* pb, const void* gbx,
                const void* tbx, uint64_t seed, uint64_t first_draw, int k, int total,
-               const IterState* gate, void* stream) {
+               const IterState* gate, void* stream, const unsigned long long* words,
+               long long wbase) {
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     const unsigned grid = unsigned((s.rows + kStepRows - 1) / kStepRows);
     if (grid == 0) return 0;
@@ -172,17 +210,17 @@ int stage_step(bool fp64, const StageShape& s, const double* hypers, const void*
         k_step<double, 1><<<grid, 256, 0, st>>>(s, hypers, (const double*)lo, (const double*)hi,
                                                 (double*)x, (double*)v, (const double*)pb,
                                                 (const double*)gbx, (const double*)tbx, seed,
-                                                first_draw, k, total, gate);
+                                                first_draw, k, total, gate, words, wbase);
     else if (s.D % 4 == 0)
         k_step<float, 4><<<grid, 256, 0, st>>>(s, hypers, (const float*)lo, (const float*)hi,
                                                (float*)x, (float*)v, (const float*)pb,
                                                (const float*)gbx, (const float*)tbx, seed,
-                                               first_draw, k, total, gate);
+                                               first_draw, k, total, gate, words, wbase);
     else
         k_step<float, 1><<<grid, 256, 0, st>>>(s, hypers, (const float*)lo, (const float*)hi,
                                                (float*)x, (float*)v, (const float*)pb,
                                                (const float*)gbx, (const float*)tbx, seed,
-                                               first_draw, k, total, gate);
+                                               first_draw, k, total, gate, words, wbase);
     return int(cudaGetLastError());
 }
 

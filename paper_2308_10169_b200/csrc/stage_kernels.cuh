@@ -33,14 +33,28 @@ struct IterState {
     int pad[2];
 };
 
+// words != nullptr: draw i is words[i - wbase] (a pre-generated mt19937_64
+// window, stage_mt_fill); otherwise the Philox word of index i.
 int stage_init(bool fp64, const StageShape& s, const double* hypers, const void* lo,
                const void* hi, uint64_t seed, uint64_t first_draw, const double* prev, int warm,
-               double pi_radius, void* x, void* v, void* pbest_x, void* stream);
+               double pi_radius, void* x, void* v, void* pbest_x, void* stream,
+               const unsigned long long* words = nullptr, long long wbase = 0);
 
 int stage_step(bool fp64, const StageShape& s, const double* hypers, const void* lo,
                const void* hi, void* x, void* v, const void* pbest_x, const void* gbest_x,
                const void* tbest_x, uint64_t seed, uint64_t first_draw, int k, int total,
-               const IterState* gate, void* stream);
+               const IterState* gate, void* stream, const unsigned long long* words = nullptr,
+               long long wbase = 0);
+
+// Persisted mt19937_64 generator for the staged path (device memory).
+struct MtPersist {
+    unsigned long long st[312];
+    long long blocks;
+};
+// Generate words [from, upto) of the stream into out[w - from] (one CTA);
+// earlier words are skipped.  reseed restarts the generator from `seed`.
+int stage_mt_fill(MtPersist* g, unsigned long long seed, bool reseed, long long from,
+                  long long upto, unsigned long long* out, void* stream);
 
 int stage_eval_path(bool fp64, const unsigned char* world, int max_obs, int max_verts,
                     int off_offsets, int off_verts, int D, int rows, const void* x,

@@ -5,6 +5,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include "mt19937.cuh"
 #include "swarm_device.cuh"
 
 namespace cg = cooperative_groups;
@@ -100,16 +101,14 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
 
     // ------------------------------------------------------- initialisation
     // swarm.hpp:94-132 / planner.hpp:77-133: x draws [0, R*D), v draws [R*D, 2*R*D)
+    MtState mt{(unsigned long long*)S8(L.mt), 0, 0};
     {
         const bool warm_on = p.has_prev != nullptr && p.has_prev[swarm] != 0;
         const double* prev = warm_on ? p.prev + size_t(swarm) * D : nullptr;
         const T rad = T(p.pi_radius);
-        ElemWalk w(c.fD, tid, nthr, D);
-        for (int e = tid; e < c.P * D; e += nthr, w.next()) {
-            const int pl = w.pl, d = w.col;
+        // one position / velocity draw for element e = (pl, d) of this CTA
+        auto put_x = [&](int pl, int d, T ux) {
             const int row = c.row0 + pl, g = int(c.fN.div(uint32_t(row))), n = row - g * N;
-            const uint64_t ix = uint64_t(row) * uint64_t(D) + uint64_t(d);
-            const T ux = unit_from_word<T>(philox_word(seed, ix));
             const T lo = c.lo[d], hi = c.hi[d];
             T xv;
             if (warm_on && n < p.warm) {
@@ -120,12 +119,34 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
             } else {
                 xv = A::add(lo, A::mul(ux, A::sub(hi, lo)));
             }
-            const T uv = unit_from_word<T>(philox_word(seed, uint64_t(R) * D + ix));
-            const T vmax = A::mul(c.hyp[g * 6 + 5], A::sub(hi, lo));
+            c.x[pl * D + d] = xv;
+            c.pb[pl * D + d] = xv;
+        };
+        auto put_v = [&](int pl, int d, T uv) {
+            const int row = c.row0 + pl, g = int(c.fN.div(uint32_t(row)));
+            const T vmax = A::mul(c.hyp[g * 6 + 5], A::sub(c.hi[d], c.lo[d]));
             const T vlo = -vmax;
-            c.x[e] = xv;
-            c.pb[e] = xv;
-            c.v[e] = A::add(vlo, A::mul(uv, A::sub(vmax, vlo)));
+            c.v[pl * D + d] = A::add(vlo, A::mul(uv, A::sub(vmax, vlo)));
+        };
+        if (p.rng == kMt19937) {
+            // the reference's sequential stream: every word passes through this
+            // CTA, which keeps the ones of its own rows (mt19937.cuh)
+            mt_seed(mt, seed);
+            const long long RD = (long long)R * D, x0 = (long long)c.row0 * D, x1 = (long long)row1 * D;
+            mt_deliver(mt, 0, 2 * RD, [&](long long w, unsigned long long word) {
+                const long long wx = w < RD ? w : w - RD;
+                if (wx < x0 || wx >= x1) return;
+                const int e = int(wx - x0), pl = int(c.fD.div(uint32_t(e))), d = e - pl * D;
+                if (w < RD) put_x(pl, d, unit_from_word<T>(word));
+                else put_v(pl, d, unit_from_word<T>(word));
+            });
+        } else {
+            ElemWalk w(c.fD, tid, nthr, D);
+            for (int e = tid; e < c.P * D; e += nthr, w.next()) {
+                const uint64_t ix = uint64_t(c.row0 + w.pl) * uint64_t(D) + uint64_t(w.col);
+                put_x(w.pl, w.col, unit_from_word<T>(philox_word(seed, ix)));
+                put_v(w.pl, w.col, unit_from_word<T>(philox_word(seed, uint64_t(R) * D + ix)));
+            }
         }
     }
     __syncthreads();
@@ -325,7 +346,7 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
                 }
             }
             if (lane == 0) m->k_done = k;
-        } else if (k < p.cap) {
+        } else if (k < p.cap && p.rng == kPhilox) {
             // meanwhile: this step's draws (draw_step_randoms, swarm.hpp:59-70) --
             // they depend only on (seed, k, row), not on the bests
             const uint64_t base = 2ull * uint64_t(R) * uint64_t(D) + uint64_t(k - 1) * 3ull * uint64_t(R);
@@ -336,7 +357,7 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
                 c.coef[j * c.P + pl] = A::mul(c.hyp[g * 6 + j], u);   // a_j = c_j * r_j
             }
         }
-        if (nthr == 32 && k < p.cap) {   // single-warp CTA: draws after the bests
+        if (nthr == 32 && k < p.cap && p.rng == kPhilox) {   // single-warp CTA: draws after the bests
             const uint64_t base = 2ull * uint64_t(R) * uint64_t(D) + uint64_t(k - 1) * 3ull * uint64_t(R);
             for (int t = tid; t < 3 * c.P; t += 32) {
                 const int j = t >= 2 * c.P ? 2 : (t >= c.P ? 1 : 0), pl = t - j * c.P;
@@ -357,6 +378,19 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
                 for (int d = tid; d < D; d += nthr) c.tbx[d] = pxb[tslot * D + d];
             __syncthreads();
             break;
+        }
+        if (p.rng == kMt19937) {
+            // draw_step_randoms (swarm.hpp:59-70) from the reference stream:
+            // r1 block, r2 block, r3 block of R words each
+            const long long base = 2ll * R * D + (long long)(k - 1) * 3 * R;
+            mt_deliver(mt, base, base + 3ll * R, [&](long long w, unsigned long long word) {
+                const long long o = w - base;
+                const int j = o >= 2ll * R ? 2 : (o >= R ? 1 : 0);
+                const int row = int(o - (long long)j * R);
+                if (row < c.row0 || row >= row1) return;
+                const int g = int(c.fN.div(uint32_t(row)));
+                c.coef[j * c.P + (row - c.row0)] = A::mul(c.hyp[g * 6 + j], unit_from_word<T>(word));
+            });
         }
         // --------------------------------------------------- step k (swarm.hpp:138-174)
         // Improved group bests / the new tbest are read straight from the pushed

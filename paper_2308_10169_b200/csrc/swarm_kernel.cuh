@@ -18,6 +18,8 @@
 
 namespace sepso {
 
+enum RngKind : int { kPhilox = 0, kMt19937 = 1 };
+
 enum ProblemKind : int {
     kPath = 0, kSphere = 1, kRosenbrock = 2, kRastrigin = 3, kGriewank = 4, kAckley = 5
 };
@@ -67,6 +69,7 @@ struct SwarmParams {
     double alpha, beta, delta, pi_radius;
     int beta_int;            // >= 1: beta is this small integer (exact repeated product)
     double at_gap;           // delta * sqrt(2 tw) * (1 + 1e-9): exact AT pre-test bound
+    int rng;                 // 0: Philox counter stream, 1: mt19937_64 (the reference's stream)
     // inputs
     const double* hypers;  long long hypers_stride;   // doubles between swarms (0 = shared)
     const unsigned long long* seeds;
@@ -95,7 +98,7 @@ struct Part {
 
 struct SmemLayout {
     size_t x, v, pb, pbf, pbq, q, fit, imp, seglen, coef, lo, hi, hyp, gbx, gbf, gbq, chg, tbx,
-        win, part, px, allpart, allbad, gtab, ctab, obb, ooff, ofl, vert, edge, list, misc, total;
+        win, part, px, allpart, allbad, gtab, ctab, obb, ooff, ofl, vert, edge, list, mt, misc, total;
 };
 
 #ifdef __CUDACC__
@@ -146,6 +149,7 @@ SEPSO_LHD SmemLayout smem_layout(const SwarmParams& p, size_t tsz, bool path) {
     L.vert = take(V * 2 * tsz);
     L.edge = take(V * 4 * tsz);
     L.list = take(path ? size_t(p.entry_cap) * 4 : 0);
+    L.mt = take(p.rng == 1 ? 2 * 312 * 8 : 0);
     L.total = o;
     return L;
 }

@@ -38,8 +38,10 @@ ABI_SYMBOLS = [
     "sf_generate_world", "sf_step_world", "sf_run_scenario", "sf_scene_batch_create",
     "sf_scene_batch_run", "sf_scene_batch_records", "sf_scene_batch_destroy",
     "sf_ctx_last_io_bytes", "sf_measure_fp32_peak", "sf_ctx_set_l2_flush",
-    "sf_comm_unique_id", "sf_ctx_init_comm", "sf_plan_frame_sharded",
+    "sf_comm_unique_id", "sf_ctx_init_comm", "sf_plan_frame_sharded", "sf_ctx_set_rng",
+    "sf_ctx_rng",
 ]
+RNGS = {"philox": 0, "mt19937": 1}
 
 
 class NonFiniteFitnessError(RuntimeError):
@@ -128,6 +130,8 @@ def lib():
         "sf_ctx_stream": (C.c_void_p, [C.c_void_p]),
         "sf_ctx_synchronize": (C.c_int, [C.c_void_p]),
         "sf_ctx_set_launch": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
+        "sf_ctx_set_rng": (C.c_int, [C.c_void_p, C.c_int]),
+        "sf_ctx_rng": (C.c_int, [C.c_void_p]),
         "sf_ctx_enable_timing": (C.c_int, [C.c_void_p, C.c_int]),
         "sf_ctx_kernel_time": (C.c_int, [C.c_void_p, _dp, _u64p]),
         "sf_plan_frame": (C.c_int, [C.c_void_p, W, _dp, _dp, P, C.c_uint64, _dp, _u32p,
@@ -155,7 +159,7 @@ def lib():
                                         C.c_double, _dp, _u32p]),
         "sf_eval_bench_rows": (C.c_int, [C.c_void_p, C.c_int, _dp, C.c_uint32, C.c_uint32, _dp]),
         "sf_should_truncate": (C.c_int, [_dp, C.c_uint32, C.c_int, P, C.POINTER(C.c_int)]),
-        "sf_generate_world": (C.c_int, [C.POINTER(_ScenarioCfg), C.c_uint64, W, _u32p,
+        "sf_generate_world": (C.c_int, [C.POINTER(_ScenarioCfg), C.c_uint64, C.c_int, W, _u32p,
                                         C.POINTER(_Point), C.POINTER(_Point)]),
         "sf_step_world": (C.c_int, [W, C.POINTER(_Point), C.POINTER(_Point), C.c_double]),
         "sf_run_scenario": (C.c_int, [C.c_void_p, C.POINTER(_ScenarioCfg), C.c_int, C.c_uint32,
@@ -345,15 +349,15 @@ def encode_path(waypoints) -> np.ndarray:
     return np.concatenate([w[:, 0], w[:, 1]])
 
 
-def generate_world(config: ScenarioConfig, seed: int) -> PolygonWorld:
-    """simenv.hpp:83-132 (engine stream)."""
+def generate_world(config: ScenarioConfig, seed: int, rng: str = "mt19937") -> PolygonWorld:
+    """simenv.hpp:83-132 on the host, drawing the given stream."""
     n = config.dynamic_obstacles + config.static_obstacles
     off = np.zeros(n + 1, dtype=np.uint32)
     verts = np.zeros((4 * n, 2))
     vel = np.zeros((max(n, 1), 2))
     w = _World()
     P = C.POINTER(_Point)
-    _check(lib().sf_generate_world(C.byref(config._c()), seed, C.byref(w), _p(off, _u32p),
+    _check(lib().sf_generate_world(C.byref(config._c()), seed, RNGS[rng], C.byref(w), _p(off, _u32p),
                                    verts.ctypes.data_as(P), vel.ctypes.data_as(P)))
     out = PolygonWorld(w.width, w.height, (w.start.x, w.start.y), (w.target.x, w.target.y),
                        [verts[4 * i:4 * i + 4] for i in range(n)],
@@ -386,12 +390,14 @@ def should_truncate(window, best_is_collision_free: bool, config: PlannerConfig)
 class Engine:
     """One device context (stream + device arena); fp32 = production, fp64 = parity."""
 
-    def __init__(self, device: int = 0, precision: str = "fp32"):
+    def __init__(self, device: int = 0, precision: str = "fp32", rng: str = "mt19937"):
         self._L = lib()
         self.precision = FP64 if precision == "fp64" else FP32
         h = C.c_void_p()
         _check(self._L.sf_ctx_create(device, self.precision, C.byref(h)))
         self._h = h
+        self.rng = rng
+        _check(self._L.sf_ctx_set_rng(self._h, RNGS[rng]))
 
     def close(self):
         if getattr(self, "_h", None):

@@ -13,17 +13,36 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: longer-running parity sweep")
 
 
+def _engine(precision, rng):
+    from paper_2308_10169_b200 import Engine
+    return Engine(0, precision, rng)
+
+
+# Philox-stream engines: compared with the oracle / the shared-RNG harness build
 @pytest.fixture(scope="session")
 def eng32():
-    from paper_2308_10169_b200 import Engine
-    e = Engine(0, "fp32")
+    e = _engine("fp32", "philox")
     yield e
     e.close()
 
 
 @pytest.fixture(scope="session")
 def eng64():
-    from paper_2308_10169_b200 import Engine
-    e = Engine(0, "fp64")
+    e = _engine("fp64", "philox")
+    yield e
+    e.close()
+
+
+# the reference's own mt19937_64 stream: compared with the UNMODIFIED reference
+@pytest.fixture(scope="session")
+def eng32mt():
+    e = _engine("fp32", "mt19937")
+    yield e
+    e.close()
+
+
+@pytest.fixture(scope="session")
+def eng64mt():
+    e = _engine("fp64", "mt19937")
     yield e
     e.close()

@@ -99,13 +99,14 @@ def test_should_truncate_host_predicate():
     assert pe.should_truncate([1000.0, 5.0, 5.0, 5.0], True, c)
 
 
-def test_generate_and_step_world_match_oracle():
-    """simenv.hpp:83-184 on the host (engine stream) == oracle, 50 steps."""
+@pytest.mark.parametrize("rng,rk", [("mt19937", 0), ("philox", 1)])
+def test_generate_and_step_world_match_oracle(rng, rk):
+    """simenv.hpp:83-184 on the host, both streams == oracle, 50 steps."""
     o = oracle()
     for root in range(4):
         seed = o.or_derive_seed(root, b"world")
-        w = pe.generate_world(pe.ScenarioConfig(), seed)
-        wo = generate_world("oracle", seed, RNG_PHILOX)
+        w = pe.generate_world(pe.ScenarioConfig(), seed, rng)
+        wo = generate_world("oracle", seed, rk)
         assert np.array_equal(w.vertices.reshape(-1), wo.verts)
         for _ in range(50):
             w = pe.step_world(w, 1.0)

@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import paper_2308_10169_b200 as pe
-from oracle_lib import (EVOLVED_PATH_HYPERS, RNG_PHILOX, generate_world, oracle, oracle_plan_frame,
+from oracle_lib import (EVOLVED_PATH_HYPERS, RNG_MT, RNG_PHILOX, generate_world, oracle, oracle_plan_frame,
                         planner_cfg, ptr, u32p)
 
 pytestmark = pytest.mark.gpu
@@ -33,32 +33,32 @@ def parse_frames(text):
     return rows
 
 
-def test_plan_route_matches_python_engine(eng32):
+def test_plan_route_matches_python_engine(eng32mt):
     rows = parse_frames(run("plan_route", 12, 3))
-    recs = eng32.run_scenario(pe.ScenarioConfig(root_seed=3), "sepso", 12,
+    recs = eng32mt.run_scenario(pe.ScenarioConfig(root_seed=3), "sepso", 12,
                               pe.PlannerConfig(max_iters_per_frame=30, window_carryover=True))
     assert [(r.iterations, int(r.truncated), r.intersections, r.fitness, r.length) for r in recs] == rows
 
 
 def test_plan_route_fp64_equals_reference_harness():
-    """FP64 drop-in == the reference's plan_frame under the shared Philox stream."""
+    """FP64 drop-in (default mt19937 stream) == the UNMODIFIED reference's frames."""
     rows = parse_frames(run("plan_route", 8, 3, precision="fp64"))
     o = oracle()
-    w = generate_world("oracle", o.or_derive_seed(3, b"world"), RNG_PHILOX)
+    w = generate_world("oracle", o.or_derive_seed(3, b"world"), RNG_MT)
     cfg = planner_cfg(max_iters=30, window_carryover=1)
     prev, win = None, []
     for f, (it, tr, q, fit, length) in enumerate(rows):
         st, rec, best, win, _ = oracle_plan_frame(w, prev, EVOLVED_PATH_HYPERS, cfg,
-                                                  o.or_derive_seed_idx(3, b"plan", f), RNG_PHILOX, win)
+                                                  o.or_derive_seed_idx(3, b"plan", f), RNG_MT, win)
         assert (rec.iterations, rec.truncated, rec.intersections) == (it, tr, q)
         assert rec.fitness == fit and rec.length == length
         prev = best
         o.or_step_world(ptr(w.head), w.n, ptr(w.offsets, u32p), ptr(w.verts), ptr(w.vel), 1.0)
 
 
-def test_minimize_rastrigin_matches_python_engine(eng32):
+def test_minimize_rastrigin_matches_python_engine(eng32mt):
     text = run("minimize_rastrigin")
     final = float(text.splitlines()[0].split()[3])
-    r = eng32.run_dtpso("BF3", pe.DEFAULT_GROUP_HYPERS, 8, 10, 1400, 42, dim=30)
+    r = eng32mt.run_dtpso("BF3", pe.DEFAULT_GROUP_HYPERS, 8, 10, 1400, 42, dim=30)
     assert final == r["final_fitness"]
     assert "evolve best" in text
