@@ -50,3 +50,76 @@ extern "C" int sf_measure_fp32_peak(sf_ctx* ctx, double* tflops) {
     *tflops = 2.0 * 8.0 * double(iters) * blocks * 256.0 / (double(ms) * 1e-3) / 1e12;
     return SF_OK;
 }
+
+#include "mt19937.cuh"
+
+namespace sepso {
+// mt19937_64 generator throughput probe: cycles per 312-word block.
+__global__ void __launch_bounds__(1024) k_mt_probe(long long blocks, int mode, unsigned long long* out,
+                                                  long long* cycles) {
+    __shared__ unsigned long long buf[kMtStateWords];
+    __shared__ float sinkbuf[1024];
+    MtState s{buf, 0, 0};
+    const MtGroup g{int(threadIdx.x), int(blockDim.x), 0};
+    const long long t0 = clock64();
+    mt_seed(s, g, 12345ull);
+    unsigned long long acc = 0;
+    if (mode == 0)
+        mt_generate(s, g, 0, 312 * blocks, [&](int w, unsigned long long word) { acc ^= word; });
+    else if (mode == 1)
+        mt_generate(s, g, 0, 312 * blocks, [&](int w, unsigned long long word) {
+            if ((w & 15) == 0) sinkbuf[threadIdx.x] = unit_from_word<float>(word);
+        });
+    else if (mode == 2) {          // barrier + one LDS/STS round trip per "block"
+        for (long long b = 0; b < blocks; ++b) {
+            const int i = threadIdx.x % 312;
+            buf[((b + 1) & 1) * 312 + i] = buf[(b & 1) * 312 + ((i + 1) % 312)] + 1;
+            __syncthreads();
+        }
+        acc = buf[threadIdx.x % 312];
+    } else if (mode == 4 || mode == 5) {   // fused-kernel step shape: warps 1..6, 3 windows of 85 rows per 4080 words
+        __syncthreads();
+        const int tid = threadIdx.x;
+        if (tid >= 32 && tid < 224) {
+            const MtGroup gg{tid - 32, 192, 1};
+            MtState st{buf, s.cur, s.blocks};
+            const long long steps = blocks * 312 / 4080;
+            for (long long k = 0; k < steps; ++k) {
+                const long long base = 4080 * k;
+                if (mode == 4) {
+                    for (int j = 0; j < 3; ++j)
+                        mt_generate(st, gg, base + j * 1360 + 85, base + j * 1360 + 170,
+                                    [&](int pl, unsigned long long word) { sinkbuf[j * 85 + pl] = unit_from_word<float>(word); });
+                } else {
+                    mt_generate(st, gg, base, base + 4080, [&](int pl, unsigned long long word) {
+                        if (pl < 85) sinkbuf[pl] = unit_from_word<float>(word); });
+                }
+            }
+        }
+        __syncthreads();
+    } else if (mode == 3) {        // barrier only
+        for (long long b = 0; b < blocks; ++b) __syncthreads();
+    }
+    if (acc == 42) out[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) *cycles = clock64() - t0;
+}
+} // namespace sepso
+
+extern "C" int sf_debug_mt_probe(sf_ctx* ctx, long long blocks, int threads, int mode, double* cycles_per_block) {
+    using namespace sepso;
+    cudaSetDevice(ctx->device);
+    unsigned long long* out;
+    long long* cyc;
+    cudaMalloc(&out, 1024 * 8);
+    cudaMalloc(&cyc, 8);
+    k_mt_probe<<<1, threads, 0, ctx->stream>>>(blocks, mode, out, cyc);
+    long long h = 0;
+    cudaMemcpyAsync(&h, cyc, 8, cudaMemcpyDeviceToHost, ctx->stream);
+    const cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(out);
+    cudaFree(cyc);
+    if (e != cudaSuccess) return cuda_fail(e, "mt probe");
+    *cycles_per_block = double(h) / double(blocks);
+    return SF_OK;
+}

@@ -227,7 +227,6 @@ FusedPlan plan_fused(sf_ctx* ctx, int problem, int n_swarms, int G, int N, int D
         }
         if (want_t > 0) p.nthreads = std::min(1024, std::max(32, want_t / 32 * 32));
         p.rng = ctx->rng;
-        if (p.rng == SF_RNG_MT19937) p.nthreads = std::max(p.nthreads, 320);   // one 312-word block per pass
         fp.smem = smem_layout(p, fp64 ? 8 : 4, path).total;
         if (int(fp.smem) <= smem_max) { fp.fits = true; break; }
         if (C >= 16 || want_c > 0) break;
@@ -266,6 +265,15 @@ int launch_fused(sf_ctx* ctx, FusedPlan& fp, int problem) {
         }
         std::fprintf(stderr, "[phase] C=%d T=%d iters=%d cycles/iter:", fp.p.C, fp.p.nthreads, iters);
         for (int i = 0; i < 11; ++i) std::fprintf(stderr, " %s=%.0f", names[i], iters ? acc[i] / iters : 0.0);
+        double g0 = 0, g1 = 0, b1 = 0;
+        int gi = 0;
+        for (int k = 0; k < iters; ++k) {
+            const long long* r = h.data() + size_t(k) * kProfPhases;
+            if (r[12] == 0 || r[13] == 0) continue;
+            ++gi;
+            g0 += double(r[12] - r[8]); g1 += double(r[13] - r[12]); b1 += double(r[14] - r[8]);
+        }
+        if (gi) std::fprintf(stderr, " | B1work=%.0f gen_start=%.0f gen=%.0f", b1 / gi, g0 / gi, g1 / gi);
         std::fprintf(stderr, "\n");
     }
     if (e != 0) return cuda_fail(cudaError_t(e), "fused swarm launch");

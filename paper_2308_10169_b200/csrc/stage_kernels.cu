@@ -38,20 +38,21 @@ __device__ __forceinline__ uint64_t stream_word(uint64_t seed, uint64_t i, const
 __global__ void __launch_bounds__(320) k_mt_fill(MtPersist* g, unsigned long long seed, int reseed,
                                                  long long from, long long upto,
                                                  unsigned long long* out) {
-    __shared__ unsigned long long buf[2 * 312];
+    __shared__ unsigned long long buf[kMtStateWords];
     MtState s{buf, 0, 0};
+    const MtGroup grp{int(threadIdx.x), int(blockDim.x), 0};
     if (reseed) {
-        mt_seed(s, seed);
+        mt_seed(s, grp, seed);
     } else {
-        for (int i = threadIdx.x; i < 312; i += blockDim.x) buf[i] = g->st[i];
+        for (int i = threadIdx.x; i < 624; i += blockDim.x) buf[i] = g->st[i];   // pair 0
         s.blocks = g->blocks;
         __syncthreads();
     }
-    const long long base = from;
-    mt_deliver(s, from < 0 ? 0 : from, upto, [&](long long w, unsigned long long word) {
-        if (out) out[w - base] = word;
+    const long long f0 = from < 0 ? 0 : from;
+    mt_generate(s, grp, f0, upto, [&](int rel, unsigned long long word) {
+        if (out) out[(f0 - from) + rel] = word;
     });
-    for (int i = threadIdx.x; i < 312; i += blockDim.x) g->st[i] = buf[s.cur * 312 + i];
+    for (int i = threadIdx.x; i < 624; i += blockDim.x) g->st[i] = buf[s.cur * 624 + i];
     if (threadIdx.x == 0) g->blocks = s.blocks;
 }
 

@@ -48,7 +48,7 @@ int stage_step(bool fp64, const StageShape& s, const double* hypers, const void*
 
 // Persisted mt19937_64 generator for the staged path (device memory).
 struct MtPersist {
-    unsigned long long st[312];
+    unsigned long long st[624];     // the two latest blocks (mt19937.cuh MtState pair)
     long long blocks;
 };
 // Generate words [from, upto) of the stream into out[w - from] (one CTA);

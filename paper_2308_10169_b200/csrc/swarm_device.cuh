@@ -37,6 +37,8 @@ template <class T> struct Misc {
     T tbf;
     int tbq, tsrc_slot, stop, truncated, status, bad_row, bad_min, n_pair, n_cont;
     int win_len, win_head, k_done, cont_cap;
+    int mt_cur;                 // mt19937_64 generator bookkeeping (MtState outside generation)
+    long long mt_blocks;
 };
 
 // alpha * q^beta (geometry.hpp:240): exact repeated product for small integer

@@ -13,6 +13,25 @@ namespace cg = cooperative_groups;
 namespace sepso {
 
 // ------------------------------------------------------------------ kernel
+// r1, r2, r3 of step k (draw_step_randoms, swarm.hpp:59-70): R words each at
+// 2RD + (k-1)*3R of the mt19937_64 stream; rows [row0, row1) keep a_j = c_j * r_j.
+template <class T>
+__device__ void mt_step_draws(Ctx<T>& c, unsigned long long* mtbuf, const MtGroup& grp, int k, int row1) {
+    using A = Ar<T>;
+    const int R = c.R;
+    const long long base = 2ll * R * c.D + (long long)(k - 1) * 3 * R;
+    MtState mt{mtbuf, c.m->mt_cur, c.m->mt_blocks};      // registers only while generating
+    // one window per factor: only this CTA's rows are tempered and kept
+    for (int j = 0; j < 3; ++j)
+        mt_generate(mt, grp, base + (long long)j * R + c.row0, base + (long long)j * R + row1,
+                    [&](int pl, unsigned long long word) {
+                        const int g = int(c.fN.div(uint32_t(c.row0 + pl)));
+                        c.coef[j * c.P + pl] = A::mul(c.hyp[g * 6 + j], unit_from_word<T>(word));
+                    });
+    // every group thread has read the bookkeeping before the first barrier
+    if (grp.lt == 0) { c.m->mt_cur = mt.cur; c.m->mt_blocks = mt.blocks; }
+}
+
 // Element loops walk (particle, column) pairs with an incremental carry instead
 // of integer division: thread t starts at element t and advances by nthr.
 struct ElemWalk {
@@ -101,7 +120,7 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
 
     // ------------------------------------------------------- initialisation
     // swarm.hpp:94-132 / planner.hpp:77-133: x draws [0, R*D), v draws [R*D, 2*R*D)
-    MtState mt{(unsigned long long*)S8(L.mt), 0, 0};
+    unsigned long long* const mtbuf = (unsigned long long*)S8(L.mt);
     {
         const bool warm_on = p.has_prev != nullptr && p.has_prev[swarm] != 0;
         const double* prev = warm_on ? p.prev + size_t(swarm) * D : nullptr;
@@ -129,17 +148,24 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
             c.v[pl * D + d] = A::add(vlo, A::mul(uv, A::sub(vmax, vlo)));
         };
         if (p.rng == kMt19937) {
-            // the reference's sequential stream: every word passes through this
-            // CTA, which keeps the ones of its own rows (mt19937.cuh)
-            mt_seed(mt, seed);
+            // The reference's sequential stream (mt19937.cuh), walked by the
+            // whole CTA through all 2RD init words; only the words of this
+            // CTA's rows are tempered and go straight into x / v.
             const long long RD = (long long)R * D, x0 = (long long)c.row0 * D, x1 = (long long)row1 * D;
-            mt_deliver(mt, 0, 2 * RD, [&](long long w, unsigned long long word) {
-                const long long wx = w < RD ? w : w - RD;
-                if (wx < x0 || wx >= x1) return;
-                const int e = int(wx - x0), pl = int(c.fD.div(uint32_t(e))), d = e - pl * D;
-                if (w < RD) put_x(pl, d, unit_from_word<T>(word));
-                else put_v(pl, d, unit_from_word<T>(word));
+            const MtGroup grp{tid, nthr, 0};
+            MtState mt{mtbuf, 0, 0};
+            mt_seed(mt, grp, seed);
+            mt_generate(mt, grp, x0, x1, [&](int e, unsigned long long word) {
+                const int pl = int(c.fD.div(uint32_t(e)));
+                put_x(pl, e - pl * D, unit_from_word<T>(word));
             });
+            mt_generate(mt, grp, RD + x0, RD + x1, [&](int e, unsigned long long word) {
+                const int pl = int(c.fD.div(uint32_t(e)));
+                put_v(pl, e - pl * D, unit_from_word<T>(word));
+            });
+            // the rest of the init words, so that the step draws start at 2RD
+            mt_generate(mt, grp, 2 * RD, 2 * RD, [&](int, unsigned long long) {});
+            if (tid == 0) { c.m->mt_cur = mt.cur; c.m->mt_blocks = mt.blocks; }
         } else {
             ElemWalk w(c.fD, tid, nthr, D);
             for (int e = tid; e < c.P * D; e += nthr, w.next()) {
@@ -346,6 +372,16 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
                 }
             }
             if (lane == 0) m->k_done = k;
+            SEPSO_MARK(14);
+        } else if (k < p.cap && p.rng == kMt19937) {
+            // meanwhile, warps 1..4 walk the reference stream to this step's
+            // r1, r2, r3 blocks (draw_step_randoms, swarm.hpp:59-70) and keep
+            // this CTA's rows as the step factors a_j = c_j * r_j
+            const int gn = nthr - 32 < 128 ? nthr - 32 : 128;
+            long long* gprof = (p.prof != nullptr && swarm == 0 && c.crank == 0 && tid == 32) ? p.prof : nullptr;
+            if (gprof) gprof[(k - 1) * kProfPhases + 12] = clock64();
+            if (tid - 32 < gn) mt_step_draws(c, mtbuf, MtGroup{tid - 32, gn, 1}, k, row1);
+            if (gprof) gprof[(k - 1) * kProfPhases + 13] = clock64();
         } else if (k < p.cap && p.rng == kPhilox) {
             // meanwhile: this step's draws (draw_step_randoms, swarm.hpp:59-70) --
             // they depend only on (seed, k, row), not on the bests
@@ -357,7 +393,9 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
                 c.coef[j * c.P + pl] = A::mul(c.hyp[g * 6 + j], u);   // a_j = c_j * r_j
             }
         }
-        if (nthr == 32 && k < p.cap && p.rng == kPhilox) {   // single-warp CTA: draws after the bests
+        if (nthr == 32 && k < p.cap && p.rng == kMt19937)     // single-warp CTA: draws after the bests
+            mt_step_draws(c, mtbuf, MtGroup{tid, 32, 0}, k, row1);
+        if (nthr == 32 && k < p.cap && p.rng == kPhilox) {
             const uint64_t base = 2ull * uint64_t(R) * uint64_t(D) + uint64_t(k - 1) * 3ull * uint64_t(R);
             for (int t = tid; t < 3 * c.P; t += 32) {
                 const int j = t >= 2 * c.P ? 2 : (t >= c.P ? 1 : 0), pl = t - j * c.P;
@@ -378,19 +416,6 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
                 for (int d = tid; d < D; d += nthr) c.tbx[d] = pxb[tslot * D + d];
             __syncthreads();
             break;
-        }
-        if (p.rng == kMt19937) {
-            // draw_step_randoms (swarm.hpp:59-70) from the reference stream:
-            // r1 block, r2 block, r3 block of R words each
-            const long long base = 2ll * R * D + (long long)(k - 1) * 3 * R;
-            mt_deliver(mt, base, base + 3ll * R, [&](long long w, unsigned long long word) {
-                const long long o = w - base;
-                const int j = o >= 2ll * R ? 2 : (o >= R ? 1 : 0);
-                const int row = int(o - (long long)j * R);
-                if (row < c.row0 || row >= row1) return;
-                const int g = int(c.fN.div(uint32_t(row)));
-                c.coef[j * c.P + (row - c.row0)] = A::mul(c.hyp[g * 6 + j], unit_from_word<T>(word));
-            });
         }
         // --------------------------------------------------- step k (swarm.hpp:138-174)
         // Improved group bests / the new tbest are read straight from the pushed

@@ -87,7 +87,7 @@ struct SwarmParams {
     // debug: per-iteration phase timestamps of swarm 0 / CTA 0 (SEPSO_PHASE_PROF)
     long long* prof;
 };
-constexpr int kProfPhases = 12;
+constexpr int kProfPhases = 15;   // 0..11 phase marks, 12/13 generator start/end, 14 B1 end
 
 // One CTA's best (pbest_f, row) of one group, read by its peers over DSMEM in
 // a single 16-byte load.
@@ -149,7 +149,7 @@ SEPSO_LHD SmemLayout smem_layout(const SwarmParams& p, size_t tsz, bool path) {
     L.vert = take(V * 2 * tsz);
     L.edge = take(V * 4 * tsz);
     L.list = take(path ? size_t(p.entry_cap) * 4 : 0);
-    L.mt = take(p.rng == 1 ? 2 * 312 * 8 : 0);
+    L.mt = take(p.rng == 1 ? 4 * 312 * 8 : 0);
     L.total = o;
     return L;
 }

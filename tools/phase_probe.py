@@ -6,7 +6,7 @@ sys.path.insert(0, ROOT)
 import paper_2308_10169_b200 as pe
 eng = pe.Engine(0, sys.argv[1] if len(sys.argv) > 1 else "fp32")
 planner = pe.PlannerConfig(max_iters_per_frame=30, window_carryover=True)
-for C, T in ((8, 1024), (16, 512), (16, 1024)):
+for C, T in ((16, 1024), (8, 1024)):
     eng.set_launch(C, T)
     sb = pe.SceneBatch(eng, [pe.ScenarioConfig(root_seed=3)], planner, pe.EVOLVED_PATH_HYPERS, 6)
     sb.run(6)
