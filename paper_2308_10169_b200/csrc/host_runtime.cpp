@@ -241,13 +241,13 @@ int launch_fused(sf_ctx* ctx, FusedPlan& fp, int problem) {
     static const bool phase_prof = std::getenv("SEPSO_PHASE_PROF") != nullptr;
     long long* prof = nullptr;
     if (phase_prof && fp.p.cap > 0) {
-        cudaMalloc(&prof, sizeof(long long) * kProfPhases * fp.p.cap);
-        cudaMemsetAsync(prof, 0, sizeof(long long) * kProfPhases * fp.p.cap, ctx->stream);
+        cudaMalloc(&prof, sizeof(long long) * kProfPhases * (fp.p.cap + 1));
+        cudaMemsetAsync(prof, 0, sizeof(long long) * kProfPhases * (fp.p.cap + 1), ctx->stream);
         fp.p.prof = prof;
     }
     const int e = launch_swarms(fp.p, problem, ctx->precision == SF_FP64, ctx->stream, &smem);
     if (prof) {
-        std::vector<long long> h(size_t(kProfPhases) * fp.p.cap);
+        std::vector<long long> h(size_t(kProfPhases) * (fp.p.cap + 1));
         cudaMemcpyAsync(h.data(), prof, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream);
         cudaStreamSynchronize(ctx->stream);
         cudaFree(prof);
@@ -274,6 +274,11 @@ int launch_fused(sf_ctx* ctx, FusedPlan& fp, int problem) {
             g0 += double(r[12] - r[8]); g1 += double(r[13] - r[12]); b1 += double(r[14] - r[8]);
         }
         if (gi) std::fprintf(stderr, " | B1work=%.0f gen_start=%.0f gen=%.0f", b1 / gi, g0 / gi, g1 / gi);
+        {   // init marks (row cap): start, consts, seeded, x, v, rest, put, loop
+            const long long* r = h.data() + size_t(fp.p.cap) * kProfPhases;
+            std::fprintf(stderr, " | init: consts=%lld seed=%lld x=%lld v=%lld rest=%lld sync=%lld",
+                         r[1] - r[0], r[2] - r[1], r[3] - r[2], r[4] - r[3], r[5] - r[4], r[6] - r[5]);
+        }
         std::fprintf(stderr, "\n");
     }
     if (e != 0) return cuda_fail(cudaError_t(e), "fused swarm launch");

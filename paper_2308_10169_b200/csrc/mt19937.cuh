@@ -51,17 +51,19 @@ __device__ __forceinline__ void mt_sync(const MtGroup& g) {
     else asm volatile("bar.sync %0, %1;" ::"r"(g.bar), "r"(g.n) : "memory");
 }
 
-// std::mt19937_64(seed): the standard's seeding recurrence (sequential, one thread).
-__device__ inline void mt_seed(MtState& s, const MtGroup& g, unsigned long long seed) {
-    if (g.lt == 0) {
-        unsigned long long* st = s.buf + 312;                  // pair 0, slot 1
-        unsigned long long x = seed;
-        st[0] = x;
-        for (int i = 1; i < 312; ++i) {
-            x = 6364136223846793005ull * (x ^ (x >> 62)) + (unsigned long long)i;
-            st[i] = x;
-        }
+// std::mt19937_64(seed): the standard's seeding recurrence, sequential, by one
+// thread into st[0..311] (slot 1 of pair 0 of an MtState buffer).
+__device__ inline void mt_seed_words(unsigned long long* st, unsigned long long seed) {
+    unsigned long long x = seed;
+    st[0] = x;
+    for (int i = 1; i < 312; ++i) {
+        x = 6364136223846793005ull * (x ^ (x >> 62)) + (unsigned long long)i;
+        st[i] = x;
     }
+}
+
+__device__ inline void mt_seed(MtState& s, const MtGroup& g, unsigned long long seed) {
+    if (g.lt == 0) mt_seed_words(s.buf + 312, seed);
     s.cur = 0;
     s.blocks = 0;
     mt_sync(g);

@@ -389,9 +389,19 @@ __device__ __forceinline__ uint32_t order_key(float f) {
 // short-edge flag; sets endpoints, the cull margin and the path search box
 // (geometry.hpp:252-255).
 template <class T>
-__device__ void load_world(Ctx<T>& c, const unsigned char* wrec, int off_offsets, int off_verts) {
+__device__ void world_regs(Ctx<T>& c, const unsigned char* wrec) {
+    const WorldHeader* wh = reinterpret_cast<const WorldHeader*>(wrec);
+    c.O = int(wh->n_obs);
+    c.sx = T(wh->sx); c.sy = T(wh->sy); c.tx = T(wh->tx); c.ty = T(wh->ty);
+    const T width = T(wh->width), height = T(wh->height);
+    c.margin = sizeof(T) == 8 ? T(1e-9) : T(1e-6) * (T(1) + (width > height ? width : height));
+}
+
+// threads [0, nthr) fill the world tables; bar = named barrier id (0: __syncthreads)
+template <class T>
+__device__ void load_world(Ctx<T>& c, const unsigned char* wrec, int off_offsets, int off_verts,
+                           int tid = threadIdx.x, int nthr = blockDim.x, int bar = 0) {
     using A = Ar<T>;
-    const int tid = threadIdx.x, nthr = blockDim.x;
     const WorldHeader* wh = reinterpret_cast<const WorldHeader*>(wrec);
     const uint32_t* woff = reinterpret_cast<const uint32_t*>(wrec + off_offsets);
     const double* wv = reinterpret_cast<const double*>(wrec + off_verts);
@@ -408,7 +418,8 @@ __device__ void load_world(Ctx<T>& c, const unsigned char* wrec, int off_offsets
     }
     for (int i = tid; i <= c.O; i += nthr) c.ooff[i] = int(woff[i]);
     for (int i = tid; i < 2 * nv; i += nthr) c.vert[i] = T(wv[i]);
-    __syncthreads();
+    if (bar == 0) __syncthreads();
+    else asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nthr) : "memory");
     for (int o = tid; o < c.O; o += nthr) {                  // bbox_of, geometry.hpp:167-177
         const int v0 = c.ooff[o], v1 = c.ooff[o + 1];
         T bx0 = c.vert[2 * v0], by0 = c.vert[2 * v0 + 1], bx1 = bx0, by1 = by0;

@@ -13,6 +13,10 @@ namespace cg = cooperative_groups;
 namespace sepso {
 
 // ------------------------------------------------------------------ kernel
+// cluster barrier split into arrive (release) and wait (acquire)
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
+
 // r1, r2, r3 of step k (draw_step_randoms, swarm.hpp:59-70): R words each at
 // 2RD + (k-1)*3R of the mt19937_64 stream; rows [row0, row1) keep a_j = c_j * r_j.
 template <class T>
@@ -87,40 +91,56 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
     const int G = c.G, N = c.N, D = c.D, R = c.R;
     long long* const prof = (p.prof != nullptr && swarm == 0 && c.crank == 0 && tid == 0) ? p.prof : nullptr;
 #define SEPSO_MARK(ph) do { if (prof) prof[(k - 1) * kProfPhases + (ph)] = clock64(); } while (0)
+#define SEPSO_IMARK(ph) do { if (prof) prof[p.cap * kProfPhases + (ph)] = clock64(); } while (0)
+    SEPSO_IMARK(0);
 
     // ---------------------------------------------------------- constants
-    const double* hyp_src = p.hypers + size_t(swarm) * size_t(p.hypers_stride);
-    for (int i = tid; i < G * 6; i += nthr) c.hyp[i] = T(hyp_src[i]);
+    // With the mt19937 stream, the last warp's lane 0 seeds the generator
+    // (a 311-step sequential recurrence) while the other warps stage the
+    // constants; they synchronise on named barrier 2.
+    unsigned long long* const mtbuf = (unsigned long long*)S8(L.mt);
+    const bool mt_on = p.rng == kMt19937;
+    const int cw = (mt_on && nthr >= 64) ? nthr - 32 : nthr;
+    const unsigned char* wrec = PATH ? p.worlds + size_t(swarm) * size_t(p.world_stride) : nullptr;
     c.O = 0;
-    if (PATH) {
-        load_world(c, p.worlds + size_t(swarm) * size_t(p.world_stride), p.off_offsets, p.off_verts);
+    if (tid >= cw) {
+        if (tid == cw) mt_seed_words(mtbuf + 312, seed);
+        if (PATH) world_regs(c, wrec);
     } else {
-        for (int d = tid; d < D; d += nthr) { c.lo[d] = T(p.lo[d]); c.hi[d] = T(p.hi[d]); }
+        const double* hyp_src = p.hypers + size_t(swarm) * size_t(p.hypers_stride);
+        for (int i = tid; i < G * 6; i += cw) c.hyp[i] = T(hyp_src[i]);
+        if (PATH) {
+            world_regs(c, wrec);
+            load_world(c, wrec, p.off_offsets, p.off_verts, tid, cw, cw == nthr ? 0 : 2);
+        } else {
+            for (int d = tid; d < D; d += cw) { c.lo[d] = T(p.lo[d]); c.hi[d] = T(p.hi[d]); }
+        }
+        if (tid == 0) {
+            Misc<T>* m = c.m;
+            m->tbf = A::inf(); m->tbq = 0; m->tsrc_slot = -1; m->stop = 0; m->truncated = 0;
+            m->status = 0; m->bad_row = INT_MAX; m->bad_min = INT_MAX; m->n_pair = 0; m->n_cont = 0;
+            m->k_done = 0;
+            m->cont_cap = 0;
+            const int wl = p.carry ? p.win_len[swarm] : 0;
+            m->win_len = wl < p.tw ? wl : p.tw;
+            m->win_head = 0;
+            if (mt_on && cw == nthr) mt_seed_words(mtbuf + 312, seed);
+        }
+        if (p.carry)
+            for (int i = tid; i < p.tw; i += cw) c.win[i] = p.win_vals[size_t(swarm) * p.tw + i];
+        for (int g = tid; g < G; g += cw) {
+            c.gbf[g] = A::inf(); c.gbq[g] = 0; c.chg[g] = -1;
+            c.gtab[2 * g] = (g * N) / p.rows_per_cta;               // CTAs owning group g
+            c.gtab[2 * g + 1] = ((g + 1) * N - 1) / p.rows_per_cta;
+        }
+        for (int cc = tid; cc < c.C; cc += cw) c.ctab[cc] = (cc * p.rows_per_cta) / N;
+        for (int pl = tid; pl < c.P; pl += cw) { c.pbf[pl] = A::inf(); c.pbq[pl] = 0; c.q[pl] = 0; }
     }
-    if (tid == 0) {
-        Misc<T>* m = c.m;
-        m->tbf = A::inf(); m->tbq = 0; m->tsrc_slot = -1; m->stop = 0; m->truncated = 0;
-        m->status = 0; m->bad_row = INT_MAX; m->bad_min = INT_MAX; m->n_pair = 0; m->n_cont = 0;
-        m->k_done = 0;
-        m->cont_cap = 0;
-        const int wl = p.carry ? p.win_len[swarm] : 0;
-        m->win_len = wl < p.tw ? wl : p.tw;
-        m->win_head = 0;
-    }
-    if (p.carry)
-        for (int i = tid; i < p.tw; i += nthr) c.win[i] = p.win_vals[size_t(swarm) * p.tw + i];
-    for (int g = tid; g < G; g += nthr) {
-        c.gbf[g] = A::inf(); c.gbq[g] = 0; c.chg[g] = -1;
-        c.gtab[2 * g] = (g * N) / p.rows_per_cta;               // CTAs owning group g
-        c.gtab[2 * g + 1] = ((g + 1) * N - 1) / p.rows_per_cta;
-    }
-    for (int cc = tid; cc < c.C; cc += nthr) c.ctab[cc] = (cc * p.rows_per_cta) / N;
-    for (int pl = tid; pl < c.P; pl += nthr) { c.pbf[pl] = A::inf(); c.pbq[pl] = 0; c.q[pl] = 0; }
     __syncthreads();
+    SEPSO_IMARK(1);
 
     // ------------------------------------------------------- initialisation
     // swarm.hpp:94-132 / planner.hpp:77-133: x draws [0, R*D), v draws [R*D, 2*R*D)
-    unsigned long long* const mtbuf = (unsigned long long*)S8(L.mt);
     {
         const bool warm_on = p.has_prev != nullptr && p.has_prev[swarm] != 0;
         const double* prev = warm_on ? p.prev + size_t(swarm) * D : nullptr;
@@ -148,24 +168,30 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
             c.v[pl * D + d] = A::add(vlo, A::mul(uv, A::sub(vmax, vlo)));
         };
         if (p.rng == kMt19937) {
-            // The reference's sequential stream (mt19937.cuh), walked by the
-            // whole CTA through all 2RD init words; only the words of this
-            // CTA's rows are tempered and go straight into x / v.
+            // The reference's sequential stream (mt19937.cuh), walked by warps
+            // 0..3 (one per SM sub-partition; named barrier 3) through all 2RD
+            // init words; only the words of this CTA's rows are tempered and
+            // go straight into x / v.  The seeded state is already in place.
             const long long RD = (long long)R * D, x0 = (long long)c.row0 * D, x1 = (long long)row1 * D;
-            const MtGroup grp{tid, nthr, 0};
+            const MtGroup grp = nthr >= 160 ? MtGroup{tid, 128, 3} : MtGroup{tid, nthr, 0};
             MtState mt{mtbuf, 0, 0};
-            mt_seed(mt, grp, seed);
-            mt_generate(mt, grp, x0, x1, [&](int e, unsigned long long word) {
-                const int pl = int(c.fD.div(uint32_t(e)));
-                put_x(pl, e - pl * D, unit_from_word<T>(word));
-            });
-            mt_generate(mt, grp, RD + x0, RD + x1, [&](int e, unsigned long long word) {
-                const int pl = int(c.fD.div(uint32_t(e)));
-                put_v(pl, e - pl * D, unit_from_word<T>(word));
-            });
-            // the rest of the init words, so that the step draws start at 2RD
-            mt_generate(mt, grp, 2 * RD, 2 * RD, [&](int, unsigned long long) {});
-            if (tid == 0) { c.m->mt_cur = mt.cur; c.m->mt_blocks = mt.blocks; }
+            SEPSO_IMARK(2);
+            if (tid < grp.n) {
+                mt_generate(mt, grp, x0, x1, [&](int e, unsigned long long word) {
+                    const int pl = int(c.fD.div(uint32_t(e)));
+                    put_x(pl, e - pl * D, unit_from_word<T>(word));
+                });
+                SEPSO_IMARK(3);
+                mt_generate(mt, grp, RD + x0, RD + x1, [&](int e, unsigned long long word) {
+                    const int pl = int(c.fD.div(uint32_t(e)));
+                    put_v(pl, e - pl * D, unit_from_word<T>(word));
+                });
+                SEPSO_IMARK(4);
+                // the rest of the init words, so that the step draws start at 2RD
+                mt_generate(mt, grp, 2 * RD, 2 * RD, [&](int, unsigned long long) {});
+                SEPSO_IMARK(5);
+                if (tid == 0) { c.m->mt_cur = mt.cur; c.m->mt_blocks = mt.blocks; }
+            }
         } else {
             ElemWalk w(c.fD, tid, nthr, D);
             for (int e = tid; e < c.P * D; e += nthr, w.next()) {
@@ -176,6 +202,7 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
         }
     }
     __syncthreads();
+    SEPSO_IMARK(6);
 
     // ------------------------------------------------------------ iterations
     int k = 1;
@@ -263,7 +290,21 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
             rb[buf * c.C + c.crank] = c.m->bad_row;
         }
         SEPSO_MARK(6);
-        cluster.sync();   // partials of every CTA visible cluster-wide
+        // Partials of every CTA visible cluster-wide (barrier.cluster arrive +
+        // wait).  With the mt19937 stream the last four warps arrive early and
+        // walk the stream to this step's r1, r2, r3 (draw_step_randoms,
+        // swarm.hpp:59-70) while the cluster synchronises and warp 0 updates
+        // the bests; the factors are read after the barrier that follows B1.
+        const bool gen_early = p.rng == kMt19937 && k < p.cap && nthr >= 192;
+        const int gw0 = (nthr >> 5) - 4;
+        cluster_arrive();
+        if (gen_early && warp >= gw0) {
+            long long* gprof = (p.prof != nullptr && swarm == 0 && c.crank == 0 && tid == gw0 * 32) ? p.prof : nullptr;
+            if (gprof) gprof[(k - 1) * kProfPhases + 12] = clock64();
+            mt_step_draws(c, mtbuf, MtGroup{tid - gw0 * 32, 128, 1}, k, row1);
+            if (gprof) gprof[(k - 1) * kProfPhases + 13] = clock64();
+        }
+        cluster_wait();
         SEPSO_MARK(7);
 
         // partials were pushed before the barrier: nothing to gather
@@ -373,15 +414,10 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
             }
             if (lane == 0) m->k_done = k;
             SEPSO_MARK(14);
-        } else if (k < p.cap && p.rng == kMt19937) {
-            // meanwhile, warps 1..4 walk the reference stream to this step's
-            // r1, r2, r3 blocks (draw_step_randoms, swarm.hpp:59-70) and keep
-            // this CTA's rows as the step factors a_j = c_j * r_j
-            const int gn = nthr - 32 < 128 ? nthr - 32 : 128;
-            long long* gprof = (p.prof != nullptr && swarm == 0 && c.crank == 0 && tid == 32) ? p.prof : nullptr;
-            if (gprof) gprof[(k - 1) * kProfPhases + 12] = clock64();
-            if (tid - 32 < gn) mt_step_draws(c, mtbuf, MtGroup{tid - 32, gn, 1}, k, row1);
-            if (gprof) gprof[(k - 1) * kProfPhases + 13] = clock64();
+        } else if (k < p.cap && p.rng == kMt19937 && !gen_early) {
+            // small CTAs: warps 1.. walk the stream to this step's factors
+            // while warp 0 updates the bests
+            if (nthr >= 64) mt_step_draws(c, mtbuf, MtGroup{tid - 32, nthr - 32, 1}, k, row1);
         } else if (k < p.cap && p.rng == kPhilox) {
             // meanwhile: this step's draws (draw_step_randoms, swarm.hpp:59-70) --
             // they depend only on (seed, k, row), not on the bests

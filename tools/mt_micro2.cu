@@ -71,6 +71,21 @@ __global__ void __launch_bounds__(1024) k_mt_probe(long long blocks, int mode, u
     if (threadIdx.x == 0) *cycles = clock64() - t0;
 }
 
+// fused-kernel init shape: 1024 threads, warps 0..3 generate (named barrier 3), no deliveries
+__global__ void __launch_bounds__(1024, 1) k_b(long long blocks, long long* cyc, float* gsink, int gsize) {
+    __shared__ unsigned long long buf[kMtStateWords];
+    const int tid = threadIdx.x;
+    if (tid == 0) mt_seed_words(buf + 312, 12345ull);
+    __syncthreads();
+    const long long t0 = clock64();
+    const MtGroup grp = gsize < int(blockDim.x) ? MtGroup{tid, gsize, 3} : MtGroup{tid, int(blockDim.x), 0};
+    MtState mt{buf, 0, 0};
+    if (tid < grp.n) mt_generate(mt, grp, 312 * blocks, 312 * blocks, [&](int, unsigned long long) {});
+    __syncthreads();
+    if (tid == 0) *cyc = clock64() - t0;
+    if (buf[tid % 624] == 42) gsink[0] = 1.f;
+}
+
 __global__ void k_spin(long long cycles, float* o) {
     const long long t0 = clock64();
     float x = threadIdx.x;
@@ -94,6 +109,11 @@ int main() {
         long long h;
         k_mt_probe<<<1, 320>>>(2000, mode, out, cyc); cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
         printf("calib copy mode %d: %.1f\n", mode, double(h) / 2000);
+    }
+    for (int gs : {128, 1024}) {
+        long long h;
+        k_b<<<1, 1024>>>(2000, cyc, sb, gs); cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+        printf("init shape group %d: %.1f per block\n", gs, double(h) / 2000);
     }
     for (int rep = 0; rep < 2; ++rep)
     for (long long B : {2000ll, 4000ll}) {
