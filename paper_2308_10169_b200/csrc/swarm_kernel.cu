@@ -92,7 +92,9 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
     long long* const prof = (p.prof != nullptr && swarm == 0 && c.crank == 0 && tid == 0) ? p.prof : nullptr;
 #define SEPSO_MARK(ph) do { if (prof) prof[(k - 1) * kProfPhases + (ph)] = clock64(); } while (0)
 #define SEPSO_IMARK(ph) do { if (prof) prof[p.cap * kProfPhases + (ph)] = clock64(); } while (0)
+#define SEPSO_GMARK(ph) do { if (prof) { unsigned long long g_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_)); prof[p.cap * kProfPhases + (ph)] = (long long)g_; } } while (0)
     SEPSO_IMARK(0);
+    SEPSO_GMARK(7);
 
     // ---------------------------------------------------------- constants
     // With the mt19937 stream, the last warp's lane 0 seeds the generator
@@ -203,6 +205,7 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
     }
     __syncthreads();
     SEPSO_IMARK(6);
+    SEPSO_GMARK(8);
 
     // ------------------------------------------------------------ iterations
     int k = 1;
@@ -488,6 +491,24 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
     }
 
     // ---------------------------------------------------------------- results
+    SEPSO_GMARK(9);
+    // record length = path_length(best) in FP64 (planner.hpp:194): warp 0 of
+    // rank 0 computes the S segment hypots in parallel, summed in path order
+    double path_len = 0.0;
+    if (PATH && c.crank == 0 && warp == 0) {
+        for (int j0 = 0; j0 < c.S; j0 += 32) {
+            const int j = j0 + lane;
+            double h = 0.0;
+            if (j < c.S) {
+                const double px = j == 0 ? double(c.sx) : double(c.tbx[j - 1]);
+                const double py = j == 0 ? double(c.sy) : double(c.tbx[c.W + j - 1]);
+                const double nx = j < c.W ? double(c.tbx[j]) : double(c.tx);
+                const double ny = j < c.W ? double(c.tbx[c.W + j]) : double(c.ty);
+                h = hypot_glibc(__dsub_rn(nx, px), __dsub_rn(ny, py));
+            }
+            for (int i = 0; i < 32 && j0 + i < c.S; ++i) path_len = __dadd_rn(path_len, __shfl_sync(0xffffffffu, h, i));
+        }
+    }
     if (c.crank == 0 && tid == 0) {
         const Misc<T>* m = c.m;
         SwarmOut o{};
@@ -502,17 +523,7 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
         } else {
             o.fitness = double(m->tbf);
             o.q = uint32_t(m->tbq);
-            if (PATH) {   // record length = path_length(best) in FP64 (planner.hpp:194)
-                double total = 0.0;
-                double px = double(c.sx), py = double(c.sy);
-                for (int j = 1; j <= c.W + 1; ++j) {
-                    const double nx = j <= c.W ? double(c.tbx[j - 1]) : double(c.tx);
-                    const double ny = j <= c.W ? double(c.tbx[c.W + j - 1]) : double(c.ty);
-                    total = __dadd_rn(total, hypot_glibc(__dsub_rn(nx, px), __dsub_rn(ny, py)));
-                    px = nx; py = ny;
-                }
-                o.length = total;
-            }
+            if (PATH) o.length = path_len;
         }
         p.out[swarm] = o;
     }
@@ -523,7 +534,9 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
                 p.win_vals[size_t(swarm) * p.tw + i] = c.win[(c.m->win_head + i) % p.tw];
         if (tid == 0 && p.carry) p.win_len[swarm] = c.m->win_len;
     }
+    SEPSO_GMARK(10);
     cluster.sync();   // no CTA leaves while a peer may still read its shared memory
+    SEPSO_GMARK(11);
 }
 
 // ------------------------------------------------------------------ launcher
@@ -628,6 +641,11 @@ __global__ void k_step_worlds(unsigned char* worlds, int n, long long stride, in
 int launch_step_worlds(unsigned char* worlds, int n, long long stride, int off_offsets,
                        int off_verts, int off_vel, double dt, void* stream) {
     if (n <= 0) return 0;
+    static bool carve = false;       // keep the SM shared-memory split of the planning kernel
+    if (!carve) {
+        cudaFuncSetAttribute(k_step_worlds, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        carve = true;
+    }
     k_step_worlds<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
         worlds, n, stride, off_offsets, off_verts, off_vel, dt);
     return int(cudaGetLastError());
