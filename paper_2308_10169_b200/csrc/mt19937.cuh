@@ -109,14 +109,19 @@ __device__ __forceinline__ void mt_store_quad(unsigned long long* nb, int t, con
 }
 
 // Words of a stored pair (624 words, first at stream offset rel from `from`)
-// that fall in [0, len), handed to the sink by the group's threads.
+// that fall in [0, len), handed to the sink by the group's threads -- by the
+// threads beyond the four compute warps when the group has them, so delivery
+// stays off the generation chain.
 template <class Sink>
 __device__ __forceinline__ void mt_deliver_pair(const unsigned long long* pr, long long rel, int len,
                                                 const MtGroup& g, Sink& sink) {
     const int lo = rel < 0 ? int(-rel) : 0;
     const long long hi_ = (long long)len - rel;
     const int hi = hi_ < 624 ? int(hi_) : 624;
-    for (int i = lo + g.lt; i < hi; i += g.n) sink(int(rel + i), mt_temper(pr[i]));
+    const bool helpers = g.n >= 256;
+    const int dl = helpers ? g.lt - 128 : g.lt, dn = helpers ? g.n - 128 : g.n;
+    if (dl < 0) return;
+    for (int i = lo + dl; i < hi; i += dn) sink(int(rel + i), mt_temper(pr[i]));
 }
 
 // Deliver stream words [from, upto) to sink(w - from, tempered word) (callers

@@ -86,6 +86,36 @@ __global__ void __launch_bounds__(1024, 1) k_b(long long blocks, long long* cyc,
     if (buf[tid % 624] == 42) gsink[0] = 1.f;
 }
 
+// generator-CTA step shape: group of gs threads, every word delivered to smem
+__global__ void __launch_bounds__(1024, 1) k_c(long long blocks, long long* cyc, float* gsink, int gs, int mode) {
+    __shared__ unsigned long long buf[kMtStateWords];
+    __shared__ float stage[4096];
+    __shared__ float hyp[48];
+    const int tid = threadIdx.x;
+    if (tid < 48) hyp[tid] = 0.5f + tid;
+    if (tid == 0) mt_seed_words(buf + 312, 12345ull);
+    __syncthreads();
+    const long long t0 = clock64();
+    const MtGroup grp = gs < int(blockDim.x) ? MtGroup{tid, gs, 3} : MtGroup{tid, int(blockDim.x), 0};
+    MtState mt{buf, 0, 0};
+    if (tid < grp.n) {
+        for (long long w0 = 0; w0 < 312 * blocks; w0 += 4080) {
+            if (mode == 0)
+                mt_generate(mt, grp, w0, w0 + 4080, [&](int e, unsigned long long word) {
+                    stage[e & 4095] = unit_from_word<float>(word);
+                });
+            else
+                mt_generate(mt, grp, w0, w0 + 4080, [&](int e, unsigned long long word) {
+                    const int j = e >= 2720 ? 2 : (e >= 1360 ? 1 : 0), row = e - j * 1360;
+                    stage[e & 4095] = hyp[(row / 170) * 6 + j] * unit_from_word<float>(word);
+                });
+        }
+    }
+    __syncthreads();
+    if (tid == 0) *cyc = clock64() - t0;
+    if (stage[tid] == 42.f) gsink[0] = 1.f;
+}
+
 __global__ void k_spin(long long cycles, float* o) {
     const long long t0 = clock64();
     float x = threadIdx.x;
@@ -109,6 +139,12 @@ int main() {
         long long h;
         k_mt_probe<<<1, 320>>>(2000, mode, out, cyc); cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
         printf("calib copy mode %d: %.1f\n", mode, double(h) / 2000);
+    }
+    for (int mode = 0; mode < 2; ++mode)
+    for (int gs : {128, 256, 512, 1024}) {
+        long long h;
+        k_c<<<1, 1024>>>(2000, cyc, sb, gs, mode); cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+        printf("gcta shape mode %d group %d: %.1f per block\n", mode, gs, double(h) / 2000);
     }
     for (int gs : {128, 1024}) {
         long long h;
