@@ -17,6 +17,41 @@ namespace sepso {
 __device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.aligned;" ::: "memory"); }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
 
+// ---- partial exchange over DSMEM: st.async with mbarrier transaction counts.
+// Every CTA expects a fixed byte count per iteration into mbarrier (k & 1);
+// peers' stores complete it, so no cluster-wide barrier (and none of its
+// GPU-scope fence / L1 invalidation) sits in the iteration.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return uint32_t(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t peer_addr(uint32_t a, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_async_v4(uint32_t dst, uint4 v, uint32_t bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
+                 ::"r"(dst), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void st_async_b32(uint32_t dst, uint32_t v, uint32_t bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];"
+                 ::"r"(dst), "r"(v), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred P1;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+        " @!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(bar), "r"(parity) : "memory");
+}
+
 // r1, r2, r3 of step k (draw_step_randoms, swarm.hpp:59-70): R words each at
 // 2RD + (k-1)*3R of the mt19937_64 stream; rows [row0, row1) keep a_j = c_j * r_j.
 template <class T>
@@ -69,6 +104,15 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
     c.fD.init(uint32_t(c.D));
     c.fN.init(uint32_t(c.N));
     c.C = p.C; c.crank = int(cluster.block_rank());
+    // partial-exchange mbarriers (one arrival: the local expect_tx); published
+    // to the peers by a cluster arrive here and a wait before the first push
+    const uint32_t mbar0 = smem_addr(smem + L.mbar);
+    if (threadIdx.x == 0) {
+        mbar_init(mbar0, 1);
+        mbar_init(mbar0 + 8, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cluster_arrive();
     c.row0 = c.crank * p.rows_per_cta;
     const int row1 = min(c.R, c.row0 + p.rows_per_cta);
     c.P = max(0, row1 - c.row0);
@@ -85,6 +129,14 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
     c.obb = (T*)S8(L.obb); c.ooff = (int*)S8(L.ooff); c.ofl = (int*)S8(L.ofl); c.vert = (T*)S8(L.vert);
     c.edge = (T*)S8(L.edge); c.list = (uint32_t*)S8(L.list); c.m = (Misc<T>*)S8(L.misc);
     const int LGM = p.max_local_groups;
+    // bytes every CTA receives per iteration: each CTA's group partials (16 B)
+    // and their rows (D values), plus every CTA's first non-finite row (4 B)
+    uint32_t xbytes = 0;
+    for (int cc = 0; cc < c.C; ++cc) {
+        const int r0 = cc * p.rows_per_cta, r1 = min(c.R, r0 + p.rows_per_cta);
+        if (r1 > r0) xbytes += uint32_t(((r1 - 1) / c.N - r0 / c.N + 1) * (16 + c.D * int(sizeof(T))));
+        xbytes += 4;
+    }
     const uint64_t seed =
         p.roots ? splitmix64(splitmix64(p.roots[swarm] ^ p.tag_hash) + uint64_t(p.frame_index))
                 : p.seeds[swarm];
@@ -208,6 +260,7 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
     SEPSO_GMARK(8);
 
     // ------------------------------------------------------------ iterations
+    if (p.cap < 1) cluster_wait();
     int k = 1;
     for (; k <= p.cap; ++k) {
         const int buf = k & 1;
@@ -237,6 +290,8 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
         }
         __syncthreads();
         SEPSO_MARK(5);
+        if (tid == 0) mbar_expect(mbar0 + 8 * buf, xbytes);
+        if (k == 1) cluster_wait();       // every peer is running, its mbarriers initialised
         // per-CTA group partials: (pbest_f, row) lexicographic min, one warp per group
         for (int lg = warp; lg < c.LG; lg += nthr >> 5) {
             const int g = gfirst + lg;
@@ -260,38 +315,40 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
             }
             br = __shfl_sync(0xffffffffu, br, 0);
             // push (value, row, q) and the row itself into every peer's slot
-            // (crank, lg) of buffer buf: after the cluster barrier all reads are local
+            // (crank, lg) of buffer buf with st.async; each store completes its
+            // bytes on the peer's mbarrier of this parity.  A group without a
+            // finite best still sends a row so the byte count stays fixed.
             const int slot = c.crank * LGM + lg;
             Part pt;
             pt.f = br == INT_MAX ? double(A::inf()) : double(c.pbf[br]);
             pt.row = br == INT_MAX ? INT_MAX : br + c.row0;
             pt.q = br == INT_MAX ? 0 : c.pbq[br];
+            const int brow = br == INT_MAX ? 0 : br;
+            const uint32_t mb = mbar0 + 8 * buf;
             for (int r = lane; r < c.C; r += 32) {
-                Part* rp = cluster.map_shared_rank(c.part, r);
-                rp[buf * c.C * LGM + slot] = pt;
+                const uint4 v = *reinterpret_cast<const uint4*>(&pt);
+                st_async_v4(peer_addr(smem_addr(c.part + buf * c.C * LGM + slot), r), v, peer_addr(mb, r));
             }
-            if (br != INT_MAX) {
-                if (sizeof(T) == 4 && (D & 3) == 0) {          // 16-byte remote stores
-                    const int D4 = D >> 2;
-                    for (int t = lane; t < c.C * D4; t += 32) {
-                        const int r = t / D4, d4 = t - r * D4;
-                        float4* rx = reinterpret_cast<float4*>(cluster.map_shared_rank(c.px, r));
-                        rx[(buf * c.C * LGM + slot) * D4 + d4] =
-                            reinterpret_cast<const float4*>(c.pb + br * D)[d4];
-                    }
-                } else {
-                    for (int t = lane; t < c.C * D; t += 32) {
-                        const int r = int(c.fD.div(uint32_t(t))), d = t - r * D;
-                        T* rx = cluster.map_shared_rank(c.px, r);
-                        rx[(buf * c.C * LGM + slot) * D + d] = c.pb[br * D + d];
-                    }
+            const uint32_t dst0 = smem_addr(c.px + size_t(buf * c.C * LGM + slot) * D);
+            if ((D * int(sizeof(T))) % 16 == 0) {                         // 16-byte vectors
+                const int V4 = (D * int(sizeof(T))) / 16;
+                const uint4* src = reinterpret_cast<const uint4*>(c.pb + brow * D);
+                for (int t = lane; t < c.C * V4; t += 32) {
+                    const int r = t / V4, q4 = t - r * V4;
+                    st_async_v4(peer_addr(dst0 + 16 * q4, r), src[q4], peer_addr(mb, r));
+                }
+            } else {                                                      // 4-byte words
+                const int V1 = (D * int(sizeof(T))) / 4;
+                const uint32_t* src = reinterpret_cast<const uint32_t*>(c.pb + brow * D);
+                for (int t = lane; t < c.C * V1; t += 32) {
+                    const int r = t / V1, q1 = t - r * V1;
+                    st_async_b32(peer_addr(dst0 + 4 * q1, r), src[q1], peer_addr(mb, r));
                 }
             }
         }
-        if (tid < c.C) {
-            int* rb = cluster.map_shared_rank(c.allbad, tid);
-            rb[buf * c.C + c.crank] = c.m->bad_row;
-        }
+        if (tid < c.C)
+            st_async_b32(peer_addr(smem_addr(c.allbad + buf * c.C + c.crank), tid), uint32_t(c.m->bad_row),
+                         peer_addr(mbar0 + 8 * buf, tid));
         SEPSO_MARK(6);
         // Partials of every CTA visible cluster-wide (barrier.cluster arrive +
         // wait).  With the mt19937 stream the last four warps arrive early and
@@ -300,14 +357,13 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
         // the bests; the factors are read after the barrier that follows B1.
         const bool gen_early = p.rng == kMt19937 && k < p.cap && nthr >= 192;
         const int gw0 = (nthr >> 5) - 4;
-        cluster_arrive();
         if (gen_early && warp >= gw0) {
             long long* gprof = (p.prof != nullptr && swarm == 0 && c.crank == 0 && tid == gw0 * 32) ? p.prof : nullptr;
             if (gprof) gprof[(k - 1) * kProfPhases + 12] = clock64();
             mt_step_draws(c, mtbuf, MtGroup{tid - gw0 * 32, 128, 1}, k, row1);
             if (gprof) gprof[(k - 1) * kProfPhases + 13] = clock64();
         }
-        cluster_wait();
+        if (warp == 0) mbar_wait(mbar0 + 8 * buf, uint32_t(((k - 1) >> 1) & 1));   // every CTA's partials
         SEPSO_MARK(7);
 
         // partials were pushed before the barrier: nothing to gather

@@ -98,7 +98,7 @@ struct Part {
 
 struct SmemLayout {
     size_t x, v, pb, pbf, pbq, q, fit, imp, seglen, coef, lo, hi, hyp, gbx, gbf, gbq, chg, tbx,
-        win, part, px, allpart, allbad, gtab, ctab, obb, ooff, ofl, vert, edge, list, mt, misc, total;
+        win, part, px, allpart, allbad, gtab, ctab, obb, ooff, ofl, vert, edge, list, mt, mbar, misc, total;
 };
 
 #ifdef __CUDACC__
@@ -118,6 +118,7 @@ SEPSO_LHD SmemLayout smem_layout(const SwarmParams& p, size_t tsz, bool path) {
     size_t o = 0;
     auto take = [&](size_t bytes) { const size_t at = o; o = sm_align(o + bytes); return at; };
     L.misc = take(256);
+    L.mbar = take(16);                     // partial-exchange mbarriers, one per iteration parity
     L.x = take(P * D * tsz);
     L.v = take(P * D * tsz);
     L.pb = take(P * D * tsz);

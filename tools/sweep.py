@@ -11,8 +11,10 @@ eng = pe.Engine(0, prec)
 planner = pe.PlannerConfig(max_iters_per_frame=30, window_carryover=True)
 cold = pe.PlannerConfig(max_iters_per_frame=30)
 res = []
-for C in (4, 8, 16):
-    for T in (256, 512, 1024):
+CS = [int(x) for x in os.environ.get('SWEEP_C', '4,8,16').split(',')]
+TS = [int(x) for x in os.environ.get('SWEEP_T', '256,512,1024').split(',')]
+for C in CS:
+    for T in TS:
         eng.set_launch(C, T)
         try:
             # latency: one scenario, 40 frames
