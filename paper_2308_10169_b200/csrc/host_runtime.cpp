@@ -241,13 +241,14 @@ int launch_fused(sf_ctx* ctx, FusedPlan& fp, int problem) {
     static const bool phase_prof = std::getenv("SEPSO_PHASE_PROF") != nullptr;
     long long* prof = nullptr;
     if (phase_prof && fp.p.cap > 0) {
-        cudaMalloc(&prof, sizeof(long long) * kProfPhases * (fp.p.cap + 1));
-        cudaMemsetAsync(prof, 0, sizeof(long long) * kProfPhases * (fp.p.cap + 1), ctx->stream);
+        const size_t nprof = size_t(kProfPhases) * (fp.p.cap + 1) + 2 * 16 * size_t(fp.p.cap);
+        cudaMalloc(&prof, sizeof(long long) * nprof);
+        cudaMemsetAsync(prof, 0, sizeof(long long) * nprof, ctx->stream);
         fp.p.prof = prof;
     }
     const int e = launch_swarms(fp.p, problem, ctx->precision == SF_FP64, ctx->stream, &smem);
     if (prof) {
-        std::vector<long long> h(size_t(kProfPhases) * (fp.p.cap + 1));
+        std::vector<long long> h(size_t(kProfPhases) * (fp.p.cap + 1) + 2 * 16 * size_t(fp.p.cap));
         cudaMemcpyAsync(h.data(), prof, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream);
         cudaStreamSynchronize(ctx->stream);
         cudaFree(prof);
@@ -280,6 +281,19 @@ int launch_fused(sf_ctx* ctx, FusedPlan& fp, int problem) {
                          r[1] - r[0], r[2] - r[1], r[3] - r[2], r[4] - r[3], r[5] - r[4], r[6] - r[5]);
             std::fprintf(stderr, " | ns: init=%lld loop=%lld out=%lld exit=%lld total=%lld",
                          r[8] - r[7], r[9] - r[8], r[10] - r[9], r[11] - r[10], r[11] - r[7]);
+            // per-CTA work before the partial exchange (cycles): spread over CTAs
+            const long long* w = h.data() + size_t(kProfPhases) * (fp.p.cap + 1);
+            double smin = 0, smax = 0, sown = 0;
+            int nk = 0;
+            for (int k = 0; k < iters; ++k) {
+                long long mn = LLONG_MAX, mx = 0;
+                for (int cc = 0; cc < std::min(16, fp.p.C); ++cc) {
+                    const long long v = w[(size_t(k) * 16 + cc) * 2];
+                    mn = std::min(mn, v); mx = std::max(mx, v);
+                }
+                smin += double(mn); smax += double(mx); sown += double(w[(size_t(k) * 16) * 2 + 1]); ++nk;
+            }
+            if (nk) std::fprintf(stderr, " | per-CTA fitness..push: min=%.0f max=%.0f cta0_wait=%.0f", smin / nk, smax / nk, sown / nk);
         }
         std::fprintf(stderr, "\n");
     }

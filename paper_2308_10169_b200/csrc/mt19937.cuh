@@ -133,14 +133,15 @@ __device__ __forceinline__ void mt_deliver_pair(const unsigned long long* pr, lo
 // shared memory during pass j+1 (the pair stays intact until pass j+2).  The
 // sink's writes are complete when every group thread has returned; callers
 // synchronise before reading them.
-template <class Sink>
+// FN > 0: the group is known to have FN >= 128 threads (fast path only).
+template <int FN = 0, class Sink>
 __device__ inline void mt_generate(MtState& s, const MtGroup& g, long long from, long long upto,
                                    Sink&& sink) {
     const int len = int(upto - from);
     long long rel = 312 * s.blocks - from;        // offset of the next new word
     bool pend = s.blocks > 0 && rel > 0 && rel - 624 < len;   // the latest pair
     long long prel = rel - 624;
-    if (g.n >= 128) {
+    if (FN >= 128 || g.n >= 128) {
         const int lt = g.lt;
         const bool act = lt < 128;
         const int w = lt >> 5, l = lt & 31;
@@ -163,7 +164,7 @@ __device__ inline void mt_generate(MtState& s, const MtGroup& g, long long from,
             pend = rel + 624 > 0;
             rel += 624;
         }
-    } else {
+    } else if (FN == 0) {
         while (rel < len) {
             const unsigned long long* o = s.buf + s.cur * 624 + 312;
             unsigned long long* nb = s.buf + (s.cur ^ 1) * 624;

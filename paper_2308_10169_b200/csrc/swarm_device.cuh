@@ -169,7 +169,7 @@ struct FastDiv {
 template <class T> struct Ctx {
     // shape
     int G, N, D, W, S, R, P, row0, LG, O, C, crank;
-    FastDiv fS, fD, fN;
+    FastDiv fS, fD, fN, fV;       // fV: 16- or 4-byte units of one pushed row
     // shared arrays
     T *x, *v, *pb, *pbf, *fit, *seglen, *coef, *lo, *hi, *hyp, *gbx, *gbf, *tbx, *px;
     int *pbq, *q, *imp, *gbq, *chg, *ooff, *ofl, *allbad, *gtab, *ctab;
@@ -230,6 +230,13 @@ inline __device__ int pair_count<double>(const Ctx<double>& c, int pl, int s, in
     return pair_count_pts(c, a1x, a1y, a2x, a2y, o);
 }
 
+// FP32 engine fallback to the FP64 reference predicate, kept out of line so the
+// hot loop's code stays compact (the fallback is rare).
+static __device__ __noinline__ int seg_ref_f(float a1x, float a1y, float a2x, float a2y, float b1x, float b1y,
+                                      float b2x, float b2y) {
+    return segments_intersect_ref(a1x, a1y, a2x, a2y, b1x, b1y, b2x, b2y);
+}
+
 // FP32 engine: filtered orientation signs.
 // Vertex crosses cv_i = d x (v_i - a1) are shared by the two edges meeting at
 // v_i (o1 of edge i is o2 of edge i-1).  With every |cv| above the bound B and
@@ -269,10 +276,10 @@ inline __device__ int pair_count_pts(const Ctx<float>& c, float a1x, float a1y, 
         int r3 = fast_pair(a1x, a1y, dx, dy, e3.x, e3.y, e3.z, e3.w, B);
         if ((r0 | r1 | r2 | r3) < 0) {                 // some sign uncertain: FP64 reference
             const float* vv = c.vert + 2 * v0;
-            if (r0 < 0) r0 = segments_intersect_ref(a1x, a1y, a2x, a2y, vv[0], vv[1], vv[2], vv[3]);
-            if (r1 < 0) r1 = segments_intersect_ref(a1x, a1y, a2x, a2y, vv[2], vv[3], vv[4], vv[5]);
-            if (r2 < 0) r2 = segments_intersect_ref(a1x, a1y, a2x, a2y, vv[4], vv[5], vv[6], vv[7]);
-            if (r3 < 0) r3 = segments_intersect_ref(a1x, a1y, a2x, a2y, vv[6], vv[7], vv[0], vv[1]);
+            if (r0 < 0) r0 = seg_ref_f(a1x, a1y, a2x, a2y, vv[0], vv[1], vv[2], vv[3]);
+            if (r1 < 0) r1 = seg_ref_f(a1x, a1y, a2x, a2y, vv[2], vv[3], vv[4], vv[5]);
+            if (r2 < 0) r2 = seg_ref_f(a1x, a1y, a2x, a2y, vv[4], vv[5], vv[6], vv[7]);
+            if (r3 < 0) r3 = seg_ref_f(a1x, a1y, a2x, a2y, vv[6], vv[7], vv[0], vv[1]);
         }
         return r0 + r1 + r2 + r3;
     }
@@ -295,8 +302,8 @@ inline __device__ int pair_count_pts(const Ctx<float>& c, float a1x, float a1y, 
             atomicAdd(&c.m->n_cont, 1);
 #endif
             const int j = (i + 1 == v1) ? v0 : i + 1;
-            r = segments_intersect_ref(a1x, a1y, a2x, a2y, c.vert[2 * i], c.vert[2 * i + 1],
-                                       c.vert[2 * j], c.vert[2 * j + 1]);
+            r = seg_ref_f(a1x, a1y, a2x, a2y, c.vert[2 * i], c.vert[2 * i + 1], c.vert[2 * j],
+                          c.vert[2 * j + 1]);
         }
         cnt += r;
     }
@@ -319,6 +326,13 @@ __device__ int contain_count_ref(const Ctx<T>& c, int pl, int o) {
     const T* vb = c.vert + 2 * v0;
     return point_strictly_inside_ref(
         px, py, n, [vb](int i) { return double(vb[2 * i]); },
+        [vb](int i) { return double(vb[2 * i + 1]); });
+}
+
+// FP32 engine fallback, out of line (rare): point (px, py) vs polygon vb[0..n)
+static __device__ __noinline__ int contain_ref_f(float px, float py, const float* vb, int n) {
+    return point_strictly_inside_ref(
+        double(px), double(py), n, [vb](int i) { return double(vb[2 * i]); },
         [vb](int i) { return double(vb[2 * i + 1]); });
 }
 
@@ -347,7 +361,7 @@ template <> inline __device__ int contain_count<float>(const Ctx<float>& c, int 
 #pragma unroll
         for (int i = 0; i < 4; ++i) cr[i] = fmaf(e[i].z, py - e[i].y, -(e[i].w * (px - e[i].x)));
         if (!(fminf(fminf(fabsf(cr[0]), fabsf(cr[1])), fminf(fabsf(cr[2]), fabsf(cr[3]))) > B))
-            return contain_count_ref(c, pl, o);
+            return contain_ref_f(px, py, c.vert + 2 * v0, 4);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const float ay = e[i].y, by = e[(i + 1) & 3].y;
@@ -358,7 +372,7 @@ template <> inline __device__ int contain_count<float>(const Ctx<float>& c, int 
     for (int i = v0; i < v1; ++i) {
         const float4 e = E[i];                       // a = (e.x, e.y), b - a = (e.z, e.w)
         const float cr = fmaf(e.z, py - e.y, -(e.w * (px - e.x)));
-        if (!(fabsf(cr) > B)) return contain_count_ref(c, pl, o);
+        if (!(fabsf(cr) > B)) return contain_ref_f(px, py, c.vert + 2 * v0, v1 - v0);
         const int j = (i + 1 == v1) ? v0 : i + 1;
         const float ay = e.y, by = c.vert[2 * j + 1];
         if ((ay > py) != (by > py) && ((cr > 0.f) == (by > ay))) inside = !inside;
@@ -455,8 +469,9 @@ __device__ void load_world(Ctx<T>& c, const unsigned char* wrec, int off_offsets
 //       fallback); first-waypoint containment tasks continue the item space.
 //   A3  fitness = sum of lengths in chain order + alpha * Q^beta.
 template <class T>
-__device__ void path_fitness_phase(const SwarmParams& p, Ctx<T>& c, long long* prof = nullptr,
+__device__ void path_fitness_phase(const SwarmParams& p, Ctx<T>& c, long long* prof_ = nullptr,
                                    int k = 0) {
+    long long* const prof = kProfiling ? prof_ : nullptr;
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int S = c.S, items = c.P * S, O = c.O;
     // ---- A1

@@ -54,15 +54,16 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 
 // r1, r2, r3 of step k (draw_step_randoms, swarm.hpp:59-70): R words each at
 // 2RD + (k-1)*3R of the mt19937_64 stream; rows [row0, row1) keep a_j = c_j * r_j.
-template <class T>
+template <int FN, class T>
 __device__ void mt_step_draws(Ctx<T>& c, unsigned long long* mtbuf, const MtGroup& grp, int k, int row1) {
     using A = Ar<T>;
     const int R = c.R;
     const long long base = 2ll * R * c.D + (long long)(k - 1) * 3 * R;
     MtState mt{mtbuf, c.m->mt_cur, c.m->mt_blocks};      // registers only while generating
     // one window per factor: only this CTA's rows are tempered and kept
+#pragma unroll 1
     for (int j = 0; j < 3; ++j)
-        mt_generate(mt, grp, base + (long long)j * R + c.row0, base + (long long)j * R + row1,
+        mt_generate<FN>(mt, grp, base + (long long)j * R + c.row0, base + (long long)j * R + row1,
                     [&](int pl, unsigned long long word) {
                         const int g = int(c.fN.div(uint32_t(c.row0 + pl)));
                         c.coef[j * c.P + pl] = A::mul(c.hyp[g * 6 + j], unit_from_word<T>(word));
@@ -103,6 +104,7 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
     c.fS.init(uint32_t(c.S));
     c.fD.init(uint32_t(c.D));
     c.fN.init(uint32_t(c.N));
+    c.fV.init(uint32_t((c.D * int(sizeof(T))) % 16 == 0 ? c.D * int(sizeof(T)) / 16 : c.D * int(sizeof(T)) / 4));
     c.C = p.C; c.crank = int(cluster.block_rank());
     // partial-exchange mbarriers (one arrival: the local expect_tx); published
     // to the peers by a cluster arrive here and a wait before the first push
@@ -141,10 +143,14 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
         p.roots ? splitmix64(splitmix64(p.roots[swarm] ^ p.tag_hash) + uint64_t(p.frame_index))
                 : p.seeds[swarm];
     const int G = c.G, N = c.N, D = c.D, R = c.R;
-    long long* const prof = (p.prof != nullptr && swarm == 0 && c.crank == 0 && tid == 0) ? p.prof : nullptr;
+    long long* const prof = (kProfiling && p.prof != nullptr && swarm == 0 && c.crank == 0 && tid == 0) ? p.prof : nullptr;
+    // per-CTA (thread 0) work before the exchange: [(k * 16 + crank) * 2] = cycles, [+1] = wait
+    long long* const wprof = (kProfiling && p.prof != nullptr && swarm == 0 && tid == 0 && c.crank < 16)
+                                 ? p.prof + size_t(kProfPhases) * (p.cap + 1) : nullptr;
+    long long wt0 = 0;
 #define SEPSO_MARK(ph) do { if (prof) prof[(k - 1) * kProfPhases + (ph)] = clock64(); } while (0)
 #define SEPSO_IMARK(ph) do { if (prof) prof[p.cap * kProfPhases + (ph)] = clock64(); } while (0)
-#define SEPSO_GMARK(ph) do { if (prof) { unsigned long long g_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_)); prof[p.cap * kProfPhases + (ph)] = (long long)g_; } } while (0)
+#define SEPSO_GMARK(ph) do { if (kProfiling && prof) { unsigned long long g_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_)); prof[p.cap * kProfPhases + (ph)] = (long long)g_; } } while (0)
     SEPSO_IMARK(0);
     SEPSO_GMARK(7);
 
@@ -265,6 +271,7 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
     for (; k <= p.cap; ++k) {
         const int buf = k & 1;
         SEPSO_MARK(0);
+        if (wprof) wt0 = clock64();
         // fitness (geometry.hpp:262-267 / benchmarks.hpp:45-53)
         if (PATH) path_fitness_phase(p, c, prof, k);
         else bench_fitness_phase(problem, c);
@@ -334,14 +341,14 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
                 const int V4 = (D * int(sizeof(T))) / 16;
                 const uint4* src = reinterpret_cast<const uint4*>(c.pb + brow * D);
                 for (int t = lane; t < c.C * V4; t += 32) {
-                    const int r = t / V4, q4 = t - r * V4;
+                    const int r = int(c.fV.div(uint32_t(t))), q4 = t - r * V4;
                     st_async_v4(peer_addr(dst0 + 16 * q4, r), src[q4], peer_addr(mb, r));
                 }
             } else {                                                      // 4-byte words
                 const int V1 = (D * int(sizeof(T))) / 4;
                 const uint32_t* src = reinterpret_cast<const uint32_t*>(c.pb + brow * D);
                 for (int t = lane; t < c.C * V1; t += 32) {
-                    const int r = t / V1, q1 = t - r * V1;
+                    const int r = int(c.fV.div(uint32_t(t))), q1 = t - r * V1;
                     st_async_b32(peer_addr(dst0 + 4 * q1, r), src[q1], peer_addr(mb, r));
                 }
             }
@@ -358,12 +365,18 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
         const bool gen_early = p.rng == kMt19937 && k < p.cap && nthr >= 192;
         const int gw0 = (nthr >> 5) - 4;
         if (gen_early && warp >= gw0) {
-            long long* gprof = (p.prof != nullptr && swarm == 0 && c.crank == 0 && tid == gw0 * 32) ? p.prof : nullptr;
+            long long* gprof = (kProfiling && p.prof != nullptr && swarm == 0 && c.crank == 0 && tid == gw0 * 32) ? p.prof : nullptr;
             if (gprof) gprof[(k - 1) * kProfPhases + 12] = clock64();
-            mt_step_draws(c, mtbuf, MtGroup{tid - gw0 * 32, 128, 1}, k, row1);
+            mt_step_draws<128>(c, mtbuf, MtGroup{tid - gw0 * 32, 128, 1}, k, row1);
             if (gprof) gprof[(k - 1) * kProfPhases + 13] = clock64();
         }
+        long long wt1 = 0;
+        if (wprof) wt1 = clock64();
         if (warp == 0) mbar_wait(mbar0 + 8 * buf, uint32_t(((k - 1) >> 1) & 1));   // every CTA's partials
+        if (wprof) {
+            wprof[(size_t(k - 1) * 16 + c.crank) * 2] = wt1 - wt0;
+            wprof[(size_t(k - 1) * 16 + c.crank) * 2 + 1] = clock64() - wt1;
+        }
         SEPSO_MARK(7);
 
         // partials were pushed before the barrier: nothing to gather
@@ -476,7 +489,7 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
         } else if (k < p.cap && p.rng == kMt19937 && !gen_early) {
             // small CTAs: warps 1.. walk the stream to this step's factors
             // while warp 0 updates the bests
-            if (nthr >= 64) mt_step_draws(c, mtbuf, MtGroup{tid - 32, nthr - 32, 1}, k, row1);
+            if (nthr >= 64) mt_step_draws<0>(c, mtbuf, MtGroup{tid - 32, nthr - 32, 1}, k, row1);
         } else if (k < p.cap && p.rng == kPhilox) {
             // meanwhile: this step's draws (draw_step_randoms, swarm.hpp:59-70) --
             // they depend only on (seed, k, row), not on the bests
@@ -489,7 +502,7 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
             }
         }
         if (nthr == 32 && k < p.cap && p.rng == kMt19937)     // single-warp CTA: draws after the bests
-            mt_step_draws(c, mtbuf, MtGroup{tid, 32, 0}, k, row1);
+            mt_step_draws<0>(c, mtbuf, MtGroup{tid, 32, 0}, k, row1);
         if (nthr == 32 && k < p.cap && p.rng == kPhilox) {
             const uint64_t base = 2ull * uint64_t(R) * uint64_t(D) + uint64_t(k - 1) * 3ull * uint64_t(R);
             for (int t = tid; t < 3 * c.P; t += 32) {

@@ -87,6 +87,13 @@ struct SwarmParams {
     // debug: per-iteration phase timestamps of swarm 0 / CTA 0 (SEPSO_PHASE_PROF)
     long long* prof;
 };
+// Phase profiler (SEPSO_PHASE_PROF=1 at run time) exists only in builds with
+// -DSEPSO_PROFILE (make PROF=1): the release kernel carries none of its code.
+#ifdef SEPSO_PROFILE
+constexpr bool kProfiling = true;
+#else
+constexpr bool kProfiling = false;
+#endif
 constexpr int kProfPhases = 15;   // 0..11 phase marks, 12/13 generator start/end, 14 B1 end
 
 // One CTA's best (pbest_f, row) of one group, read by its peers over DSMEM in
