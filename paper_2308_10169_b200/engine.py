@@ -20,7 +20,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libsepso_cuda.so")
+LIB_PATH = os.environ.get("SEPSO_LIB") or os.path.join(_HERE, "lib", "libsepso_cuda.so")
 
 SF_OK, SF_INVALID_ARGUMENT, SF_NON_FINITE, SF_CUDA_ERROR, SF_UNSUPPORTED = range(5)
 FP32, FP64 = 0, 1

@@ -1,6 +1,7 @@
 """Kernel-internal globaltimer breakdown per frame (SEPSO_PHASE_PROF=1), frames 5..44."""
 import os, sys
 os.environ["SEPSO_PHASE_PROF"] = "1"
+os.environ.setdefault("SEPSO_LIB", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2308_10169_b200", "lib_prof", "libsepso_cuda.so"))
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_2308_10169_b200 as pe
