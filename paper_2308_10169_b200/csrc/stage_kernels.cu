@@ -229,8 +229,9 @@ int stage_step(bool fp64, const StageShape& s, const double* hypers, const void*
 // K2 standalone: one CTA per tile of rows, world staged in shared memory, the
 // same cull + compaction + filtered-predicate machinery as the fused kernel.
 struct EvalSmem {
-    size_t misc, lo, hi, obb, ooff, ofl, vert, edge, seglen, q, list, total;
+    size_t misc, lo, hi, obb, ooff, ofl, vert, edge, seglen, q, list, grid, gidx, total;
 };
+constexpr int kGridDim = 32;   // wide worlds: kGridDim^2 cells over the map
 
 SEPSO_LHD EvalSmem eval_smem(int rows_tile, int D, int max_obs, int max_verts, int entry_cap,
                           size_t tsz, bool edges = true) {
@@ -249,6 +250,8 @@ SEPSO_LHD EvalSmem eval_smem(int rows_tile, int D, int max_obs, int max_verts, i
     L.seglen = take(size_t(rows_tile) * S * tsz);
     L.q = take(size_t(rows_tile) * 4);
     L.list = take(size_t(entry_cap) * 4);
+    L.grid = take(edges || entry_cap ? size_t(kGridDim * kGridDim + 1) * 4 : 0);
+    L.gidx = take(edges || entry_cap ? size_t(max_obs) * 4 : 0);
     L.total = o;
     return L;
 }
@@ -289,17 +292,21 @@ __global__ void __launch_bounds__(256) k_eval_path(const unsigned char* __restri
 
 
 // K2 for wide worlds (many obstacles, config 4): one warp per (particle,
-// segment) item, its lanes sweep the obstacles 32 at a time -- box cull and
-// the pair test of every overlapping obstacle run side by side in SIMT, no
-// work list.  The world is staged in shared memory once per CTA.
+// segment) item.  Lanes box-cull 32 obstacles at a time; the overlapping ones
+// are compacted (ballot + prefix) into a per-warp ring of 64 entries, and
+// whenever 32 are pending all lanes run pair tests together -- full SIMT width
+// for the expensive test instead of the few lanes whose box happened to hit.
+// 1024 threads per CTA (one CTA per SM: the staged world is ~120 KB).
+constexpr int kWideThreads = 1024, kWideRing = 64;
 template <class T>
-__global__ void __launch_bounds__(256) k_eval_path_wide(const unsigned char* __restrict__ world,
-                                                        SwarmParams pp, int rows, int rows_tile,
-                                                        const T* x, T* fit, int* qout,
-                                                        const IterState* gate) {
+__global__ void __launch_bounds__(kWideThreads, 1) k_eval_path_wide(const unsigned char* __restrict__ world,
+                                                                    SwarmParams pp, int rows, int rows_tile,
+                                                                    const T* x, T* fit, int* qout,
+                                                                    const IterState* gate) {
     if (gate != nullptr && gate->stop) return;
     extern __shared__ __align__(16) unsigned char smem[];
-    const EvalSmem L = eval_smem(rows_tile, pp.D, pp.max_obs, pp.max_verts, 0, sizeof(T), sizeof(T) == 4);
+    const EvalSmem L = eval_smem(rows_tile, pp.D, pp.max_obs, pp.max_verts, (kWideThreads / 32) * kWideRing,
+                                 sizeof(T), sizeof(T) == 4);
     const int r0 = blockIdx.x * rows_tile;
     Ctx<T> c{};
     c.D = pp.D; c.W = pp.D / 2; c.S = c.W + 1;
@@ -316,7 +323,56 @@ __global__ void __launch_bounds__(256) k_eval_path_wide(const unsigned char* __r
     for (int i = threadIdx.x; i < c.P; i += blockDim.x) c.q[i] = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    int* ring = reinterpret_cast<int*>(smem + L.list) + warp * kWideRing;
     const int S = c.S, items = c.P * S, O = c.O;
+    // Uniform grid over the map (an acceleration structure only): obstacle o
+    // is filed under the cell of its box's lower corner, sorted by cell; a
+    // segment visits the cells its margin-grown box can reach, extended by the
+    // largest obstacle extent, so every obstacle whose box can overlap is
+    // tested exactly once and the exact box test (geometry.hpp:167-188) decides.
+    int* gstart = reinterpret_cast<int*>(smem + L.grid);
+    int* gidx = reinterpret_cast<int*>(smem + L.gidx);
+    int* hist = reinterpret_cast<int*>(smem + L.list);          // ring space, before its use
+    __shared__ float ext[2];
+    const T span = c.hi[0] > c.hi[c.W] ? c.hi[0] : c.hi[c.W];
+    const T inv_cs = T(kGridDim) / (span > T(0) ? span : T(1));
+    auto cell_of = [&](T v) {
+        const T f = v * inv_cs;
+        return f < T(0) ? 0 : (f >= T(kGridDim - 1) ? kGridDim - 1 : int(f));
+    };
+    for (int i = threadIdx.x; i < kGridDim * kGridDim; i += blockDim.x) hist[i] = 0;
+    if (threadIdx.x < 2) ext[threadIdx.x] = 0.f;
+    __syncthreads();
+    for (int o = threadIdx.x; o < O; o += blockDim.x) {
+        const T* bb = c.obb + 4 * o;
+        atomicAdd(&hist[cell_of(bb[0]) + kGridDim * cell_of(bb[1])], 1);
+        atomicMax(reinterpret_cast<int*>(&ext[0]), __float_as_int(float(bb[2] - bb[0])));   // >= 0
+        atomicMax(reinterpret_cast<int*>(&ext[1]), __float_as_int(float(bb[3] - bb[1])));
+    }
+    __syncthreads();
+    if (warp == 0) {                                           // exclusive scan of the histogram
+        int run = 0;
+        for (int b0 = 0; b0 < kGridDim * kGridDim; b0 += 32) {
+            const int v = hist[b0 + lane];
+            int incl = v;
+            for (int off = 1; off < 32; off <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += t;
+            }
+            gstart[b0 + lane] = run + incl - v;
+            hist[b0 + lane] = run + incl - v;                  // fill cursor
+            run += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) gstart[kGridDim * kGridDim] = run;
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < O; o += blockDim.x) {
+        const T* bb = c.obb + 4 * o;
+        gidx[atomicAdd(&hist[cell_of(bb[0]) + kGridDim * cell_of(bb[1])], 1)] = o;
+    }
+    __syncthreads();
+    const T extw = T(ext[0]) * T(1.0001) + c.margin, exth = T(ext[1]) * T(1.0001) + c.margin;
     for (int it = warp; it < items; it += nw) {
         const int pl = int(c.fS.div(uint32_t(it))), s = it - pl * S;
         T a1x, a1y, a2x, a2y;
@@ -325,9 +381,29 @@ __global__ void __launch_bounds__(256) k_eval_path_wide(const unsigned char* __r
         if (lane == 0) c.seglen[it] = seg_length<T>(Ar<T>::sub(a2x, a1x), Ar<T>::sub(a2y, a1y));
         const T lx = a1x < a2x ? a1x : a2x, hx = a1x < a2x ? a2x : a1x;
         const T ly = a1y < a2y ? a1y : a2y, hy = a1y < a2y ? a2y : a1y;
-        int cnt = 0;
-        for (int o = lane; o < O; o += 32)
-            if (box_overlap(lx, ly, hx, hy, c.obb + 4 * o, c.margin)) cnt += pair_count_pts(c, a1x, a1y, a2x, a2y, o);
+        const int cx0 = cell_of(lx - extw), cx1 = cell_of(hx + c.margin);
+        const int cy0 = cell_of(ly - exth), cy1 = cell_of(hy + c.margin);
+        int cnt = 0, head = 0, pend = 0;
+        for (int cy = cy0; cy <= cy1; ++cy) {
+            const int g0 = gstart[cy * kGridDim + cx0], g1 = gstart[cy * kGridDim + cx1 + 1];
+            for (int i0 = g0; i0 < g1; i0 += 32) {
+                const int i = i0 + lane;
+                const int o = i < g1 ? gidx[i] : 0;
+                const bool ov = i < g1 && box_overlap(lx, ly, hx, hy, c.obb + 4 * o, c.margin);
+                const unsigned m = __ballot_sync(0xffffffffu, ov);
+                if (ov) ring[(head + pend + __popc(m & lt_mask)) & (kWideRing - 1)] = o;
+                pend += __popc(m);
+                __syncwarp();
+                if (pend >= 32) {
+                    cnt += pair_count_pts(c, a1x, a1y, a2x, a2y, ring[(head + lane) & (kWideRing - 1)]);
+                    head += 32;
+                    pend -= 32;
+                    __syncwarp();
+                }
+            }
+        }
+        if (lane < pend) cnt += pair_count_pts(c, a1x, a1y, a2x, a2y, ring[(head + lane) & (kWideRing - 1)]);
+        __syncwarp();
         if (s == 0)   // first waypoint (the segment's end) strictly inside (geometry.hpp:217-218)
             for (int o = lane; o < O; o += 32) {
                 const T* bb = c.obb + 4 * o;
@@ -362,22 +438,23 @@ int stage_eval_path(bool fp64, const unsigned char* world, int max_obs, int max_
     pp.beta_int = (beta == double(int(beta)) && beta >= 1.0 && beta <= 64.0) ? int(beta) : 0;
     const int S = D / 2 + 1;
     if (max_obs >= 48) {   // wide worlds: lanes over obstacles
-        const int rows_tile = 16;
+        const int rows_tile = 64;
         pp.entry_cap = 0;
         // FP64 reads the vertices only (no edge records)
-        const EvalSmem L = eval_smem(rows_tile, D, max_obs, max_verts, 0, fp64 ? 8 : 4, !fp64);
+        const EvalSmem L = eval_smem(rows_tile, D, max_obs, max_verts, (kWideThreads / 32) * kWideRing,
+                                     fp64 ? 8 : 4, !fp64);
         const unsigned grid = unsigned((rows + rows_tile - 1) / rows_tile);
         if (grid == 0) return 0;
         cudaError_t e;
         if (fp64) {
             e = cudaFuncSetAttribute(k_eval_path_wide<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.total));
             if (e != cudaSuccess) return int(e);
-            k_eval_path_wide<double><<<grid, 256, L.total, st>>>(world, pp, rows, rows_tile, (const double*)x,
+            k_eval_path_wide<double><<<grid, kWideThreads, L.total, st>>>(world, pp, rows, rows_tile, (const double*)x,
                                                                  (double*)fit, q, gate);
         } else {
             e = cudaFuncSetAttribute(k_eval_path_wide<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.total));
             if (e != cudaSuccess) return int(e);
-            k_eval_path_wide<float><<<grid, 256, L.total, st>>>(world, pp, rows, rows_tile, (const float*)x,
+            k_eval_path_wide<float><<<grid, kWideThreads, L.total, st>>>(world, pp, rows, rows_tile, (const float*)x,
                                                                 (float*)fit, q, gate);
         }
         return int(cudaGetLastError());
