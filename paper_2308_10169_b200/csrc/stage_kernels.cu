@@ -384,12 +384,34 @@ __global__ void __launch_bounds__(kWideThreads, 1) k_eval_path_wide(const unsign
         const int cx0 = cell_of(lx - extw), cx1 = cell_of(hx + c.margin);
         const int cy0 = cell_of(ly - exth), cy1 = cell_of(hy + c.margin);
         int cnt = 0, head = 0, pend = 0;
-        for (int cy = cy0; cy <= cy1; ++cy) {
-            const int g0 = gstart[cy * kGridDim + cx0], g1 = gstart[cy * kGridDim + cx1 + 1];
-            for (int i0 = g0; i0 < g1; i0 += 32) {
-                const int i = i0 + lane;
-                const int o = i < g1 ? gidx[i] : 0;
-                const bool ov = i < g1 && box_overlap(lx, ly, hx, hy, c.obb + 4 * o, c.margin);
+        // the cell rows' candidate ranges form one stream: lane r holds row r's
+        // start in gidx and its offset in the stream; 32 candidates per batch
+        const int nrows = cy1 - cy0 + 1;                       // <= kGridDim = 32
+        int rbeg = 0, rlen = 0;
+        if (lane < nrows) {
+            rbeg = gstart[(cy0 + lane) * kGridDim + cx0];
+            rlen = gstart[(cy0 + lane) * kGridDim + cx1 + 1] - rbeg;
+        }
+        int rinc = rlen;
+        for (int off = 1; off < 32; off <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, rinc, off);
+            if (lane >= off) rinc += t;
+        }
+        const int total = __shfl_sync(0xffffffffu, rinc, 31), rexc = rinc - rlen;
+        {
+            for (int b0 = 0; b0 < total; b0 += 32) {
+                const int t = b0 + lane;
+                int r = 0;                                       // last row with stream start <= t
+#pragma unroll
+                for (int step = 16; step; step >>= 1) {
+                    const int cand = r + step;
+                    const int ex = __shfl_sync(0xffffffffu, rexc, cand < 32 ? cand : 31);
+                    if (cand < nrows && ex <= t) r = cand;
+                }
+                const int gi = __shfl_sync(0xffffffffu, rbeg, r) + (t - __shfl_sync(0xffffffffu, rexc, r));
+                const bool in = t < total;
+                const int o = in ? gidx[gi] : 0;
+                const bool ov = in && box_overlap(lx, ly, hx, hy, c.obb + 4 * o, c.margin);
                 const unsigned m = __ballot_sync(0xffffffffu, ov);
                 if (ov) ring[(head + pend + __popc(m & lt_mask)) & (kWideRing - 1)] = o;
                 pend += __popc(m);
