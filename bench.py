@@ -333,6 +333,31 @@ def main():
                  "plans_per_s": 3 * nb * ws / (dist.max(ms) / 1e3),
                  "mean_iterations": float(np.mean([r.iterations for r in rb]))}
 
+    # ------------------------------------------------------------ extra: config 4
+    # one 65,536-particle swarm (G=8 x N=8192, D=128, 1,024 obstacles), one frame
+    # capped at 3 iterations: the HBM-staged path (K1 update + wide K2 fitness)
+    big = None
+    if a.workload == "scene" and not a.no_extra and rank == 0:
+        sc4 = pe.ScenarioConfig(map_size=366.0 * np.sqrt(128.0), dynamic_obstacles=768, static_obstacles=256,
+                                root_seed=1)
+        w4 = pe.generate_world(sc4, 1)
+        cfg4 = pe.PlannerConfig(groups=8, per_group=8192, dim=128, max_iters_per_frame=3, auto_truncate=False)
+        eng.plan_frame(w4, None, pe.EVOLVED_PATH_HYPERS, cfg4, 999)          # warm-up (allocations)
+        eng.enable_timing(True)
+        rec4 = eng.plan_frame(w4, None, pe.EVOLVED_PATH_HYPERS, cfg4, 1000)
+        ms4, _ = eng.kernel_time()
+        eng.enable_timing(False)
+        it4 = max(1, rec4.iterations)
+        S4, E4 = 65, 4 * w4.n_obstacles
+        fl4 = 65536.0 * FLOP_PER_EVAL(S4, E4)
+        big = {"workload": "config4: one swarm of 65,536 particles (G=8 x N=8192), D=128, 1,024 obstacles, "
+                           "3 iterations from a cold start (HBM-staged path)",
+               "ms_per_iteration": ms4 / it4, "evals_per_s": 65536.0 * it4 / (ms4 / 1e3),
+               "roofline": {"kernel": "k_eval_path_wide<float> + k_step (whole iteration)", "bound": "fp32",
+                            "achieved": fl4 / (ms4 / it4 / 1e3) / 1e12, "peak": peak, "unit": "TFLOP/s",
+                            "frac": fl4 / (ms4 / it4 / 1e3) / 1e12 / peak if peak else None,
+                            "flop_per_eval": FLOP_PER_EVAL(S4, E4)}}
+
     # ------------------------------------------------------------ CPU baseline
     cpu = None
     if rank == 0 and not a.no_cpu_baseline:
@@ -394,6 +419,7 @@ def main():
             "gpu_launches": 2 * K,
             "clocks": clk,
             "batched": extra,
+            "config4": big,
             "host_threads": cpu_thr,
         }
         print(json.dumps(line), flush=True)
