@@ -112,7 +112,7 @@ __device__ __forceinline__ void mt_store_quad(unsigned long long* nb, int t, con
 // that fall in [0, len), handed to the sink by the group's threads -- by the
 // threads beyond the four compute warps when the group has them, so delivery
 // stays off the generation chain.
-template <class Sink>
+template <bool RAW = false, class Sink>
 __device__ __forceinline__ void mt_deliver_pair(const unsigned long long* pr, long long rel, int len,
                                                 const MtGroup& g, Sink& sink) {
     const int lo = rel < 0 ? int(-rel) : 0;
@@ -121,7 +121,7 @@ __device__ __forceinline__ void mt_deliver_pair(const unsigned long long* pr, lo
     const bool helpers = g.n >= 256;
     const int dl = helpers ? g.lt - 128 : g.lt, dn = helpers ? g.n - 128 : g.n;
     if (dl < 0) return;
-    for (int i = lo + dl; i < hi; i += dn) sink(int(rel + i), mt_temper(pr[i]));
+    for (int i = lo + dl; i < hi; i += dn) sink(int(rel + i), RAW ? pr[i] : mt_temper(pr[i]));
 }
 
 // Deliver stream words [from, upto) to sink(w - from, tempered word) (callers
@@ -134,7 +134,8 @@ __device__ __forceinline__ void mt_deliver_pair(const unsigned long long* pr, lo
 // sink's writes are complete when every group thread has returned; callers
 // synchronise before reading them.
 // FN > 0: the group is known to have FN >= 128 threads (fast path only).
-template <int FN = 0, class Sink>
+// RAW: words are handed over untempered (the consumer applies mt_temper).
+template <int FN = 0, bool RAW = false, class Sink>
 __device__ inline void mt_generate(MtState& s, const MtGroup& g, long long from, long long upto,
                                    Sink&& sink) {
     const int len = int(upto - from);
@@ -156,7 +157,7 @@ __device__ inline void mt_generate(MtState& s, const MtGroup& g, long long from,
                 mt_store_quad(nb, lt, q1);
                 if (second) mt_store_quad(nb, t2, q2);
             }
-            if (pend) mt_deliver_pair(s.buf + s.cur * 624, prel, len, g, sink);
+            if (pend) mt_deliver_pair<RAW>(s.buf + s.cur * 624, prel, len, g, sink);
             mt_sync(g);
             s.cur ^= 1;
             s.blocks += 2;
@@ -169,7 +170,7 @@ __device__ inline void mt_generate(MtState& s, const MtGroup& g, long long from,
             const unsigned long long* o = s.buf + s.cur * 624 + 312;
             unsigned long long* nb = s.buf + (s.cur ^ 1) * 624;
             for (int t = g.lt; t < 156; t += g.n) mt_store_quad(nb, t, mt_quad_any(o, t));
-            if (pend) mt_deliver_pair(s.buf + s.cur * 624, prel, len, g, sink);
+            if (pend) mt_deliver_pair<RAW>(s.buf + s.cur * 624, prel, len, g, sink);
             mt_sync(g);
             s.cur ^= 1;
             s.blocks += 2;
@@ -178,7 +179,7 @@ __device__ inline void mt_generate(MtState& s, const MtGroup& g, long long from,
             rel += 624;
         }
     }
-    if (pend) mt_deliver_pair(s.buf + s.cur * 624, prel, len, g, sink);
+    if (pend) mt_deliver_pair<RAW>(s.buf + s.cur * 624, prel, len, g, sink);
 }
 
 } // namespace sepso

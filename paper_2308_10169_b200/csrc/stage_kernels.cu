@@ -28,14 +28,15 @@ static inline unsigned grid_for(long long work, int block) {
 }
 
 // word i of the stream: Philox by index, or a pre-generated mt19937_64 window
+// (stored untempered by k_mt_fill; tempered here, in parallel)
 __device__ __forceinline__ uint64_t stream_word(uint64_t seed, uint64_t i, const unsigned long long* words,
                                                 long long base) {
-    return words ? words[(long long)i - base] : philox_word(seed, i);
+    return words ? mt_temper(words[(long long)i - base]) : philox_word(seed, i);
 }
 
-// Advance a persisted mt19937_64 generator (one CTA, 320+ threads) and write
-// words [from, upto) to out[w - from]; words before `from` are skipped.
-__global__ void __launch_bounds__(320) k_mt_fill(MtPersist* g, unsigned long long seed, int reseed,
+// Advance a persisted mt19937_64 generator (one CTA of 256 threads) and write
+// words [from, upto), untempered, to out[w - from]; words before `from` are skipped.
+__global__ void __launch_bounds__(256) k_mt_fill(MtPersist* g, unsigned long long seed, int reseed,
                                                  long long from, long long upto,
                                                  unsigned long long* out) {
     __shared__ unsigned long long buf[kMtStateWords];
@@ -49,7 +50,7 @@ __global__ void __launch_bounds__(320) k_mt_fill(MtPersist* g, unsigned long lon
         __syncthreads();
     }
     const long long f0 = from < 0 ? 0 : from;
-    mt_generate(s, grp, f0, upto, [&](int rel, unsigned long long word) {
+    mt_generate<0, true>(s, grp, f0, upto, [&](int rel, unsigned long long word) {   // untempered
         if (out) out[(f0 - from) + rel] = word;
     });
     for (int i = threadIdx.x; i < 624; i += blockDim.x) g->st[i] = buf[s.cur * 624 + i];
@@ -58,7 +59,8 @@ __global__ void __launch_bounds__(320) k_mt_fill(MtPersist* g, unsigned long lon
 
 int stage_mt_fill(MtPersist* g, unsigned long long seed, bool reseed, long long from, long long upto,
                   unsigned long long* out, void* stream) {
-    k_mt_fill<<<1, 320, 0, static_cast<cudaStream_t>(stream)>>>(g, seed, reseed ? 1 : 0, from, upto, out);
+    // four warps compute each pass, four more store its (untempered) words
+    k_mt_fill<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(g, seed, reseed ? 1 : 0, from, upto, out);
     return int(cudaGetLastError());
 }
 

@@ -51,7 +51,8 @@ struct MtPersist {
     unsigned long long st[624];     // the two latest blocks (mt19937.cuh MtState pair)
     long long blocks;
 };
-// Generate words [from, upto) of the stream into out[w - from] (one CTA);
+// Generate words [from, upto) of the stream, untempered (consumers apply
+// mt_temper), into out[w - from] (one CTA);
 // earlier words are skipped.  reseed restarts the generator from `seed`.
 int stage_mt_fill(MtPersist* g, unsigned long long seed, bool reseed, long long from,
                   long long upto, unsigned long long* out, void* stream);

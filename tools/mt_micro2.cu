@@ -116,6 +116,16 @@ __global__ void __launch_bounds__(1024, 1) k_c(long long blocks, long long* cyc,
     if (stage[tid] == 42.f) gsink[0] = 1.f;
 }
 
+// staged-path fill: every word of [0, n) tempered into global memory
+template <bool RAW>
+__global__ void __launch_bounds__(1024) k_fill(long long n, unsigned long long* out) {
+    __shared__ unsigned long long buf[kMtStateWords];
+    MtState s{buf, 0, 0};
+    const MtGroup g{int(threadIdx.x), int(blockDim.x), 0};
+    mt_seed(s, g, 5489ull);
+    mt_generate<0, RAW>(s, g, 0, n, [&](int rel, unsigned long long word) { out[rel] = word; });
+}
+
 __global__ void k_spin(long long cycles, float* o) {
     const long long t0 = clock64();
     float x = threadIdx.x;
@@ -139,6 +149,21 @@ int main() {
         long long h;
         k_mt_probe<<<1, 320>>>(2000, mode, out, cyc); cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
         printf("calib copy mode %d: %.1f\n", mode, double(h) / 2000);
+    }
+    {
+        unsigned long long* big; const long long n = 2ll * 65536 * 128;
+        cudaMalloc(&big, n * 8);
+        for (int raw = 0; raw < 2; ++raw)
+        for (int th : {256, 320, 512}) {
+            cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+            if (raw) k_fill<true><<<1, th>>>(n, big); else k_fill<false><<<1, th>>>(n, big);
+            cudaEventRecord(a);
+            if (raw) k_fill<true><<<1, th>>>(n, big); else k_fill<false><<<1, th>>>(n, big);
+            cudaEventRecord(b); cudaEventSynchronize(b);
+            float ms; cudaEventElapsedTime(&ms, a, b);
+            printf("fill raw=%d %lld words, %d threads: %.2f ms (%.0f cycles/pass at 1.965 GHz)\n", raw, n, th, ms, ms * 1.965e6 / (n / 624.0));
+        }
+        cudaFree(big);
     }
     for (int mode = 0; mode < 2; ++mode)
     for (int gs : {128, 256, 512, 1024}) {
