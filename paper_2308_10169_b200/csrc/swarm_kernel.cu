@@ -442,46 +442,27 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
                 // tracked.  Lane i holds window value i (oldest first); the sums
                 // stay sequential in that order, as in the reference.  The exact
                 // pre-test (std >= range / sqrt(2 tw)) skips hopeless windows.
-                if (p.auto_truncate && p.tw <= 32 && wl >= p.tw && tbq == 0) {
-                    int at = wh + lane;
-                    if (at >= p.tw) at -= p.tw;
-                    const double wv = lane < p.tw ? c.win[at] : 0.0;
-                    const double oldest = __shfl_sync(0xffffffffu, wv, 0);
-                    const double newest = __shfl_sync(0xffffffffu, wv, p.tw - 1);
+                // lane 0, sequentially in window order as in the reference; the
+                // exact pre-test (std >= range / sqrt(2 tw)) skips hopeless windows
+                if (p.auto_truncate && wl >= p.tw && tbq == 0 && lane == 0) {
+                    const double oldest = c.win[wh];
+                    const double newest = c.win[wh == 0 ? p.tw - 1 : wh - 1];
                     if (!(fabs(newest - oldest) >= p.at_gap)) {
                         double mean = 0.0;
-#pragma unroll 4
-                        for (int i = 0; i < 32; ++i) {
-                            const double vi = __shfl_sync(0xffffffffu, wv, i);
-                            if (i < p.tw) mean = __dadd_rn(mean, vi);
+                        for (int i = 0, at = wh; i < p.tw; ++i) {
+                            mean = __dadd_rn(mean, c.win[at]);
+                            if (++at == p.tw) at = 0;
                         }
                         mean = __ddiv_rn(mean, double(p.tw));
-                        const double dv = __dsub_rn(wv, mean);
-                        const double sq = __dmul_rn(dv, dv);
                         double var = 0.0;
-#pragma unroll 4
-                        for (int i = 0; i < 32; ++i) {
-                            const double si = __shfl_sync(0xffffffffu, sq, i);
-                            if (i < p.tw) var = __dadd_rn(var, si);
+                        for (int i = 0, at = wh; i < p.tw; ++i) {
+                            const double dv = __dsub_rn(c.win[at], mean);
+                            var = __dadd_rn(var, __dmul_rn(dv, dv));
+                            if (++at == p.tw) at = 0;
                         }
                         var = __ddiv_rn(var, double(p.tw));
-                        if (lane == 0 && __dsqrt_rn(var) < p.delta) { m->truncated = 1; m->stop = 1; }
+                        if (__dsqrt_rn(var) < p.delta) { m->truncated = 1; m->stop = 1; }
                     }
-                } else if (p.auto_truncate && p.tw > 32 && wl >= p.tw && tbq == 0 && lane == 0) {
-                    double mean = 0.0;
-                    for (int i = 0, at = wh; i < p.tw; ++i) {
-                        mean = __dadd_rn(mean, c.win[at]);
-                        if (++at == p.tw) at = 0;
-                    }
-                    mean = __ddiv_rn(mean, double(p.tw));
-                    double var = 0.0;
-                    for (int i = 0, at = wh; i < p.tw; ++i) {
-                        const double dv = __dsub_rn(c.win[at], mean);
-                        var = __dadd_rn(var, __dmul_rn(dv, dv));
-                        if (++at == p.tw) at = 0;
-                    }
-                    var = __ddiv_rn(var, double(p.tw));
-                    if (__dsqrt_rn(var) < p.delta) { m->truncated = 1; m->stop = 1; }
                 }
             }
             if (lane == 0) m->k_done = k;
