@@ -422,7 +422,7 @@ def main():
             },
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": 2 * K,
+            "gpu_launches": K,                        # one fused launch per frame (world step included)
             "clocks": clk,
             "batched": extra,
             "config4": big,

@@ -1255,12 +1255,10 @@ int sf_scene_batch_run(sf_scene_batch* b, uint32_t frames) {
         p.has_prev = f == 0 ? nullptr : static_cast<const unsigned char*>(b->ones.p);
         p.best_x = static_cast<double*>(b->best.p) + size_t(f) * b->n * D;
         p.out = static_cast<SwarmOut*>(b->out.p) + size_t(f) * b->n;
+        p.off_vel = int(b->lay.off_vel);
+        p.step_dt = b->dt;                       // the world step rides on the planning launch
         int st = launch_fused(ctx, b->fp, kPath);
         if (st) return st;
-        const int e = launch_step_worlds(static_cast<unsigned char*>(b->worlds.p), int(b->n), (long long)b->lay.stride,
-                                         int(b->lay.off_offsets), int(b->lay.off_verts), int(b->lay.off_vel), b->dt,
-                                         ctx->stream);
-        if (e) return cuda_fail(cudaError_t(e), "step_worlds");
     }
     b->frames_done += frames;
     return SF_OK;

@@ -89,6 +89,9 @@ struct ElemWalk {
     }
 };
 
+__device__ void step_world_part(unsigned char* rec, int off_offsets, int off_verts, int off_vel, double dt,
+                                int t);
+
 template <class T, bool PATH>
 __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ SwarmParams p,
                                                         int problem) {
@@ -584,6 +587,12 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
                 p.win_vals[size_t(swarm) * p.tw + i] = c.win[(c.m->win_head + i) % p.tw];
         if (tid == 0 && p.carry) p.win_len[swarm] = c.m->win_len;
     }
+    // scene batches: advance this swarm's world record for the next frame
+    // (simenv.hpp:155-184); every CTA staged it long ago
+    if (PATH && p.step_dt != 0.0 && c.crank == 0)
+        for (int t = tid - 2; t < c.O; t += nthr)
+            step_world_part(const_cast<unsigned char*>(p.worlds) + size_t(swarm) * size_t(p.world_stride),
+                            p.off_offsets, p.off_verts, p.off_vel, p.step_dt, t);
     SEPSO_GMARK(10);
     cluster.sync();   // no CTA leaves while a peer may still read its shared memory
     SEPSO_GMARK(11);
@@ -646,46 +655,55 @@ __device__ __forceinline__ double reflect_axis_dev(double lo, double hi, double 
     return 0.0;
 }
 
-// simenv.hpp:155-184, one thread per world record
-__global__ void k_step_worlds(unsigned char* worlds, int n, long long stride, int off_offsets,
-                              int off_verts, int off_vel, double dt) {
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= n) return;
-    unsigned char* rec = worlds + size_t(s) * size_t(stride);
+// simenv.hpp:155-184 for one world record, one part per thread: t = -2 the
+// start, t = -1 the target, t >= 0 obstacle t (obstacles move independently;
+// each part keeps the reference's operation order)
+__device__ void step_world_part(unsigned char* rec, int off_offsets, int off_verts, int off_vel, double dt,
+                                int t) {
     WorldHeader* h = reinterpret_cast<WorldHeader*>(rec);
-    const uint32_t* off = reinterpret_cast<const uint32_t*>(rec + off_offsets);
-    double* vv = reinterpret_cast<double*>(rec + off_verts);
-    double* vel = reinterpret_cast<double*>(rec + off_vel);
-    auto move = [&](double& px, double& py, double& vx, double& vy) {
+    if (t < 0) {
+        double& px = t == -2 ? h->sx : h->tx;
+        double& py = t == -2 ? h->sy : h->ty;
+        double& vx = t == -2 ? h->svx : h->tvx;
+        double& vy = t == -2 ? h->svy : h->tvy;
         px = __dadd_rn(px, __dmul_rn(vx, dt));
         py = __dadd_rn(py, __dmul_rn(vy, dt));
         px = __dadd_rn(px, reflect_axis_dev(px, px, h->width, vx));
         py = __dadd_rn(py, reflect_axis_dev(py, py, h->height, vy));
-    };
-    move(h->sx, h->sy, h->svx, h->svy);
-    move(h->tx, h->ty, h->tvx, h->tvy);
-    for (uint32_t o = 0; o < h->n_obs; ++o) {
-        double& ovx = vel[2 * o];
-        double& ovy = vel[2 * o + 1];
-        if (ovx == 0.0 && ovy == 0.0) continue;
-        const uint32_t v0 = off[o], v1 = off[o + 1];
-        for (uint32_t i = v0; i < v1; ++i) {
-            vv[2 * i] = __dadd_rn(vv[2 * i], __dmul_rn(ovx, dt));
-            vv[2 * i + 1] = __dadd_rn(vv[2 * i + 1], __dmul_rn(ovy, dt));
-        }
-        double bx0 = vv[2 * v0], by0 = vv[2 * v0 + 1], bx1 = bx0, by1 = by0;
-        for (uint32_t i = v0; i < v1; ++i) {
-            bx0 = smin(bx0, vv[2 * i]); by0 = smin(by0, vv[2 * i + 1]);
-            bx1 = smax(bx1, vv[2 * i]); by1 = smax(by1, vv[2 * i + 1]);
-        }
-        const double sx = reflect_axis_dev(bx0, bx1, h->width, ovx);
-        const double sy = reflect_axis_dev(by0, by1, h->height, ovy);
-        if (sx != 0.0 || sy != 0.0)
-            for (uint32_t i = v0; i < v1; ++i) {
-                vv[2 * i] = __dadd_rn(vv[2 * i], sx);
-                vv[2 * i + 1] = __dadd_rn(vv[2 * i + 1], sy);
-            }
+        return;
     }
+    const uint32_t* off = reinterpret_cast<const uint32_t*>(rec + off_offsets);
+    double* vv = reinterpret_cast<double*>(rec + off_verts);
+    double* vel = reinterpret_cast<double*>(rec + off_vel);
+    double& ovx = vel[2 * t];
+    double& ovy = vel[2 * t + 1];
+    if (ovx == 0.0 && ovy == 0.0) return;
+    const uint32_t v0 = off[t], v1 = off[t + 1];
+    for (uint32_t i = v0; i < v1; ++i) {
+        vv[2 * i] = __dadd_rn(vv[2 * i], __dmul_rn(ovx, dt));
+        vv[2 * i + 1] = __dadd_rn(vv[2 * i + 1], __dmul_rn(ovy, dt));
+    }
+    double bx0 = vv[2 * v0], by0 = vv[2 * v0 + 1], bx1 = bx0, by1 = by0;
+    for (uint32_t i = v0; i < v1; ++i) {
+        bx0 = smin(bx0, vv[2 * i]); by0 = smin(by0, vv[2 * i + 1]);
+        bx1 = smax(bx1, vv[2 * i]); by1 = smax(by1, vv[2 * i + 1]);
+    }
+    const double sx = reflect_axis_dev(bx0, bx1, h->width, ovx);
+    const double sy = reflect_axis_dev(by0, by1, h->height, ovy);
+    if (sx != 0.0 || sy != 0.0)
+        for (uint32_t i = v0; i < v1; ++i) {
+            vv[2 * i] = __dadd_rn(vv[2 * i], sx);
+            vv[2 * i + 1] = __dadd_rn(vv[2 * i + 1], sy);
+        }
+}
+
+// one CTA per world record, one thread per part
+__global__ void k_step_worlds(unsigned char* worlds, int n, long long stride, int off_offsets,
+                              int off_verts, int off_vel, double dt) {
+    if (int(blockIdx.x) >= n) return;
+    unsigned char* rec = worlds + size_t(blockIdx.x) * size_t(stride);
+    const int nobs = int(reinterpret_cast<const WorldHeader*>(rec)->n_obs);
+    for (int t = int(threadIdx.x) - 2; t < nobs; t += blockDim.x) step_world_part(rec, off_offsets, off_verts, off_vel, dt, t);
 }
 
 int launch_step_worlds(unsigned char* worlds, int n, long long stride, int off_offsets,
@@ -696,7 +714,7 @@ int launch_step_worlds(unsigned char* worlds, int n, long long stride, int off_o
         cudaFuncSetAttribute(k_step_worlds, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         carve = true;
     }
-    k_step_worlds<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+    k_step_worlds<<<n, 128, 0, static_cast<cudaStream_t>(stream)>>>(
         worlds, n, stride, off_offsets, off_verts, off_vel, dt);
     return int(cudaGetLastError());
 }

@@ -77,7 +77,8 @@ struct SwarmParams {
     // (rng.hpp:52-59) with tag_hash = fnv1a64(tag)
     const unsigned long long* roots; unsigned long long tag_hash; int frame_index;
     const unsigned char* worlds; long long world_stride; int max_obs, max_verts;
-    int off_offsets, off_verts;
+    int off_offsets, off_verts, off_vel;
+    double step_dt;          // scene batches: advance the world record by dt after planning (0: off)
     const double* prev; const unsigned char* has_prev;  // per swarm: D values + flag
     const double* lo; const double* hi;                 // benchmark box (D); path: from world
     // window state (per swarm: tw values oldest..newest, effective length)

@@ -1,0 +1,59 @@
+"""Device-resident scenarios (sf_scene_batch_*): every frame is one fused
+planning launch that also advances the world record on the device
+(simenv.hpp:155-184), with derive_seed(root, "plan", f) computed on the device.
+The FP64 engine with the reference's mt19937_64 stream must reproduce the
+UNMODIFIED reference scenario (golden vectors) and the host-driven
+run_scenario (simenv.hpp:239-276) frame by frame."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2308_10169_b200 as pe
+
+pytestmark = pytest.mark.gpu
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "reference_vectors.json")))
+PLANNER = pe.PlannerConfig(max_iters_per_frame=30, window_carryover=True)
+
+
+def test_scene_batch_fp64_equals_reference_scenario(eng64mt):
+    sb = pe.SceneBatch(eng64mt, [pe.ScenarioConfig(root_seed=3)], PLANNER, pe.EVOLVED_PATH_HYPERS, 100)
+    sb.run(100)
+    recs, _ = sb.records(0, 100)
+    sb.close()
+    s = GOLD["scenario_seed3"]
+    assert [r.iterations for r in recs] == s["iterations"]
+    assert sum(r.truncated for r in recs) == s["truncated"]
+    assert abs(np.mean([r.length for r in recs]) - s["mean_length"]) < 1e-9
+
+
+def test_scene_batch_equals_host_run_scenario(eng64mt):
+    roots = [3, 17, 40]
+    frames = 12
+    sb = pe.SceneBatch(eng64mt, [pe.ScenarioConfig(root_seed=r) for r in roots], PLANNER,
+                       pe.EVOLVED_PATH_HYPERS, frames)
+    sb.run(5)
+    sb.run(frames - 5)                      # frames in two calls: state carries over
+    recs, best = sb.records(0, frames, with_best=True)
+    sb.close()
+    for i, root in enumerate(roots):
+        host = eng64mt.run_scenario(pe.ScenarioConfig(root_seed=root), "sepso", frames, PLANNER)
+        for f in range(frames):
+            d, h = recs[f * len(roots) + i], host[f]
+            assert (d.iterations, d.truncated, d.intersections) == (h.iterations, h.truncated, h.intersections)
+            assert d.fitness == h.fitness and d.length == h.length
+            assert np.array_equal(best[f, i], pe.encode_path(h.best_path) if np.ndim(h.best_path) == 2
+                                  else np.asarray(h.best_path))
+
+
+def test_scene_batch_fp32_statistics(eng32mt):
+    sb = pe.SceneBatch(eng32mt, [pe.ScenarioConfig(root_seed=3)], PLANNER, pe.EVOLVED_PATH_HYPERS, 100)
+    sb.run(100)
+    recs, _ = sb.records(0, 100)
+    sb.close()
+    s = GOLD["scenario_seed3"]
+    assert abs(np.mean([r.iterations for r in recs]) - s["mean_iterations"]) < 1.5
+    assert abs(np.mean([r.length for r in recs]) - s["mean_length"]) < 0.02 * s["mean_length"]
+    assert sum(r.collision_free for r in recs) >= 90
