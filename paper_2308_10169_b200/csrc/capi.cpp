@@ -226,17 +226,17 @@ int run_batch(sf_ctx* ctx, const BatchIn& b, BatchOut& r) {
     p.hi = reinterpret_cast<const double*>(d + io.hi);
     p.win_vals = reinterpret_cast<double*>(d + io.win);
     p.win_len = reinterpret_cast<int*>(d + io.win_len);
-    p.out = reinterpret_cast<SwarmOut*>(d + io.out);
-    p.best_x = reinterpret_cast<double*>(d + io.best);
-    p.trace = reinterpret_cast<double*>(d + io.trace);
+    // results go straight to the pinned block (mapped into the device address
+    // space under UVA): the kernel's stores cross the bus, no D2H copy follows
+    p.out = reinterpret_cast<SwarmOut*>(h + io.out);
+    p.best_x = reinterpret_cast<double*>(h + io.best);
+    p.trace = reinterpret_cast<double*>(h + io.trace);
     cudaError_t ce = cudaMemcpyAsync(d, h, io.out, cudaMemcpyHostToDevice, ctx->stream);
     if (ce != cudaSuccess) return cuda_fail(ce, "H2D io");
     ctx->last_h2d = io.out;
     ctx->last_d2h = io.end - io.out;
     st = launch_fused(ctx, fp, b.problem);
     if (st != SF_OK) return st;
-    ce = cudaMemcpyAsync(h + io.out, d + io.out, io.end - io.out, cudaMemcpyDeviceToHost, ctx->stream);
-    if (ce != cudaSuccess) return cuda_fail(ce, "D2H io");
     ce = cudaStreamSynchronize(ctx->stream);
     if (ce != cudaSuccess) return cuda_fail(ce, "swarm kernel");
     std::memcpy(r.out.data(), h + io.out, size_t(b.n) * sizeof(SwarmOut));
