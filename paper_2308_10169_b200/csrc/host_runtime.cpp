@@ -220,7 +220,9 @@ FusedPlan plan_fused(sf_ctx* ctx, int problem, int n_swarms, int G, int N, int D
         if (path) {
             // worst case Rc*S*O entries; beyond the capacity entries are evaluated in place
             p.entry_cap = 0;   // overlapping obstacles are evaluated in place (no work list)
-            p.nthreads = std::min(1024, std::max(128, ((Rc * S) + 31) / 32 * 32));
+            // one thread per (particle, segment) item; latency launches add four
+            // warps (containment tasks, the stream generator) -- measured best
+            p.nthreads = std::min(1024, std::max(128, ((Rc * S) + 31) / 32 * 32 + (latency ? 128 : 0)));
         } else {
             p.entry_cap = 0;
             p.nthreads = std::min(512, std::max(32, (Rc + 31) / 32 * 32));
