@@ -204,7 +204,9 @@ FusedPlan plan_fused(sf_ctx* ctx, int problem, int n_swarms, int G, int N, int D
     // latency mode (few swarms): spread one swarm over up to 16 SMs (~96 rows per
     // CTA); throughput mode (many swarms): ~384 rows per CTA, fewer cluster syncs
     const bool latency = n_swarms * 16 <= 2 * 148;
-    const int rows_target = latency ? 85 : 384;
+    // throughput: ~680 rows per CTA (a paper swarm on 2 CTAs), measured best
+    // for config 5 (tools/sweep_batch.py)
+    const int rows_target = latency ? 85 : 680;
     int C = want_c > 0 ? want_c : std::max(1, std::min(16, (R + rows_target - 1) / rows_target));
     for (;; C *= 2) {
         if (C > 16) C = 16;
