@@ -333,6 +333,34 @@ def main():
                  "plans_per_s": 3 * nb * ws / (dist.max(ms) / 1e3),
                  "mean_iterations": float(np.mean([r.iterations for r in rb]))}
 
+    # ------------------------------------------------------------ extra: Philox stream
+    # the same frames with the counter-based Philox stream (north star RNG; the
+    # harness build of the reference draws it): different draws, different
+    # truncation points, so a different iteration count per frame
+    phil = None
+    if a.workload == "scene" and not a.no_extra:
+        engp = pe.Engine(local, a.precision, "philox")
+        sp = pe.SceneBatch(engp, scen, planner, pe.EVOLVED_PATH_HYPERS, W + K)
+        sp.run(W)
+        engp.synchronize()
+        streamp = torch.cuda.ExternalStream(engp.stream, device=torch.device("cuda", local))
+        evp = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        with torch.cuda.stream(streamp):
+            for i in range(K):
+                flush.zero_()
+                evp[i][0].record(streamp)
+                sp.run(1)
+                evp[i][1].record(streamp)
+        torch.cuda.synchronize()
+        engp.synchronize()
+        msp = dist.max(float(np.sum([e0.elapsed_time(e1) for e0, e1 in evp])))
+        rp, _ = sp.records(W, K)
+        sp.close()
+        engp.close()
+        phil = {"workload": "config2 frames as the headline, Philox4x32-10 counter stream",
+                "plans_per_s": K * n_sc * ws / (msp / 1e3),
+                "mean_iterations_per_frame": float(np.mean([r.iterations for r in rp]))}
+
     # ------------------------------------------------------------ extra: config 4
     # one 65,536-particle swarm (G=8 x N=8192, D=128, 1,024 obstacles), one frame
     # capped at 3 iterations: the HBM-staged path (K1 update + wide K2 fitness)
@@ -426,6 +454,7 @@ def main():
             "clocks": clk,
             "batched": extra,
             "config4": big,
+            "philox": phil,
             "host_threads": cpu_thr,
         }
         print(json.dumps(line), flush=True)
