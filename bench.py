@@ -155,6 +155,30 @@ def cpu_reference_scene(frames: int, skip: int, root_seed: int = 3):
             "frames": len(timed)}
 
 
+def cpu_reference_13():
+    """Single-thread reference samples: one BF3 trial (G=8 N=10 T=1400, D=30) and
+    one HSEF inner run (lfv_fitness, 8x170x30 on the frame-0 paper world) x 80
+    candidates per evolution (hsef.hpp:125-171; the outer update is negligible)."""
+    import ctypes as C
+    from oracle_lib import ref, ptr, DEFAULT_GROUP_HYPERS, generate_world
+    r = ref("mt")
+    if r is None:
+        return None
+    trace, fp, ff = np.zeros(1400), np.zeros(30), C.c_double(0)
+    bad = (C.c_size_t * 3)()
+    t0 = time.perf_counter()
+    st = r.ref_run_dtpso(3, None, 30, 30.0, 4.0, ptr(np.ascontiguousarray(DEFAULT_GROUP_HYPERS)), 8, 10, 1400, 7,
+                         ptr(trace), ptr(fp), C.byref(ff), bad)
+    t1 = time.perf_counter()
+    assert st == 0
+    w = generate_world("mt", _derive(3, "world"))
+    cand = np.ascontiguousarray(np.tile([1.5, 1.5, 1.5, 0.9, 0.4, 0.2], 8), dtype=np.float64)
+    t2 = time.perf_counter()
+    r.ref_lfv_fitness(ptr(cand), 8, 0, C.byref(w.struct()), 16, 30.0, 4.0, 8, 170, 30, 11)
+    t3 = time.perf_counter()
+    return {"trials_per_s": 1.0 / (t1 - t0), "ms_per_evolution": 80 * (t3 - t2) * 1e3}
+
+
 def cpu_reference_batched(n_scenes: int, seconds: float = 15.0):
     """Config 5 on the host: independent cold plans (frame 0 of scenes
     0..n-1, the first frame of each scenario) on all host threads."""
@@ -392,6 +416,33 @@ def main():
                             "frac": fl4 / (ms4 / it4 / 1e3) / 1e12 / peak if peak else None,
                             "flop_per_eval": FLOP_PER_EVAL(S4, E4)}}
 
+    # ------------------------------------------------------------ extras: configs 1 and 3
+    # config 1: 1,024 BF3 (Rastrigin) trials of G=8 x N=10 x T=1400, D=30, one
+    # batched launch through the public API (host buffers in and out);
+    # config 3: HSEF evolutions (80 inner paper swarms x 30 iterations each) on
+    # the frozen frame-0 paper world, inner (8,170,30), outer (8,10,3)
+    c13 = None
+    if a.workload == "scene" and not a.no_extra and rank == 0:
+        seeds1 = np.arange(1, 1025, dtype=np.uint64)
+        eng.run_dtpso_batched("BF3", pe.DEFAULT_GROUP_HYPERS, 8, 10, 1400, seeds1[:64])
+        t0 = time.perf_counter()
+        eng.run_dtpso_batched("BF3", pe.DEFAULT_GROUP_HYPERS, 8, 10, 1400, seeds1)
+        t1 = time.perf_counter()
+        w3 = pe.generate_world(pe.ScenarioConfig(root_seed=3), _derive(3, "world"))
+        eng.evolve("path", (8, 170, 30), (8, 10, 1), 40, world=w3, dim=16)
+        t2 = time.perf_counter()
+        eng.evolve("path", (8, 170, 30), (8, 10, 3), 41, world=w3, dim=16)
+        t3 = time.perf_counter()
+        c13 = {"config1": {"workload": "1,024 BF3 trials, G=8 N=10 T=1400 D=30 (one batched call, wall)",
+                           "trials_per_s": 1024 / (t1 - t0), "evals_per_s": 1024 * 80 * 1400 / (t1 - t0)},
+               "config3": {"workload": "HSEF evolve, inner (8,170,30) path on the frame-0 paper world, outer (8,10,3)",
+                           "ms_per_evolution": (t3 - t2) / 3 * 1e3,
+                           "inner_evals_per_s": 3 * 80 * 1360 * 30 / (t3 - t2)}}
+        ref13 = cpu_reference_13() if not a.no_cpu_baseline else None
+        if ref13:
+            c13["config1"]["reference_1thread_trials_per_s"] = ref13["trials_per_s"]
+            c13["config3"]["reference_1thread_ms_per_evolution"] = ref13["ms_per_evolution"]
+
     # ------------------------------------------------------------ CPU baseline
     cpu = None
     if rank == 0 and not a.no_cpu_baseline:
@@ -455,6 +506,7 @@ def main():
             "batched": extra,
             "config4": big,
             "philox": phil,
+            "configs_1_3": c13,
             "host_threads": cpu_thr,
         }
         print(json.dumps(line), flush=True)
