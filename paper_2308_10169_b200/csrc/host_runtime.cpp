@@ -200,13 +200,14 @@ FusedPlan plan_fused(sf_ctx* ctx, int problem, int n_swarms, int G, int N, int D
     p.max_verts = path ? std::max(max_verts, 3) : 0;
     const int want_c = ctx->force_cluster ? ctx->force_cluster : env_int("SEPSO_CLUSTER", 0);
     const int want_t = ctx->force_threads ? ctx->force_threads : env_int("SEPSO_THREADS", 0);
-    // latency-oriented default: ~192 particle rows per CTA, up to 16 CTAs per cluster
-    // latency mode (few swarms): spread one swarm over up to 16 SMs (~96 rows per
-    // CTA); throughput mode (many swarms): ~384 rows per CTA, fewer cluster syncs
+    // Launch shapes (measured, tools/sweep*.py):
+    //  latency (few swarms): one swarm over up to 16 SMs, ~85 rows per CTA;
+    //  medium (up to one swarm per SM, e.g. HSEF's 80 inner swarms): ~340 rows per
+    //    CTA, 512 threads, two CTAs per SM;
+    //  throughput (many swarms, config 5): ~680 rows per CTA, 1024 threads.
     const bool latency = n_swarms * 16 <= 2 * 148;
-    // throughput: ~680 rows per CTA (a paper swarm on 2 CTAs), measured best
-    // for config 5 (tools/sweep_batch.py)
-    const int rows_target = latency ? 85 : 680;
+    const bool medium = !latency && n_swarms <= 148;
+    const int rows_target = latency ? 85 : (medium ? 340 : 680);
     int C = want_c > 0 ? want_c : std::max(1, std::min(16, (R + rows_target - 1) / rows_target));
     for (;; C *= 2) {
         if (C > 16) C = 16;
@@ -224,7 +225,7 @@ FusedPlan plan_fused(sf_ctx* ctx, int problem, int n_swarms, int G, int N, int D
             p.entry_cap = 0;   // overlapping obstacles are evaluated in place (no work list)
             // one thread per (particle, segment) item; latency launches add four
             // warps (containment tasks, the stream generator) -- measured best
-            p.nthreads = std::min(1024, std::max(128, ((Rc * S) + 31) / 32 * 32 + (latency ? 128 : 0)));
+            p.nthreads = std::min(medium ? 512 : 1024, std::max(128, ((Rc * S) + 31) / 32 * 32 + (latency ? 128 : 0)));
         } else {
             p.entry_cap = 0;
             p.nthreads = std::min(512, std::max(32, (Rc + 31) / 32 * 32));
