@@ -228,7 +228,9 @@ FusedPlan plan_fused(sf_ctx* ctx, int problem, int n_swarms, int G, int N, int D
             p.nthreads = std::min(medium ? 512 : 1024, std::max(128, ((Rc * S) + 31) / 32 * 32 + (latency ? 128 : 0)));
         } else {
             p.entry_cap = 0;
-            p.nthreads = std::min(512, std::max(32, (Rc + 31) / 32 * 32));
+            // benchmarks: a thread per row for the fitness, at least 256 for the
+            // step's Rc*D elements (config 1, 80-row swarms: measured best)
+            p.nthreads = std::min(512, std::max(256, (Rc + 31) / 32 * 32));
         }
         if (want_t > 0) p.nthreads = std::min(1024, std::max(32, want_t / 32 * 32));
         p.rng = ctx->rng;
