@@ -460,7 +460,6 @@ int stage_eval_path(bool fp64, const unsigned char* world, int max_obs, int max_
     pp.alpha = alpha;
     pp.beta = beta;
     pp.beta_int = (beta == double(int(beta)) && beta >= 1.0 && beta <= 64.0) ? int(beta) : 0;
-    const int S = D / 2 + 1;
     if (max_obs >= 48) {   // wide worlds: lanes over obstacles
         const int rows_tile = 64;
         pp.entry_cap = 0;
