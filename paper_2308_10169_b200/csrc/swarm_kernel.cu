@@ -281,6 +281,19 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
         SEPSO_MARK(4);
         // pbest (runner.hpp:73-80) incl. the x -> pbest_x row copy; non-finite
         // detection (runner.hpp:56-61).  Same thread owns fit[pl] (A3 above).
+        // mt19937: the last four warps walk the stream to this step's r1, r2, r3
+        // (draw_step_randoms, swarm.hpp:59-70).  When they own no pbest rows and
+        // no group partial they start right after the fitness barrier, outside
+        // the pbest barrier.
+        const bool gen_early = p.rng == kMt19937 && k < p.cap && nthr >= 192;
+        const int gw0 = (nthr >> 5) - 4;
+        const bool gen_first = gen_early && gw0 * 32 >= c.P && c.LG <= gw0;
+        if (gen_first && warp >= gw0) {
+            long long* gprof = (kProfiling && p.prof != nullptr && swarm == 0 && c.crank == 0 && tid == gw0 * 32) ? p.prof : nullptr;
+            if (gprof) gprof[(k - 1) * kProfPhases + 12] = clock64();
+            mt_step_draws<128>(c, mtbuf, MtGroup{tid - gw0 * 32, 128, 1}, k, row1);
+            if (gprof) gprof[(k - 1) * kProfPhases + 13] = clock64();
+        } else {
         for (int pl = tid; pl < c.P; pl += nthr) {
             const T f = c.fit[pl];
             if (!isfinite(f)) atomicMin(&c.m->bad_row, c.row0 + pl);
@@ -298,7 +311,9 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
             }
             if (PATH) c.q[pl] = 0;
         }
-        __syncthreads();
+        if (gen_first) asm volatile("bar.sync 2, %0;" ::"r"(gw0 * 32) : "memory");   // pbest done (not the generator)
+        else __syncthreads();
+        }
         SEPSO_MARK(5);
         if (tid == 0) mbar_expect(mbar0 + 8 * buf, xbytes);
         if (k == 1) cluster_wait();       // every peer is running, its mbarriers initialised
@@ -360,14 +375,10 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
             st_async_b32(peer_addr(smem_addr(c.allbad + buf * c.C + c.crank), tid), uint32_t(c.m->bad_row),
                          peer_addr(mbar0 + 8 * buf, tid));
         SEPSO_MARK(6);
-        // Partials of every CTA visible cluster-wide (barrier.cluster arrive +
-        // wait).  With the mt19937 stream the last four warps arrive early and
-        // walk the stream to this step's r1, r2, r3 (draw_step_randoms,
-        // swarm.hpp:59-70) while the cluster synchronises and warp 0 updates
-        // the bests; the factors are read after the barrier that follows B1.
-        const bool gen_early = p.rng == kMt19937 && k < p.cap && nthr >= 192;
-        const int gw0 = (nthr >> 5) - 4;
-        if (gen_early && warp >= gw0) {
+        // otherwise the last four warps generate while the partials arrive and
+        // warp 0 updates the bests; the factors are read after the barrier that
+        // follows B1
+        if (gen_early && !gen_first && warp >= gw0) {
             long long* gprof = (kProfiling && p.prof != nullptr && swarm == 0 && c.crank == 0 && tid == gw0 * 32) ? p.prof : nullptr;
             if (gprof) gprof[(k - 1) * kProfPhases + 12] = clock64();
             mt_step_draws<128>(c, mtbuf, MtGroup{tid - gw0 * 32, 128, 1}, k, row1);
