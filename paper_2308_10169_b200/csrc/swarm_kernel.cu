@@ -3,6 +3,7 @@
 // See swarm_kernel.cuh for the execution model.  Reference citations are
 // relative to proj/include/swarmforge/ in the reference tree.
 #include <cooperative_groups.h>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "mt19937.cuh"
@@ -525,8 +526,45 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
         // rows; the first local particle of each group (and particle 0 for tbest)
         // persists them for the next iteration.  Readers of gbx / tbx only read
         // when the entry did not change, so the in-loop writes cannot race.
-        {
-            const T frac = T(double(k) / double(p.cap));           // inertia_at (swarm.hpp:81-84)
+        const T frac = T(double(k) / double(p.cap));               // inertia_at (swarm.hpp:81-84)
+        if ((D & 1) == 0) {
+            // two elements of one row per thread: the row's factors, weights and
+            // best slots are loaded once, x / v / pbest as 2-vectors
+            using V2 = typename std::conditional<sizeof(T) == 4, float2, double2>::type;
+            for (int i = tid; i < (c.P * D) >> 1; i += nthr) {
+                const int e = 2 * i, pl = int(c.fD.div(uint32_t(e))), d = e - pl * D;
+                const int row = c.row0 + pl, g = int(c.fN.div(uint32_t(row)));
+                const T* h = c.hyp + g * 6;
+                const T wt = A::sub(h[3], A::mul(A::sub(h[3], h[4]), frac));
+                const int gslot = c.chg[g];
+                const T a1 = c.coef[pl], a2 = c.coef[c.P + pl], a3 = c.coef[2 * c.P + pl];
+                const V2 xv = *reinterpret_cast<const V2*>(c.x + e);
+                const V2 vv = *reinterpret_cast<const V2*>(c.v + e);
+                const V2 pv = *reinterpret_cast<const V2*>(c.pb + e);
+                const T xs[2] = {xv.x, xv.y}, vs[2] = {vv.x, vv.y}, ps[2] = {pv.x, pv.y};
+                T xo[2], vo[2];
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int dd = d + j;
+                    const T lo = c.lo[dd], hi = c.hi[dd];
+                    const T vmax = A::mul(h[5], A::sub(hi, lo));
+                    const T gv = gslot >= 0 ? pxb[gslot * D + dd] : c.gbx[g * D + dd];
+                    const T tv = tslot >= 0 ? pxb[tslot * D + dd] : c.tbx[dd];
+                    if (gslot >= 0 && row == max(g * N, c.row0)) c.gbx[g * D + dd] = gv;
+                    if (tslot >= 0 && pl == 0) c.tbx[dd] = tv;
+                    T nv = A::add(A::add(A::add(A::mul(wt, vs[j]), A::mul(a1, A::sub(ps[j], xs[j]))),
+                                         A::mul(a2, A::sub(gv, xs[j]))),
+                                  A::mul(a3, A::sub(tv, xs[j])));
+                    nv = clampT(nv, T(-vmax), vmax);
+                    vo[j] = nv;
+                    xo[j] = clampT(A::add(xs[j], nv), lo, hi);
+                }
+                V2 vn, xn;
+                vn.x = vo[0]; vn.y = vo[1]; xn.x = xo[0]; xn.y = xo[1];
+                *reinterpret_cast<V2*>(c.v + e) = vn;
+                *reinterpret_cast<V2*>(c.x + e) = xn;
+            }
+        } else {
             ElemWalk w(c.fD, tid, nthr, D);
             int g = int(c.fN.div(uint32_t(c.row0 + w.pl)));
             for (int e = tid; e < c.P * D; e += nthr, w.next()) {
