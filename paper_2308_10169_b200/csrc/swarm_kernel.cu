@@ -93,6 +93,11 @@ struct ElemWalk {
 __device__ void step_world_part(unsigned char* rec, int off_offsets, int off_verts, int off_vel, double dt,
                                 int t);
 
+#ifndef SEPSO_STEPW
+#define SEPSO_STEPW 4
+#endif
+constexpr int STEPW = SEPSO_STEPW;
+
 template <class T, bool PATH>
 __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ SwarmParams p,
                                                         int problem) {
@@ -527,24 +532,27 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
         // persists them for the next iteration.  Readers of gbx / tbx only read
         // when the entry did not change, so the in-loop writes cannot race.
         const T frac = T(double(k) / double(p.cap));               // inertia_at (swarm.hpp:81-84)
-        if ((D & 1) == 0) {
-            // two elements of one row per thread: the row's factors, weights and
-            // best slots are loaded once, x / v / pbest as 2-vectors
-            using V2 = typename std::conditional<sizeof(T) == 4, float2, double2>::type;
-            for (int i = tid; i < (c.P * D) >> 1; i += nthr) {
-                const int e = 2 * i, pl = int(c.fD.div(uint32_t(e))), d = e - pl * D;
+        auto step_rows = [&](auto width) {
+            // WIDTH elements of one row per thread: the row's factors, weights and
+            // best slots are loaded once, x / v / pbest as WIDTH-vectors
+            constexpr int WIDTH = decltype(width)::value;
+            using VW = typename std::conditional<WIDTH == 4, float4,
+                       typename std::conditional<sizeof(T) == 4, float2, double2>::type>::type;
+            for (int i = tid; i < (c.P * D) / WIDTH; i += nthr) {
+                const int e = WIDTH * i, pl = int(c.fD.div(uint32_t(e))), d = e - pl * D;
                 const int row = c.row0 + pl, g = int(c.fN.div(uint32_t(row)));
                 const T* h = c.hyp + g * 6;
                 const T wt = A::sub(h[3], A::mul(A::sub(h[3], h[4]), frac));
                 const int gslot = c.chg[g];
                 const T a1 = c.coef[pl], a2 = c.coef[c.P + pl], a3 = c.coef[2 * c.P + pl];
-                const V2 xv = *reinterpret_cast<const V2*>(c.x + e);
-                const V2 vv = *reinterpret_cast<const V2*>(c.v + e);
-                const V2 pv = *reinterpret_cast<const V2*>(c.pb + e);
-                const T xs[2] = {xv.x, xv.y}, vs[2] = {vv.x, vv.y}, ps[2] = {pv.x, pv.y};
-                T xo[2], vo[2];
+                VW xv = *reinterpret_cast<const VW*>(c.x + e);
+                VW vv = *reinterpret_cast<const VW*>(c.v + e);
+                const VW pv = *reinterpret_cast<const VW*>(c.pb + e);
+                T* xs = reinterpret_cast<T*>(&xv);
+                T* vs = reinterpret_cast<T*>(&vv);
+                const T* ps = reinterpret_cast<const T*>(&pv);
 #pragma unroll
-                for (int j = 0; j < 2; ++j) {
+                for (int j = 0; j < WIDTH; ++j) {
                     const int dd = d + j;
                     const T lo = c.lo[dd], hi = c.hi[dd];
                     const T vmax = A::mul(h[5], A::sub(hi, lo));
@@ -556,14 +564,20 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
                                          A::mul(a2, A::sub(gv, xs[j]))),
                                   A::mul(a3, A::sub(tv, xs[j])));
                     nv = clampT(nv, T(-vmax), vmax);
-                    vo[j] = nv;
-                    xo[j] = clampT(A::add(xs[j], nv), lo, hi);
+                    vs[j] = nv;
+                    xs[j] = clampT(A::add(xs[j], nv), lo, hi);
                 }
-                V2 vn, xn;
-                vn.x = vo[0]; vn.y = vo[1]; xn.x = xo[0]; xn.y = xo[1];
-                *reinterpret_cast<V2*>(c.v + e) = vn;
-                *reinterpret_cast<V2*>(c.x + e) = xn;
+                *reinterpret_cast<VW*>(c.v + e) = vv;
+                *reinterpret_cast<VW*>(c.x + e) = xv;
             }
+        };
+        bool stepped = false;
+        if constexpr (sizeof(T) == 4 && STEPW == 4) {
+            if ((D & 3) == 0) { step_rows(std::integral_constant<int, 4>{}); stepped = true; }
+        }
+        if (stepped) {
+        } else if ((D & 1) == 0) {
+            step_rows(std::integral_constant<int, 2>{});
         } else {
             ElemWalk w(c.fD, tid, nthr, D);
             int g = int(c.fN.div(uint32_t(c.row0 + w.pl)));
