@@ -309,7 +309,8 @@ def main():
         e2e = {"value": K * ws / e2e_s, "unit": "plans/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h),
                "timing": "sum of PlanRecord.wall_seconds (host steady_clock around each sf_plan_frame call: "
-                         "validate + stage + H2D + kernel + D2H + sync), frames W..W+K-1",
+                         "validate + stage + H2D copy + kernel (results stored into pinned host memory) + sync), "
+                         "frames W..W+K-1",
                "whole_call_ms_events": e_0.elapsed_time(e_1),
                "mean_iterations_per_frame": float(np.mean([r.iterations for r in recs_e2e[W:]]))}
     else:
@@ -414,7 +415,10 @@ def main():
                "roofline": {"kernel": "k_eval_path_wide<float> + k_step (whole iteration)", "bound": "fp32",
                             "achieved": fl4 / (ms4 / it4 / 1e3) / 1e12, "peak": peak, "unit": "TFLOP/s",
                             "frac": fl4 / (ms4 / it4 / 1e3) / 1e12 / peak if peak else None,
-                            "flop_per_eval": FLOP_PER_EVAL(S4, E4)}}
+                            "flop_per_eval": FLOP_PER_EVAL(S4, E4),
+                            "note": "algorithmic count of SURVEY.md 8(d): every (segment, edge) pair; the map "
+                                    "grid and the box cull skip most pairs, so the rate can exceed the FFMA "
+                                    "peak -- kernel-quality evidence: profiles/r01_k_eval_path_wide_config4.md"}}
 
     # ------------------------------------------------------------ extras: configs 1 and 3
     # config 1: 1,024 BF3 (Rastrigin) trials of G=8 x N=10 x T=1400, D=30, one
