@@ -158,6 +158,7 @@ SEPSO_LHD SmemLayout smem_layout(const SwarmParams& p, size_t tsz, bool path) {
     L.vert = take(V * 2 * tsz);
     L.edge = take(V * 4 * tsz);
     L.list = take(path ? size_t(p.entry_cap) * 4 : 0);
+    o = (o + 127) & ~size_t(127);          // generator state on a 128-byte boundary
     L.mt = take(p.rng == 1 ? 4 * 312 * 8 : 0);
     L.total = o;
     return L;
