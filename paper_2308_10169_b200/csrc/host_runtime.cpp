@@ -253,7 +253,8 @@ int launch_fused(sf_ctx* ctx, FusedPlan& fp, int problem) {
         cudaMemsetAsync(prof, 0, sizeof(long long) * nprof, ctx->stream);
         fp.p.prof = prof;
     }
-    const int e = launch_swarms(fp.p, problem, ctx->precision == SF_FP64, ctx->stream, &smem);
+    const int e = launch_swarms(fp.p, fp.p.inl ? fp.payload : nullptr, problem, ctx->precision == SF_FP64,
+                                ctx->stream, &smem);
     if (prof) {
         std::vector<long long> h(size_t(kProfPhases) * (fp.p.cap + 1) + 2 * 16 * size_t(fp.p.cap));
         cudaMemcpyAsync(h.data(), prof, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream);

@@ -77,6 +77,7 @@ struct FusedPlan {
     SwarmParams p{};
     size_t smem = 0;
     bool fits = false;
+    const ParamPayload* payload = nullptr;   // inputs inline in the launch (p.inl)
 };
 // Pick cluster size / threads / list capacity for n swarms of shape (G, N, D).
 FusedPlan plan_fused(sf_ctx* ctx, int problem, int n_swarms, int G, int N, int D, int max_obs,

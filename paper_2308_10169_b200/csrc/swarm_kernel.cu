@@ -100,6 +100,7 @@ constexpr int STEPW = SEPSO_STEPW;
 
 template <class T, bool PATH>
 __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ SwarmParams p,
+                                                        const __grid_constant__ ParamPayload pl,
                                                         int problem) {
     using A = Ar<T>;
     cg::cluster_group cluster = cg::this_cluster();
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
     }
     const uint64_t seed =
         p.roots ? splitmix64(splitmix64(p.roots[swarm] ^ p.tag_hash) + uint64_t(p.frame_index))
-                : p.seeds[swarm];
+                : (p.inl ? reinterpret_cast<const unsigned long long*>(pl.bytes + p.in_seed) : p.seeds)[swarm];
     const int G = c.G, N = c.N, D = c.D, R = c.R;
     long long* const prof = (kProfiling && p.prof != nullptr && swarm == 0 && c.crank == 0 && tid == 0) ? p.prof : nullptr;
     // per-CTA (thread 0) work before the exchange: [(k * 16 + crank) * 2] = cycles, [+1] = wait
@@ -170,19 +171,23 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
     unsigned long long* const mtbuf = (unsigned long long*)S8(L.mt);
     const bool mt_on = p.rng == kMt19937;
     const int cw = (mt_on && nthr >= 64) ? nthr - 32 : nthr;
-    const unsigned char* wrec = PATH ? p.worlds + size_t(swarm) * size_t(p.world_stride) : nullptr;
+    const unsigned char* wrec =
+        PATH ? (p.inl ? pl.bytes + p.in_world : p.worlds) + size_t(swarm) * size_t(p.world_stride) : nullptr;
     c.O = 0;
     if (tid >= cw) {
         if (tid == cw) mt_seed_words(mtbuf + 312, seed);
         if (PATH) world_regs(c, wrec);
     } else {
-        const double* hyp_src = p.hypers + size_t(swarm) * size_t(p.hypers_stride);
+        const double* hyp_src = (p.inl ? reinterpret_cast<const double*>(pl.bytes + p.in_hyp) : p.hypers) +
+                                size_t(swarm) * size_t(p.hypers_stride);
         for (int i = tid; i < G * 6; i += cw) c.hyp[i] = T(hyp_src[i]);
         if (PATH) {
             world_regs(c, wrec);
             load_world(c, wrec, p.off_offsets, p.off_verts, tid, cw, cw == nthr ? 0 : 2);
         } else {
-            for (int d = tid; d < D; d += cw) { c.lo[d] = T(p.lo[d]); c.hi[d] = T(p.hi[d]); }
+            const double* lo_src = p.inl ? reinterpret_cast<const double*>(pl.bytes + p.in_lo) : p.lo;
+            const double* hi_src = p.inl ? reinterpret_cast<const double*>(pl.bytes + p.in_hi) : p.hi;
+            for (int d = tid; d < D; d += cw) { c.lo[d] = T(lo_src[d]); c.hi[d] = T(hi_src[d]); }
         }
         if (tid == 0) {
             Misc<T>* m = c.m;
@@ -190,13 +195,14 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
             m->status = 0; m->bad_row = INT_MAX; m->bad_min = INT_MAX; m->n_pair = 0; m->n_cont = 0;
             m->k_done = 0;
             m->cont_cap = 0;
-            const int wl = p.carry ? p.win_len[swarm] : 0;
+            const int wl = p.carry ? (p.inl ? reinterpret_cast<const int*>(pl.bytes + p.in_win_len) : p.win_len)[swarm] : 0;
             m->win_len = wl < p.tw ? wl : p.tw;
             m->win_head = 0;
             if (mt_on && cw == nthr) mt_seed_words(mtbuf + 312, seed);
         }
         if (p.carry)
-            for (int i = tid; i < p.tw; i += cw) c.win[i] = p.win_vals[size_t(swarm) * p.tw + i];
+            for (int i = tid; i < p.tw; i += cw)
+                c.win[i] = (p.inl ? reinterpret_cast<const double*>(pl.bytes + p.in_win) : p.win_vals)[size_t(swarm) * p.tw + i];
         for (int g = tid; g < G; g += cw) {
             c.gbf[g] = A::inf(); c.gbq[g] = 0; c.chg[g] = -1;
             c.gtab[2 * g] = (g * N) / p.rows_per_cta;               // CTAs owning group g
@@ -211,8 +217,11 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
     // ------------------------------------------------------- initialisation
     // swarm.hpp:94-132 / planner.hpp:77-133: x draws [0, R*D), v draws [R*D, 2*R*D)
     {
-        const bool warm_on = p.has_prev != nullptr && p.has_prev[swarm] != 0;
-        const double* prev = warm_on ? p.prev + size_t(swarm) * D : nullptr;
+        const unsigned char* hp = p.inl ? (p.has_prev ? pl.bytes + p.in_has_prev : nullptr) : p.has_prev;
+        const bool warm_on = hp != nullptr && hp[swarm] != 0;
+        const double* prev = warm_on ? (p.inl ? reinterpret_cast<const double*>(pl.bytes + p.in_prev) : p.prev) +
+                                           size_t(swarm) * D
+                                     : nullptr;
         const T rad = T(p.pi_radius);
         // one position / velocity draw for element e = (pl, d) of this CTA
         auto put_x = [&](int pl, int d, T ux) {
@@ -663,7 +672,8 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
 
 // ------------------------------------------------------------------ launcher
 template <class T, bool PATH>
-static int launch_t(const SwarmParams& p, int problem, cudaStream_t st, size_t* smem_out) {
+static int launch_t(const SwarmParams& p, const ParamPayload* pl, int problem, cudaStream_t st,
+                    size_t* smem_out) {
     const SmemLayout L = smem_layout(p, sizeof(T), PATH);
     if (smem_out) *smem_out = L.total;
     auto kern = swarm_kernel<T, PATH>;
@@ -692,17 +702,19 @@ static int launch_t(const SwarmParams& p, int problem, cudaStream_t st, size_t* 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, kern, p, problem);
+    static const ParamPayload empty{};
+    e = cudaLaunchKernelEx(&cfg, kern, p, pl ? *pl : empty, problem);
     return int(e);
 }
 
-int launch_swarms(const SwarmParams& p, int problem, bool fp64, void* stream, size_t* smem) {
+int launch_swarms(const SwarmParams& p, const ParamPayload* pl, int problem, bool fp64, void* stream,
+                  size_t* smem) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const bool path = problem == kPath;
-    if (fp64) return path ? launch_t<double, true>(p, problem, st, smem)
-                          : launch_t<double, false>(p, problem, st, smem);
-    return path ? launch_t<float, true>(p, problem, st, smem)
-                : launch_t<float, false>(p, problem, st, smem);
+    if (fp64) return path ? launch_t<double, true>(p, pl, problem, st, smem)
+                          : launch_t<double, false>(p, pl, problem, st, smem);
+    return path ? launch_t<float, true>(p, pl, problem, st, smem)
+                : launch_t<float, false>(p, pl, problem, st, smem);
 }
 
 int swarm_smem_bytes(const SwarmParams& p, int problem, bool fp64, size_t* bytes) {

@@ -87,6 +87,17 @@ struct SwarmParams {
     SwarmOut* out; double* best_x; double* trace;
     // debug: per-iteration phase timestamps of swarm 0 / CTA 0 (SEPSO_PHASE_PROF)
     long long* prof;
+    // inl != 0: the inputs travel in the launch's ParamPayload (no H2D copy);
+    // in_* are their byte offsets there (seeds, worlds, hypers, prev, has_prev,
+    // lo, hi, window values, window lengths)
+    int inl, in_seed, in_world, in_hyp, in_prev, in_has_prev, in_lo, in_hi, in_win, in_win_len;
+};
+
+// Small host-buffer launches (one paper scene: ~1.8 KB of inputs) pass their
+// inputs as a kernel parameter block, copied with the launch itself.
+constexpr int kInlineBytes = 3328;
+struct ParamPayload {
+    unsigned char bytes[kInlineBytes];
 };
 // Phase profiler (SEPSO_PHASE_PROF=1 at run time) exists only in builds with
 // -DSEPSO_PROFILE (make PROF=1): the release kernel carries none of its code.
@@ -165,7 +176,7 @@ SEPSO_LHD SmemLayout smem_layout(const SwarmParams& p, size_t tsz, bool path) {
 }
 
 // host launchers (swarm_kernel.cu)
-int launch_swarms(const SwarmParams& p, int problem, bool fp64, void* stream,
+int launch_swarms(const SwarmParams& p, const ParamPayload* pl, int problem, bool fp64, void* stream,
                   size_t* smem_bytes_out);
 int swarm_smem_bytes(const SwarmParams& p, int problem, bool fp64, size_t* bytes);
 int max_smem_per_block();
