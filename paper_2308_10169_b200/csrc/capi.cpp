@@ -226,11 +226,15 @@ int run_batch(sf_ctx* ctx, const BatchIn& b, BatchOut& r) {
     p.hi = reinterpret_cast<const double*>(d + io.hi);
     p.win_vals = reinterpret_cast<double*>(d + io.win);
     p.win_len = reinterpret_cast<int*>(d + io.win_len);
-    // results go straight to the pinned block (mapped into the device address
-    // space under UVA): the kernel's stores cross the bus, no D2H copy follows
-    p.out = reinterpret_cast<SwarmOut*>(h + io.out);
-    p.best_x = reinterpret_cast<double*>(h + io.best);
-    p.trace = reinterpret_cast<double*>(h + io.trace);
+    // small results go straight to the pinned block (mapped into the device
+    // address space under UVA): the kernel's stores cross the bus, no D2H copy
+    // follows.  Large ones (batched traces) are written on the device and
+    // copied back in one transfer.
+    const bool zc_out = io.end - io.out <= 64 * 1024;
+    unsigned char* ob = zc_out ? h : d;
+    p.out = reinterpret_cast<SwarmOut*>(ob + io.out);
+    p.best_x = reinterpret_cast<double*>(ob + io.best);
+    p.trace = reinterpret_cast<double*>(ob + io.trace);
     // small inputs (one paper scene: ~1.8 KB) ride in the launch's parameter
     // block instead of a separate H2D copy; larger ones take the copy
     static thread_local ParamPayload payload;
@@ -251,6 +255,10 @@ int run_batch(sf_ctx* ctx, const BatchIn& b, BatchOut& r) {
     ctx->last_d2h = io.end - io.out;
     st = launch_fused(ctx, fp, b.problem);
     if (st != SF_OK) return st;
+    if (!zc_out) {
+        ce = cudaMemcpyAsync(h + io.out, d + io.out, io.end - io.out, cudaMemcpyDeviceToHost, ctx->stream);
+        if (ce != cudaSuccess) return cuda_fail(ce, "D2H io");
+    }
     ce = cudaStreamSynchronize(ctx->stream);
     if (ce != cudaSuccess) return cuda_fail(ce, "swarm kernel");
     std::memcpy(r.out.data(), h + io.out, size_t(b.n) * sizeof(SwarmOut));
