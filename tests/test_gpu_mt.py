@@ -98,3 +98,16 @@ def test_evolve_mt_equals_reference(eng64mt):
                             ptr(np.ascontiguousarray(DEFAULT_GROUP_HYPERS[:2])), RNG_MT, ptr(bt), ptr(rt),
                             ptr(bh)) == 0
     assert np.array_equal(r["best_lfv_trace"], bt) and np.array_equal(r["best"].reshape(-1), bh)
+
+
+@pytest.mark.parametrize("G,N", [(40, 3), (33, 2)])
+def test_run_dtpso_many_groups_equals_oracle(eng64mt, G, N):
+    """More groups than lanes of a warp (the best update loops over groups)."""
+    rng = np.random.default_rng(G)
+    hyp = np.column_stack([rng.uniform(0.5, 2.5, (G, 3)), rng.uniform(0.6, 1.0, G), rng.uniform(0.1, 0.5, G),
+                           rng.uniform(0.05, 0.5, G)])
+    r = eng64mt.run_dtpso("BF3", hyp, G, N, 25, 5, dim=8)
+    st, tr, fp, ff, _ = oracle_run_dtpso(3, hyp, G, N, 25, 5, D=8, lo=np.full(8, -600.0), hi=np.full(8, 600.0),
+                                         rng=RNG_MT)
+    assert st == 0 and np.allclose(r["trace"], tr, rtol=1e-12, atol=0) and np.allclose(r["final_point"], fp,
+                                                                                       rtol=1e-12, atol=1e-9)
