@@ -222,7 +222,9 @@ FusedPlan plan_fused(sf_ctx* ctx, int problem, int n_swarms, int G, int N, int D
         p.max_local_groups = lgm;
         if (path) {
             // worst case Rc*S*O entries; beyond the capacity entries are evaluated in place
-            p.entry_cap = 0;   // overlapping obstacles are evaluated in place (no work list)
+            // throughput launches: per-warp rings of 64 compacted (item, obstacle)
+            // pairs in A1 (latency launches keep one item per thread in place)
+            p.entry_cap = (!latency && env_int("SEPSO_NO_RING", 0) == 0) ? 1024 / 32 * 64 : 0;
             // one thread per (particle, segment) item; latency launches add four
             // warps (containment tasks, the stream generator) -- measured best
             p.nthreads = std::min(medium ? 512 : 1024, std::max(128, ((Rc * S) + 31) / 32 * 32 + (latency ? 128 : 0)));

@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(256) k_eval_path(const unsigned char* __restri
     c.obb = (T*)(smem + L.obb); c.ooff = (int*)(smem + L.ooff); c.ofl = (int*)(smem + L.ofl);
     c.vert = (T*)(smem + L.vert);
     c.edge = (T*)(smem + L.edge); c.seglen = (T*)(smem + L.seglen); c.q = (int*)(smem + L.q);
-    c.list = (uint32_t*)(smem + L.list); c.m = (Misc<T>*)(smem + L.misc);
+    c.list = pp.entry_cap > 0 ? (uint32_t*)(smem + L.list) : nullptr; c.m = (Misc<T>*)(smem + L.misc);
     load_world(c, world, pp.off_offsets, pp.off_verts);
     if (threadIdx.x == 0) {
         c.m->n_pair = 0;
@@ -483,7 +483,7 @@ int stage_eval_path(bool fp64, const unsigned char* world, int max_obs, int max_
         return int(cudaGetLastError());
     }
     const int rows_tile = 64;
-    pp.entry_cap = 0;
+    pp.entry_cap = 256 / 32 * 64;            // per-warp rings of compacted pair tests (A1)
     const size_t tsz = fp64 ? 8 : 4;
     const EvalSmem L = eval_smem(rows_tile, D, max_obs, max_verts, pp.entry_cap, tsz);
     const unsigned grid = unsigned((rows + rows_tile - 1) / rows_tile);

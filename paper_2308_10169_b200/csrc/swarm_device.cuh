@@ -468,14 +468,78 @@ __device__ void load_world(Ctx<T>& c, const unsigned char* wrec, int off_offsets
 //       evaluated in place (vertex-cross early exit, filtered pair test, FP64
 //       fallback); first-waypoint containment tasks continue the item space.
 //   A3  fitness = sum of lengths in chain order + alpha * Q^beta.
-template <class T>
+// RING: compacted pair tests (throughput launches, stage evaluation); the
+// latency launch instantiates the in-place variant only (smaller hot loop).
+template <class T, bool RING = true>
 __device__ void path_fitness_phase(const SwarmParams& p, Ctx<T>& c, long long* prof_ = nullptr,
                                    int k = 0) {
     long long* const prof = kProfiling ? prof_ : nullptr;
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int S = c.S, items = c.P * S, O = c.O;
     // ---- A1
-    {
+    if (RING && c.list != nullptr) {
+        // Items in warp-wide rounds; the (item, obstacle) pairs whose boxes
+        // overlap are compacted into a per-warp ring of 64 entries and tested
+        // 32 at a time by all lanes -- no lane idles while another works
+        // through a long list of overlaps.
+        const int lane = tid & 31, warp = tid >> 5;
+        const unsigned lt_mask = (1u << lane) - 1u;
+        uint32_t* ring = c.list + warp * 64;
+        int head = 0, pend = 0;
+        auto drain = [&](int n) {
+            if (lane < n) {
+                const uint32_t en = ring[(head + lane) & 63];
+                const int epl = int(en >> 19), es = int((en >> 11) & 0xffu), eo = int(en & 0x7ffu);
+                T b1x, b1y, b2x, b2y;
+                chain_pt(c, epl, es, b1x, b1y);
+                chain_pt(c, epl, es + 1, b2x, b2y);
+                const int r = pair_count_pts(c, b1x, b1y, b2x, b2y, eo);
+                if (r) atomicAdd(&c.q[epl], r);
+            }
+            head += n;
+            pend -= n;
+        };
+        for (int base = warp * 32; base < items; base += nthr) {
+            const int it = base + lane;
+            const bool valid = it < items;
+            const int pl = valid ? int(c.fS.div(uint32_t(it))) : 0, s = it - pl * S;
+            T lx = T(0), ly = T(0), hx = T(0), hy = T(0);
+            if (valid) {
+                T a1x, a1y, a2x, a2y;
+                chain_pt(c, pl, s, a1x, a1y);
+                chain_pt(c, pl, s + 1, a2x, a2y);
+                c.seglen[pl * S + s] = seg_length<T>(Ar<T>::sub(a2x, a1x), Ar<T>::sub(a2y, a1y));
+                lx = a1x < a2x ? a1x : a2x; hx = a1x < a2x ? a2x : a1x;
+                ly = a1y < a2y ? a1y : a2y; hy = a1y < a2y ? a2y : a1y;
+            }
+            if (prof && it == tid) prof[(k - 1) * kProfPhases + 1] = clock64();
+            for (int o0 = 0; o0 < O; o0 += 32) {
+                uint32_t mask = 0;
+                if (valid) {
+                    const int oe = min(32, O - o0);
+#pragma unroll 8
+                    for (int j = 0; j < oe; ++j)
+                        if (box_overlap(lx, ly, hx, hy, c.obb + 4 * (o0 + j), c.margin)) mask |= 1u << j;
+                }
+                unsigned any = __reduce_or_sync(0xffffffffu, mask);
+                while (any) {
+                    const int j = __ffs(any) - 1;
+                    any &= any - 1;
+                    const bool ov = (mask >> j) & 1u;
+                    const unsigned m = __ballot_sync(0xffffffffu, ov);
+                    if (ov) ring[(head + pend + __popc(m & lt_mask)) & 63] = pack_entry(pl, s, o0 + j);
+                    pend += __popc(m);
+                    __syncwarp();
+                    if (pend >= 32) {
+                        drain(32);
+                        __syncwarp();
+                    }
+                }
+            }
+            if (prof && it == tid) prof[(k - 1) * kProfPhases + 2] = clock64();
+        }
+        if (pend > 0) drain(pend);
+    } else {
         const int step_pl = int(c.fS.div(uint32_t(nthr))), step_s = nthr - step_pl * S;
         int pl = int(c.fS.div(uint32_t(tid))), s = tid - pl * S;
         for (int it = tid; it < items; it += nthr) {
@@ -485,7 +549,6 @@ __device__ void path_fitness_phase(const SwarmParams& p, Ctx<T>& c, long long* p
             c.seglen[pl * S + s] = seg_length<T>(Ar<T>::sub(a2x, a1x), Ar<T>::sub(a2y, a1y));
             const T lx = a1x < a2x ? a1x : a2x, hx = a1x < a2x ? a2x : a1x;
             const T ly = a1y < a2y ? a1y : a2y, hy = a1y < a2y ? a2y : a1y;
-            if (prof && it == tid) prof[(k - 1) * kProfPhases + 1] = clock64();
             int cnt = 0;
             for (int o0 = 0; o0 < O; o0 += 32) {
                 uint32_t mask = 0;
@@ -499,12 +562,13 @@ __device__ void path_fitness_phase(const SwarmParams& p, Ctx<T>& c, long long* p
                     cnt += pair_count_pts(c, a1x, a1y, a2x, a2y, o0 + j);
                 }
             }
-            if (prof && it == tid) prof[(k - 1) * kProfPhases + 2] = clock64();
             if (cnt) atomicAdd(&c.q[pl], cnt);
             pl += step_pl;
             s += step_s;
             if (s >= S) { s -= S; ++pl; }
         }
+    }
+    {
         // first waypoint strictly inside an obstacle (geometry.hpp:217-218):
         // particle tasks continue the item index space so they land on the
         // threads with the fewest items

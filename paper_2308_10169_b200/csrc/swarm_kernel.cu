@@ -98,7 +98,7 @@ __device__ void step_world_part(unsigned char* rec, int off_offsets, int off_ver
 #endif
 constexpr int STEPW = SEPSO_STEPW;
 
-template <class T, bool PATH>
+template <class T, bool PATH, bool RING>
 __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ SwarmParams p,
                                                         const __grid_constant__ ParamPayload pl,
                                                         int problem) {
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
     c.part = (Part*)S8(L.part); c.px = (T*)S8(L.px); c.allpart = (Part*)S8(L.allpart);
     c.allbad = (int*)S8(L.allbad); c.gtab = (int*)S8(L.gtab); c.ctab = (int*)S8(L.ctab);
     c.obb = (T*)S8(L.obb); c.ooff = (int*)S8(L.ooff); c.ofl = (int*)S8(L.ofl); c.vert = (T*)S8(L.vert);
-    c.edge = (T*)S8(L.edge); c.list = (uint32_t*)S8(L.list); c.m = (Misc<T>*)S8(L.misc);
+    c.edge = (T*)S8(L.edge); c.list = p.entry_cap > 0 ? (uint32_t*)S8(L.list) : nullptr; c.m = (Misc<T>*)S8(L.misc);
     const int LGM = p.max_local_groups;
     // bytes every CTA receives per iteration: each CTA's group partials (16 B)
     // and their rows (D values), plus every CTA's first non-finite row (4 B)
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
         SEPSO_MARK(0);
         if (wprof) wt0 = clock64();
         // fitness (geometry.hpp:262-267 / benchmarks.hpp:45-53)
-        if (PATH) path_fitness_phase(p, c, prof, k);
+        if (PATH) path_fitness_phase<T, RING>(p, c, prof, k);
         else bench_fitness_phase(problem, c);
         SEPSO_MARK(4);
         // pbest (runner.hpp:73-80) incl. the x -> pbest_x row copy; non-finite
@@ -671,12 +671,12 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
 }
 
 // ------------------------------------------------------------------ launcher
-template <class T, bool PATH>
+template <class T, bool PATH, bool RING>
 static int launch_t(const SwarmParams& p, const ParamPayload* pl, int problem, cudaStream_t st,
                     size_t* smem_out) {
     const SmemLayout L = smem_layout(p, sizeof(T), PATH);
     if (smem_out) *smem_out = L.total;
-    auto kern = swarm_kernel<T, PATH>;
+    auto kern = swarm_kernel<T, PATH, RING>;
     cudaError_t e = cudaSuccess;
     static thread_local size_t smem_set = 0;     // attributes are sticky per function
     static thread_local bool nonportable = false;
@@ -711,10 +711,13 @@ int launch_swarms(const SwarmParams& p, const ParamPayload* pl, int problem, boo
                   size_t* smem) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const bool path = problem == kPath;
-    if (fp64) return path ? launch_t<double, true>(p, pl, problem, st, smem)
-                          : launch_t<double, false>(p, pl, problem, st, smem);
-    return path ? launch_t<float, true>(p, pl, problem, st, smem)
-                : launch_t<float, false>(p, pl, problem, st, smem);
+    const bool ring = p.entry_cap > 0;
+    if (fp64) return path ? (ring ? launch_t<double, true, true>(p, pl, problem, st, smem)
+                                  : launch_t<double, true, false>(p, pl, problem, st, smem))
+                          : launch_t<double, false, false>(p, pl, problem, st, smem);
+    return path ? (ring ? launch_t<float, true, true>(p, pl, problem, st, smem)
+                        : launch_t<float, true, false>(p, pl, problem, st, smem))
+                : launch_t<float, false, false>(p, pl, problem, st, smem);
 }
 
 int swarm_smem_bytes(const SwarmParams& p, int problem, bool fp64, size_t* bytes) {
