@@ -660,8 +660,9 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
         if (tid == 0 && p.carry) p.win_len[swarm] = c.m->win_len;
     }
     // scene batches: advance this swarm's world record for the next frame
-    // (simenv.hpp:155-184); every CTA staged it long ago
-    if (PATH && p.step_dt != 0.0 && c.crank == 0)
+    // (simenv.hpp:155-184); every CTA staged it long ago.  Rank 1 does it
+    // while rank 0 writes the record.
+    if (PATH && p.step_dt != 0.0 && c.crank == (c.C > 1 ? 1 : 0))
         for (int t = tid - 2; t < c.O; t += nthr)
             step_world_part(const_cast<unsigned char*>(p.worlds) + size_t(swarm) * size_t(p.world_stride),
                             p.off_offsets, p.off_verts, p.off_vel, p.step_dt, t);
