@@ -667,7 +667,8 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
             step_world_part(const_cast<unsigned char*>(p.worlds) + size_t(swarm) * size_t(p.world_stride),
                             p.off_offsets, p.off_verts, p.off_vel, p.step_dt, t);
     SEPSO_GMARK(10);
-    cluster.sync();   // no CTA leaves while a peer may still read its shared memory
+    // No closing cluster barrier: a CTA only ever reads its own shared memory,
+    // and every st.async into it completed before its last best update.
     SEPSO_GMARK(11);
 }
 

@@ -57,3 +57,16 @@ def test_scene_batch_fp32_statistics(eng32mt):
     assert abs(np.mean([r.iterations for r in recs]) - s["mean_iterations"]) < 1.5
     assert abs(np.mean([r.length for r in recs]) - s["mean_length"]) < 0.02 * s["mean_length"]
     assert sum(r.collision_free for r in recs) >= 90
+
+
+def test_scene_batch_philox_equals_host_run_scenario(eng64):
+    """The same device-resident loop with the Philox stream (the harness build's)."""
+    frames = 8
+    sb = pe.SceneBatch(eng64, [pe.ScenarioConfig(root_seed=5)], PLANNER, pe.EVOLVED_PATH_HYPERS, frames)
+    sb.run(frames)
+    recs, _ = sb.records(0, frames)
+    sb.close()
+    host = eng64.run_scenario(pe.ScenarioConfig(root_seed=5), "sepso", frames, PLANNER)
+    for d, h in zip(recs, host):
+        assert (d.iterations, d.truncated, d.intersections) == (h.iterations, h.truncated, h.intersections)
+        assert d.fitness == h.fitness and d.length == h.length
