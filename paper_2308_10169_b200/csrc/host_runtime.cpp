@@ -304,6 +304,14 @@ int launch_fused(sf_ctx* ctx, FusedPlan& fp, int problem) {
                 smin += double(mn); smax += double(mx); sown += double(w[(size_t(k) * 16) * 2 + 1]); ++nk;
             }
             if (nk) std::fprintf(stderr, " | per-CTA fitness..push: min=%.0f max=%.0f cta0_wait=%.0f", smin / nk, smax / nk, sown / nk);
+            if (nk) {
+                std::fprintf(stderr, " | by CTA:");
+                for (int cc = 0; cc < std::min(16, fp.p.C); ++cc) {
+                    double s = 0;
+                    for (int k = 0; k < iters; ++k) s += double(w[(size_t(k) * 16 + cc) * 2]);
+                    std::fprintf(stderr, " %.0f", s / nk);
+                }
+            }
         }
         std::fprintf(stderr, "\n");
     }
