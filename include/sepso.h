@@ -110,6 +110,12 @@ int sf_ctx_synchronize(sf_ctx* ctx);
 int sf_ctx_set_launch(sf_ctx* ctx, int cluster, int threads);
 int sf_ctx_set_rng(sf_ctx* ctx, int rng);
 int sf_ctx_rng(const sf_ctx* ctx);
+/* Jump-ahead polynomial of the std::mt19937_64 stream (host only): out[312]
+ * = x^steps mod phi (bit i = coefficient of x^i, phi the generator's
+ * characteristic polynomial).  XOR-ing the raw windows x[i .. i+311] over
+ * its terms i gives the state `steps` words later (long fills start segments
+ * from such states). */
+int sf_mt_jump_poly(uint64_t steps, uint64_t* out);
 /* Device time of the engine kernels, bracketed by CUDA events on the context
  * stream while enabled: total milliseconds and launch count since enable. */
 int sf_ctx_enable_timing(sf_ctx* ctx, int enable);

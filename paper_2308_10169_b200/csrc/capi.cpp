@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "host_runtime.hpp"
+#include "mt_jump.hpp"
 #include "stage_kernels.cuh"
 
 using namespace sepso;
@@ -350,6 +351,13 @@ int sf_ctx_set_rng(sf_ctx* ctx, int rng) {
 }
 
 int sf_ctx_rng(const sf_ctx* ctx) { return ctx ? ctx->rng : -1; }
+
+int sf_mt_jump_poly(uint64_t steps, uint64_t* out) {
+    if (!out) return fail(SF_INVALID_ARGUMENT, "null argument");
+    const std::vector<uint64_t> g = mt_jump_poly(steps);
+    std::copy(g.begin(), g.end(), out);
+    return SF_OK;
+}
 
 int sf_ctx_enable_timing(sf_ctx* ctx, int enable) {
     if (!ctx) return fail(SF_INVALID_ARGUMENT, "ctx is null");

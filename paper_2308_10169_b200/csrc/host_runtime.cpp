@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <limits>
 
+#include "mt_jump.hpp"
 #include "stage_kernels.cuh"
 
 namespace sepso {
@@ -374,6 +375,14 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
     const bool mt = ctx->rng == SF_RNG_MT19937;
     const size_t o_mt = take(mt ? sizeof(MtPersist) : 0);
     const size_t o_words = take(mt ? size_t(2) * R * D * 8 : 0);   // init window; steps reuse it
+    // long init windows are generated in parallel segments from jumped states
+    const long long init_words = 2ll * R * D;
+    int jlevels = 0;
+    while (mt && jlevels < kMaxJumpLevels && (init_words >> (jlevels + 1)) >= (1ll << 17)) ++jlevels;
+    if (std::getenv("SEPSO_SEQ_FILL")) jlevels = 0;
+    const bool jump = jlevels >= 2;
+    const size_t o_jst = take(jump ? (size_t(1) << jlevels) * 312 * 8 : 0);
+    const size_t o_jpoly = take(jump ? size_t(jlevels) * 312 * 8 : 0);
     cudaError_t ce = ctx->scratch.ensure(off);
     if (ce != cudaSuccess) return cuda_fail(ce, "staged arena");
     unsigned char* dev = static_cast<unsigned char*>(ctx->scratch.p);
@@ -420,8 +429,20 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
     IterState* dst = reinterpret_cast<IterState*>(dev + o_st);
     unsigned long long* words = mt ? reinterpret_cast<unsigned long long*>(dev + o_words) : nullptr;
     MtPersist* mtg = mt ? reinterpret_cast<MtPersist*>(dev + o_mt) : nullptr;
-    if (mt) {   // the reference stream, sequential: init words [0, 2RD)
-        const int fe = stage_mt_fill(mtg, r.seed, true, 0, 2ll * R * D, words, st);
+    if (mt && jump) {   // the reference stream, init words [0, 2RD) in 2^jlevels segments
+        const long long seg = (init_words + (1ll << jlevels) - 1) >> jlevels;
+        const long long Q = (seg + 623) / 624 * 624;                // whole generator passes
+        const std::vector<std::vector<uint64_t>>& ladder = mt_jump_ladder(uint64_t(Q), jlevels);
+        for (int j = 0; j < jlevels; ++j)
+            cudaMemcpyAsync(dev + o_jpoly + size_t(j) * 312 * 8, ladder[size_t(j)].data(), 312 * 8,
+                            cudaMemcpyHostToDevice, st);
+        const int fe = stage_mt_fill_parallel(mtg, r.seed, init_words, words,
+                                              reinterpret_cast<unsigned long long*>(dev + o_jst),
+                                              reinterpret_cast<const unsigned long long*>(dev + o_jpoly), jlevels, Q,
+                                              st);
+        if (fe) return cuda_fail(cudaError_t(fe), "stage_mt_fill_parallel");
+    } else if (mt) {   // sequential
+        const int fe = stage_mt_fill(mtg, r.seed, true, 0, init_words, words, st);
         if (fe) return cuda_fail(cudaError_t(fe), "stage_mt_fill");
     }
     int e = stage_init(fp64, s, reinterpret_cast<double*>(dev + o_hyp), dev + o_lo, dev + o_hi, r.seed, 0,

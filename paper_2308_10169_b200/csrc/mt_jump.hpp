@@ -1,0 +1,19 @@
+// mt_jump.hpp -- jump-ahead polynomials for the mt19937_64 stream (host side;
+// mt_jump.cpp).  Polynomials are bit vectors of kMtPolyWords words.
+#pragma once
+#include <cstdint>
+#include <vector>
+
+namespace sepso {
+
+constexpr int kMtDegree = 19937;       // state bits of std::mt19937_64
+constexpr int kMtPolyWords = 312;      // 19,968 bits
+constexpr int kMaxJumpLevels = 6;      // parallel fills: at most 64 segments
+
+// x^steps mod phi: applying it to the state at word w gives the state at w + steps
+std::vector<uint64_t> mt_jump_poly(uint64_t steps);
+
+// x^(quantum * 2^j) mod phi for j = 0 .. levels-1 (cached per process)
+const std::vector<std::vector<uint64_t>>& mt_jump_ladder(uint64_t quantum, int levels);
+
+} // namespace sepso

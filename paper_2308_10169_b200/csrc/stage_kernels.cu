@@ -4,6 +4,7 @@
 #include <algorithm>
 
 #include "mt19937.cuh"
+#include "mt_jump.hpp"
 #include "stage_kernels.cuh"
 #include "swarm_device.cuh"
 
@@ -61,6 +62,107 @@ int stage_mt_fill(MtPersist* g, unsigned long long seed, bool reseed, long long 
                   unsigned long long* out, void* stream) {
     // four warps compute each pass, four more store its (untempered) words
     k_mt_fill<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(g, seed, reseed ? 1 : 0, from, upto, out);
+    return int(cudaGetLastError());
+}
+
+// ------------------------------------------------------- parallel stream fill
+// A long fill [0, upto) in 2^levels segments of Q words generated in parallel,
+// each from its start state s_{mQ} = g(A) s_0 (mt_jump.cpp): the states come
+// from a doubling ladder of jumps, level j taking states 0 .. 2^j - 1 to
+// 2^j .. 2^(j+1) - 1 with g = x^(Q 2^j) mod phi.  A state is a raw 312-word
+// window (slot 1 of an MtState pair).
+
+__global__ void k_mt_seed_state(unsigned long long* st, unsigned long long seed) {
+    if (threadIdx.x == 0) mt_seed_words(st, seed);
+}
+
+// s_dst = XOR over g's terms i in this CTA's chunk of the window x[i .. i+311]
+// of s_src (split CTAs per jump); dst is zeroed by the host and combined with
+// atomicXor.
+__global__ void __launch_bounds__(1024) k_mt_jump(unsigned long long* states, int n_src, int split,
+                                                  const unsigned long long* poly) {
+    extern __shared__ __align__(16) unsigned long long jsm[];
+    unsigned long long* buf = jsm;                      // generator (4 x 312)
+    unsigned long long* P = jsm + kMtStateWords;        // g, 312 words
+    unsigned long long* X = P + 312;                    // x[0 .. i1 + 311]
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int m = blockIdx.x / split, part = blockIdx.x % split, chunk = (kMtDegree + split - 1) / split;
+    const int i0 = part * chunk, i1 = min(kMtDegree, i0 + chunk);
+    const unsigned long long* src = states + size_t(m) * 312;
+    unsigned long long* dst = states + size_t(m + n_src) * 312;
+    for (int k = tid; k < 312; k += nthr) {
+        const unsigned long long w = src[k];
+        buf[312 + k] = w;
+        X[k] = w;
+        P[k] = poly[k];
+    }
+    __syncthreads();
+    MtState s{buf, 0, 0};
+    mt_generate<0, true>(s, MtGroup{tid, nthr, 0}, 0, i1,
+                         [&](int rel, unsigned long long word) { X[312 + rel] = word; });
+    __syncthreads();
+    unsigned long long acc = 0;
+    const int k = tid % 312, sub = tid / 312;
+    if (sub < 3) {
+        const int c3 = (i1 - i0 + 2) / 3, a = i0 + sub * c3, b = min(i1, a + c3);
+        for (int q = a >> 6; a < b && q <= (b - 1) >> 6; ++q) {
+            unsigned long long bits = P[q];
+            const int lo = q * 64;
+            if (a > lo) bits &= ~0ull << (a - lo);
+            if (b < lo + 64) bits &= (1ull << (b - lo)) - 1ull;
+            while (bits) {
+                const int bb = __ffsll((long long)bits) - 1;
+                bits &= bits - 1;
+                acc ^= X[lo + bb + k];
+            }
+        }
+        buf[tid] = acc;                                 // generator buffer is free now
+    }
+    __syncthreads();
+    if (tid < 312) atomicXor(dst + tid, buf[tid] ^ buf[312 + tid] ^ buf[624 + tid]);
+}
+
+// segment m: words [mQ, min(upto, (m+1)Q)), untempered, from state m; the
+// segment holding the end leaves the generator in g as k_mt_fill would
+__global__ void __launch_bounds__(256) k_mt_fill_seg(const unsigned long long* states, long long Q, long long upto,
+                                                     unsigned long long* out, MtPersist* g) {
+    __shared__ __align__(128) unsigned long long buf[kMtStateWords];
+    const long long start = (long long)blockIdx.x * Q;
+    if (start >= upto) return;
+    const long long len = upto - start < Q ? upto - start : Q;
+    for (int k = threadIdx.x; k < 312; k += blockDim.x) buf[312 + k] = states[size_t(blockIdx.x) * 312 + k];
+    __syncthreads();
+    MtState s{buf, 0, 0};
+    mt_generate<0, true>(s, MtGroup{int(threadIdx.x), int(blockDim.x), 0}, 0, len,
+                         [&](int rel, unsigned long long word) { out[start + rel] = word; });
+    if (start + len == upto) {
+        for (int i = threadIdx.x; i < 624; i += blockDim.x) g->st[i] = buf[s.cur * 624 + i];
+        if (threadIdx.x == 0) g->blocks = s.blocks + start / 312;
+    }
+}
+
+size_t mt_jump_smem_bytes() { return size_t(kMtStateWords + 312 + 312 + kMtDegree) * 8; }
+
+int stage_mt_fill_parallel(MtPersist* g, unsigned long long seed, long long upto, unsigned long long* out,
+                           unsigned long long* states, const unsigned long long* polys, int levels, long long Q,
+                           void* stream) {
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    static thread_local bool attr = false;
+    if (!attr) {
+        const cudaError_t e = cudaFuncSetAttribute(k_mt_jump, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   int(mt_jump_smem_bytes()));
+        if (e != cudaSuccess) return int(e);
+        attr = true;
+    }
+    k_mt_seed_state<<<1, 32, 0, st>>>(states, seed);
+    for (int j = 0; j < levels; ++j) {
+        const int n = 1 << j;
+        cudaError_t e = cudaMemsetAsync(states + size_t(n) * 312, 0, size_t(n) * 312 * 8, st);
+        if (e != cudaSuccess) return int(e);
+        const int split = std::max(8, std::min(32, 256 / n));      // fill the GPU at the narrow levels
+        k_mt_jump<<<n * split, 1024, mt_jump_smem_bytes(), st>>>(states, n, split, polys + size_t(j) * 312);
+    }
+    k_mt_fill_seg<<<1u << levels, 256, 0, st>>>(states, Q, upto, out, g);
     return int(cudaGetLastError());
 }
 

@@ -56,6 +56,13 @@ struct MtPersist {
 // earlier words are skipped.  reseed restarts the generator from `seed`.
 int stage_mt_fill(MtPersist* g, unsigned long long seed, bool reseed, long long from,
                   long long upto, unsigned long long* out, void* stream);
+// The same fill of [0, upto) from a fresh seed in 2^levels parallel segments of
+// Q words (Q a multiple of 624, Q * 2^levels >= upto) started from jumped
+// states (mt_jump.cpp); polys = mt_jump_ladder(Q, levels) on the device,
+// states = scratch for 2^levels x 312 words.  Identical words and final g.
+int stage_mt_fill_parallel(MtPersist* g, unsigned long long seed, long long upto, unsigned long long* out,
+                           unsigned long long* states, const unsigned long long* polys, int levels, long long Q,
+                           void* stream);
 
 int stage_eval_path(bool fp64, const unsigned char* world, int max_obs, int max_verts,
                     int off_offsets, int off_verts, int D, int rows, const void* x,

@@ -39,7 +39,7 @@ ABI_SYMBOLS = [
     "sf_scene_batch_run", "sf_scene_batch_records", "sf_scene_batch_destroy",
     "sf_ctx_last_io_bytes", "sf_measure_fp32_peak", "sf_ctx_set_l2_flush",
     "sf_comm_unique_id", "sf_ctx_init_comm", "sf_plan_frame_sharded", "sf_ctx_set_rng",
-    "sf_ctx_rng",
+    "sf_ctx_rng", "sf_mt_jump_poly",
 ]
 RNGS = {"philox": 0, "mt19937": 1}
 
@@ -171,6 +171,7 @@ def lib():
         "sf_scene_batch_destroy": (C.c_int, [C.c_void_p]),
         "sf_ctx_last_io_bytes": (C.c_int, [C.c_void_p, _u64p, _u64p]),
         "sf_measure_fp32_peak": (C.c_int, [C.c_void_p, _dp]),
+        "sf_mt_jump_poly": (C.c_int, [C.c_uint64, _u64p]),
         "sf_ctx_set_l2_flush": (C.c_int, [C.c_void_p, C.c_uint64]),
         "sf_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
         "sf_ctx_init_comm": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8), C.c_int, C.c_int]),

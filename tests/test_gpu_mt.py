@@ -111,3 +111,21 @@ def test_run_dtpso_many_groups_equals_oracle(eng64mt, G, N):
                                          rng=RNG_MT)
     assert st == 0 and np.allclose(r["trace"], tr, rtol=1e-12, atol=0) and np.allclose(r["final_point"], fp,
                                                                                        rtol=1e-12, atol=1e-9)
+
+
+@pytest.mark.parametrize("per_group", [2048, 8192])
+def test_parallel_stream_fill_equals_sequential(eng64mt, per_group):
+    """Long init fills run as parallel segments from jumped generator states
+    (mt_jump.cpp, stage_mt_fill_parallel): the same words and the same
+    generator state afterwards (the step draws continue from it)."""
+    o = oracle()
+    w = pe.generate_world(pe.ScenarioConfig(), o.or_derive_seed(7, b"world"), "mt19937")
+    cfg = pe.PlannerConfig(max_iters_per_frame=4, per_group=per_group, auto_truncate=False)
+    os.environ["SEPSO_SEQ_FILL"] = "1"
+    try:
+        a = eng64mt.plan_frame_sharded(w, None, EVOLVED_PATH_HYPERS, cfg, 99)
+    finally:
+        del os.environ["SEPSO_SEQ_FILL"]
+    b = eng64mt.plan_frame_sharded(w, None, EVOLVED_PATH_HYPERS, cfg, 99)
+    assert a.iterations == b.iterations == 4
+    assert a.fitness == b.fitness and np.array_equal(a.best_path, b.best_path)
