@@ -74,3 +74,41 @@ def test_sharded_with_one_rank_nccl_comm():
         assert a.fitness == b.fitness and np.array_equal(a.best_path, b.best_path)
     finally:
         e.close()
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_config4_size_fitness_equals_oracle(prec, eng32, eng64):
+    """BASELINE config 4 at full size: 1,024 obstacles (768 dynamic + 256 static
+    on a 4,140.8 cm map), D = 128 (64 waypoints, 65 segments x 4,096 edges per
+    row).  A sample of 48 rows -- random, and random walks near the straight
+    start-target line, where the overlaps concentrate -- through the wide
+    evaluation kernel: Q exact in both precisions, fitness bit-exact in FP64
+    and within 1e-5 (relative) in FP32 (on the FP32-rounded world)."""
+    eng = eng64 if prec == "fp64" else eng32
+    sc = pe.ScenarioConfig(map_size=366.0 * np.sqrt(128.0), dynamic_obstacles=768, static_obstacles=256)
+    w = pe.generate_world(sc, 1)
+    if prec == "fp32":
+        w = float_world(w)
+    rng = np.random.default_rng(4)
+    size = w.width
+    xs = rng.uniform(0.0, size, (24, 128))
+    t = np.linspace(0.0, 1.0, 66)[1:-1]
+    line = np.concatenate([w.start[0] + t * (w.target[0] - w.start[0]), w.start[1] + t * (w.target[1] - w.start[1])])
+    walks = np.clip(line[None, :] + rng.normal(0.0, 60.0, (24, 128)), 0.0, size)
+    xs = np.vstack([xs, walks])
+    if prec == "fp32":
+        xs = xs.astype(np.float32).astype(np.float64)
+    f, q = eng.eval_path_rows(w, xs, 128)
+    import ctypes as C
+    from oracle_lib import ptr, u32p
+    wb = world_from_engine(w)
+    n = len(xs)
+    fo, qo = np.zeros(n), np.zeros(n, dtype=np.uint32)
+    oracle().or_eval_path_rows(ptr(np.ascontiguousarray(xs)), n, 128, C.byref(wb.struct()), 30.0, 4.0, ptr(fo),
+                               ptr(qo, u32p))
+    assert np.array_equal(q, qo)
+    assert qo[:24].min() > 0 and qo.max() > 50          # dense worlds: many crossings per row
+    if prec == "fp64":
+        assert np.array_equal(f, fo)
+    else:
+        assert np.all(np.abs(f - fo) <= 1e-5 * np.maximum(1.0, fo))
