@@ -70,3 +70,28 @@ def test_scene_batch_philox_equals_host_run_scenario(eng64):
     for d, h in zip(recs, host):
         assert (d.iterations, d.truncated, d.intersections) == (h.iterations, h.truncated, h.intersections)
         assert d.fitness == h.fitness and d.length == h.length
+
+
+@pytest.mark.parametrize("eng_name", ["eng32mt", "eng64mt"])
+def test_config5_size_batch_equals_single_scenes(eng_name, request):
+    """BASELINE config 5 per GPU: 1,024 scenes in one batch (the throughput
+    launch shape: ~680 rows per CTA, compacted pair tests) give, scene by
+    scene, exactly the records and best paths of the same scenes run alone
+    (the latency shape: 16 CTAs, in-place pair tests) -- in FP32 as in FP64."""
+    eng = request.getfixturevalue(eng_name)
+    n, frames = 1024, 3
+    sb = pe.SceneBatch(eng, [pe.ScenarioConfig(root_seed=s) for s in range(n)], PLANNER, pe.EVOLVED_PATH_HYPERS,
+                       frames)
+    sb.run(frames)
+    recs, best = sb.records(0, frames, with_best=True)
+    sb.close()
+    for s in (0, 1, 511, 1023):
+        one = pe.SceneBatch(eng, [pe.ScenarioConfig(root_seed=s)], PLANNER, pe.EVOLVED_PATH_HYPERS, frames)
+        one.run(frames)
+        r1, b1 = one.records(0, frames, with_best=True)
+        one.close()
+        for f in range(frames):
+            d, h = recs[f * n + s], r1[f]
+            assert (d.iterations, d.truncated, d.intersections) == (h.iterations, h.truncated, h.intersections)
+            assert d.fitness == h.fitness and d.length == h.length
+            assert np.array_equal(best[f, s], b1[f, 0])
