@@ -433,9 +433,11 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
         const long long seg = (init_words + (1ll << jlevels) - 1) >> jlevels;
         const long long Q = (seg + 623) / 624 * 624;                // whole generator passes
         const std::vector<std::vector<uint64_t>>& ladder = mt_jump_ladder(uint64_t(Q), jlevels);
-        for (int j = 0; j < jlevels; ++j)
-            cudaMemcpyAsync(dev + o_jpoly + size_t(j) * 312 * 8, ladder[size_t(j)].data(), 312 * 8,
-                            cudaMemcpyHostToDevice, st);
+        for (int j = 0; j < jlevels; ++j) {
+            ce = cudaMemcpyAsync(dev + o_jpoly + size_t(j) * 312 * 8, ladder[size_t(j)].data(), 312 * 8,
+                                 cudaMemcpyHostToDevice, st);
+            if (ce != cudaSuccess) return cuda_fail(ce, "jump polynomials");
+        }
         const int fe = stage_mt_fill_parallel(mtg, r.seed, init_words, words,
                                               reinterpret_cast<unsigned long long*>(dev + o_jst),
                                               reinterpret_cast<const unsigned long long*>(dev + o_jpoly), jlevels, Q,

@@ -40,11 +40,12 @@ inline uint64_t window64(const Bits& a, long pos) {
     return r ? (lo >> r) | (hi << (64 - r)) : lo;
 }
 
-// a ^= b << s (bit shift), a sized to hold the result
+// a ^= b << s (bit shift) for the low bbits bits of b; bits beyond a are dropped
 void xor_shifted(Bits& a, const Bits& b, long s, long bbits) {
+    if (bbits <= 0 || s < 0 || size_t(s >> 6) >= a.size()) return;
     const size_t q = size_t(s >> 6);
     const int r = int(s & 63);
-    const size_t nb = size_t((bbits + 63) >> 6);
+    const size_t nb = std::min(b.size(), size_t((bbits + 63) >> 6));
     for (size_t k = 0; k < nb; ++k) {
         const uint64_t w = b[k];
         if (q + k < a.size()) a[q + k] ^= r ? (w << r) : w;
