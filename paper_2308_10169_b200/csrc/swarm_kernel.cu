@@ -3,6 +3,7 @@
 // See swarm_kernel.cuh for the execution model.  Reference citations are
 // relative to proj/include/swarmforge/ in the reference tree.
 #include <cooperative_groups.h>
+#include <algorithm>
 #include <type_traits>
 #include <cuda_runtime.h>
 
@@ -98,23 +99,39 @@ __device__ void step_world_part(unsigned char* rec, int off_offsets, int off_ver
 #endif
 constexpr int STEPW = SEPSO_STEPW;
 
+// a pushed pbest row in st.async units: 16-byte vectors, else 4-byte words
+template <class T>
+__host__ __device__ inline int row_units(int D) {
+    const int bytes = D * int(sizeof(T));
+    return bytes % 16 == 0 ? bytes / 16 : bytes / 4;
+}
+
+// Launch constants derived on the host from the shape (launch_t): the shared
+// memory layout, the exchange byte count and the fast divisors -- so no thread
+// spends the prologue on them (the generator seeding waits behind it).
+struct LaunchDerived {
+    SmemLayout lay;
+    uint32_t xbytes;            // bytes every CTA receives per iteration
+    uint32_t dmul[4], dshr[4];  // FastDiv of S, D, N, V (pushed-row units)
+};
+
 template <class T, bool PATH, bool RING>
 __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ SwarmParams p,
                                                         const __grid_constant__ ParamPayload pl,
-                                                        int problem) {
+                                                        const __grid_constant__ LaunchDerived ld, int problem) {
     using A = Ar<T>;
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ __align__(16) unsigned char smem[];
-    const SmemLayout L = smem_layout(p, sizeof(T), PATH);
+    const SmemLayout& L = ld.lay;
     const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5;
     const int swarm = blockIdx.x / p.C;
 
     Ctx<T> c;
     c.G = p.G; c.N = p.N; c.D = p.D; c.W = p.D / 2; c.S = c.W + 1; c.R = p.G * p.N;
-    c.fS.init(uint32_t(c.S));
-    c.fD.init(uint32_t(c.D));
-    c.fN.init(uint32_t(c.N));
-    c.fV.init(uint32_t((c.D * int(sizeof(T))) % 16 == 0 ? c.D * int(sizeof(T)) / 16 : c.D * int(sizeof(T)) / 4));
+    c.fS.d = uint32_t(c.S); c.fS.mul = ld.dmul[0]; c.fS.shr = ld.dshr[0];
+    c.fD.d = uint32_t(c.D); c.fD.mul = ld.dmul[1]; c.fD.shr = ld.dshr[1];
+    c.fN.d = uint32_t(c.N); c.fN.mul = ld.dmul[2]; c.fN.shr = ld.dshr[2];
+    c.fV.d = uint32_t(row_units<T>(c.D)); c.fV.mul = ld.dmul[3]; c.fV.shr = ld.dshr[3];
     c.C = p.C; c.crank = int(cluster.block_rank());
     // partial-exchange mbarriers (one arrival: the local expect_tx); published
     // to the peers by a cluster arrive here and a wait before the first push
@@ -141,14 +158,7 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
     c.obb = (T*)S8(L.obb); c.ooff = (int*)S8(L.ooff); c.ofl = (int*)S8(L.ofl); c.vert = (T*)S8(L.vert);
     c.edge = (T*)S8(L.edge); c.list = p.entry_cap > 0 ? (uint32_t*)S8(L.list) : nullptr; c.m = (Misc<T>*)S8(L.misc);
     const int LGM = p.max_local_groups;
-    // bytes every CTA receives per iteration: each CTA's group partials (16 B)
-    // and their rows (D values), plus every CTA's first non-finite row (4 B)
-    uint32_t xbytes = 0;
-    for (int cc = 0; cc < c.C; ++cc) {
-        const int r0 = cc * p.rows_per_cta, r1 = min(c.R, r0 + p.rows_per_cta);
-        if (r1 > r0) xbytes += uint32_t(((r1 - 1) / c.N - r0 / c.N + 1) * (16 + c.D * int(sizeof(T))));
-        xbytes += 4;
-    }
+    const uint32_t xbytes = ld.xbytes;
     const uint64_t seed =
         p.roots ? splitmix64(splitmix64(p.roots[swarm] ^ p.tag_hash) + uint64_t(p.frame_index))
                 : (p.inl ? reinterpret_cast<const unsigned long long*>(pl.bytes + p.in_seed) : p.seeds)[swarm];
@@ -705,7 +715,26 @@ static int launch_t(const SwarmParams& p, const ParamPayload* pl, int problem, c
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     static const ParamPayload empty{};
-    e = cudaLaunchKernelEx(&cfg, kern, p, pl ? *pl : empty, problem);
+    LaunchDerived ld{};
+    ld.lay = L;
+    {
+        const int R = p.G * p.N, Dv = p.D, Sv = p.D / 2 + 1;
+        uint32_t xb = 0;                     // each CTA's group partials (16 B) + their rows, + 4 B each
+        for (int cc = 0; cc < p.C; ++cc) {
+            const int r0 = cc * p.rows_per_cta, r1 = std::min(R, r0 + p.rows_per_cta);
+            if (r1 > r0) xb += uint32_t(((r1 - 1) / p.N - r0 / p.N + 1) * (16 + Dv * int(sizeof(T))));
+            xb += 4;
+        }
+        ld.xbytes = xb;
+        const int divs[4] = {Sv, Dv, p.N, row_units<T>(Dv)};
+        for (int i = 0; i < 4; ++i) {
+            FastDiv f;
+            f.init(uint32_t(divs[i]));
+            ld.dmul[i] = f.mul;
+            ld.dshr[i] = f.shr;
+        }
+    }
+    e = cudaLaunchKernelEx(&cfg, kern, p, pl ? *pl : empty, ld, problem);
     return int(e);
 }
 
