@@ -447,10 +447,17 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
                 }
                 // tbest: (gbest_f, g) lexicographic min over groups, strict '<'
                 // vs the incumbent (runner.hpp:88-91)
-                for (int off = 16; off; off >>= 1) {
-                    const T ov = __shfl_xor_sync(0xffffffffu, tv, off);
-                    const int og = __shfl_xor_sync(0xffffffffu, tg, off);
-                    if (ov < tv || (ov == tv && og < tg)) { tv = ov; tg = og; }
+                if (sizeof(T) == 4) {          // ordered keys: two warp reductions
+                    const uint32_t key = order_key(float(tv));
+                    const uint32_t kmin = __reduce_min_sync(0xffffffffu, key);
+                    tg = int(__reduce_min_sync(0xffffffffu, key == kmin ? uint32_t(tg) : 0xffffffffu));
+                    tv = __shfl_sync(0xffffffffu, tv, __ffs(__ballot_sync(0xffffffffu, key == kmin)) - 1);
+                } else {
+                    for (int off = 16; off; off >>= 1) {
+                        const T ov = __shfl_xor_sync(0xffffffffu, tv, off);
+                        const int og = __shfl_xor_sync(0xffffffffu, tg, off);
+                        if (ov < tv || (ov == tv && og < tg)) { tv = ov; tg = og; }
+                    }
                 }
                 // tbest update, trace, window push + trim to tw (planner.hpp:179-180)
                 const bool tnew = tv < m->tbf;
