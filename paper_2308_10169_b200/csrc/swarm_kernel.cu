@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
             // init words; only the words of this CTA's rows are tempered and
             // go straight into x / v.  The seeded state is already in place.
             const long long RD = (long long)R * D, x0 = (long long)c.row0 * D, x1 = (long long)row1 * D;
-            const MtGroup grp = nthr >= 160 ? MtGroup{tid, 128, 3} : MtGroup{tid, nthr, 0};
+            const MtGroup grp = nthr >= 288 ? MtGroup{tid, 256, 3} : (nthr >= 160 ? MtGroup{tid, 128, 3} : MtGroup{tid, nthr, 0});
             MtState mt{mtbuf, 0, 0};
             SEPSO_IMARK(2);
             if (tid < grp.n) {
