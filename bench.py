@@ -54,6 +54,28 @@ def parse():
     return ap.parse_args()
 
 
+def committed_dram_bytes(kernel, grid):
+    """Mean DRAM bytes (read + write) per launch of `kernel` with this grid in the
+    committed ncu launch list (profiles/r01_bench_launches.csv), or None."""
+    import csv
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_bench_launches.csv")
+    try:
+        rows = list(csv.reader(open(path)))
+        hdr = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+        ix = {k: i for i, k in enumerate(rows[hdr])}
+        per = {}
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        for r in rows[hdr + 1:]:
+            if len(r) != len(rows[hdr]) or kernel not in r[ix["Kernel Name"]] or r[ix["Grid Size"]] != grid:
+                continue
+            if r[ix["Metric Name"]].startswith("dram__bytes_"):
+                per[r[ix["ID"]]] = per.get(r[ix["ID"]], 0.0) + float(r[ix["Metric Value"]].replace(",", "")) * \
+                    scale.get(r[ix["Metric Unit"]], 1.0)
+        return sum(per.values()) / len(per) if per else None
+    except (OSError, StopIteration, KeyError, ValueError):
+        return None
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -498,7 +520,9 @@ def main():
                 "peak_source": "measured FFMA probe (sf_measure_fp32_peak) on this GPU",
                 "unit": "TFLOP/s",
                 "frac": achieved / peak if peak else None,
-                "traffic": None,
+                "traffic": committed_dram_bytes("swarm_kernel<float, 1, 0>", "(16, 1, 1)"),
+                "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum per launch of this kernel, "
+                                  "profiles/r01_bench_launches.csv (ncu launch list of this bench, cold-cache replays)",
                 "flop_per_launch": flop_launch,
                 "flop_per_eval": FLOP_PER_EVAL(S, E),
                 "avg_launch_us": 1e3 * k_ms / k_n,
