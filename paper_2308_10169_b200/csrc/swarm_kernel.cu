@@ -113,7 +113,36 @@ struct LaunchDerived {
     SmemLayout lay;
     uint32_t xbytes;            // bytes every CTA receives per iteration
     uint32_t dmul[4], dshr[4];  // FastDiv of S, D, N, V (pushed-row units)
+    double at_var_bound;        // AT: sqrt_rn(v /rn tw) < delta  <=>  v < at_var_bound
 };
+
+// The AT decision std = sqrt(var / tw) < delta (planner.hpp:138-149) is
+// monotone in var (both operations correctly rounded), so it is exactly
+// "var < the smallest v >= 0 whose sqrt(v / tw) reaches delta" -- found once
+// on the host by bisection over the ordered bit patterns of non-negative
+// doubles, with the same IEEE operations.  Saves a division and a square root
+// per AT test on the device.
+static double at_var_bound(double delta, int tw) {
+    static thread_local double cd = std::numeric_limits<double>::quiet_NaN(), cv = 0.0;
+    static thread_local int ct = -1;
+    if (delta == cd && tw == ct) return cv;
+    double v;
+    if (!(delta > 0.0) || tw <= 0) {
+        v = 0.0;                                           // never below delta
+    } else {
+        uint64_t lo = 0, hi = 0x7FF0000000000000ull;       // +0 .. +inf
+        while (lo < hi) {
+            const uint64_t mid = lo + (hi - lo) / 2;
+            double x;
+            std::memcpy(&x, &mid, 8);
+            if (std::sqrt(x / double(tw)) >= delta) hi = mid;
+            else lo = mid + 1;
+        }
+        std::memcpy(&v, &lo, 8);
+    }
+    cd = delta; ct = tw; cv = v;
+    return v;
+}
 
 template <class T, bool PATH, bool RING>
 __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ SwarmParams p,
@@ -485,29 +514,30 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
                 }
                 __syncwarp();
                 // auto truncation (planner.hpp:181-187, 138-149) with Q(tbest)
-                // tracked.  Lane i holds window value i (oldest first); the sums
-                // stay sequential in that order, as in the reference.  The exact
-                // pre-test (std >= range / sqrt(2 tw)) skips hopeless windows.
-                // lane 0, sequentially in window order as in the reference; the
-                // exact pre-test (std >= range / sqrt(2 tw)) skips hopeless windows
+                // tracked: lane 0, the sums sequential in window order as in the
+                // reference (oldest first); each slot index comes from i alone so
+                // the loads run ahead of the add chain.  The exact pre-test
+                // (std >= range / sqrt(2 tw)) skips hopeless windows.
                 if (p.auto_truncate && wl >= p.tw && tbq == 0 && lane == 0) {
+                    const int tw = p.tw;
                     const double oldest = c.win[wh];
-                    const double newest = c.win[wh == 0 ? p.tw - 1 : wh - 1];
+                    const double newest = c.win[wh == 0 ? tw - 1 : wh - 1];
                     if (!(fabs(newest - oldest) >= p.at_gap)) {
                         double mean = 0.0;
-                        for (int i = 0, at = wh; i < p.tw; ++i) {
+#pragma unroll 4
+                        for (int i = 0; i < tw; ++i) {
+                            const int at = wh + i < tw ? wh + i : wh + i - tw;
                             mean = __dadd_rn(mean, c.win[at]);
-                            if (++at == p.tw) at = 0;
                         }
-                        mean = __ddiv_rn(mean, double(p.tw));
+                        mean = __ddiv_rn(mean, double(tw));
                         double var = 0.0;
-                        for (int i = 0, at = wh; i < p.tw; ++i) {
+#pragma unroll 4
+                        for (int i = 0; i < tw; ++i) {
+                            const int at = wh + i < tw ? wh + i : wh + i - tw;
                             const double dv = __dsub_rn(c.win[at], mean);
                             var = __dadd_rn(var, __dmul_rn(dv, dv));
-                            if (++at == p.tw) at = 0;
                         }
-                        var = __ddiv_rn(var, double(p.tw));
-                        if (__dsqrt_rn(var) < p.delta) { m->truncated = 1; m->stop = 1; }
+                        if (var < ld.at_var_bound) { m->truncated = 1; m->stop = 1; }
                     }
                 }
             }
@@ -733,6 +763,7 @@ static int launch_t(const SwarmParams& p, const ParamPayload* pl, int problem, c
             xb += 4;
         }
         ld.xbytes = xb;
+        ld.at_var_bound = at_var_bound(p.delta, p.tw);
         const int divs[4] = {Sv, Dv, p.N, row_units<T>(Dv)};
         for (int i = 0; i < 4; ++i) {
             FastDiv f;
