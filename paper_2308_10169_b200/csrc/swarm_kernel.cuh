@@ -7,9 +7,11 @@
 // row-major (g, n) order (swarm.hpp:18-49).  Per iteration:
 //   fitness (+ Q)           geometry.hpp:196-241 / benchmarks.hpp:56-88
 //   pbest + group partials  runner.hpp:68-80     (per CTA)
-//   cluster barrier, DSMEM gather of partials, gbest/tbest    runner.hpp:81-91
+//   partials (and their rows) pushed into every peer's shared memory with
+//   st.async, counted on the receiver's mbarrier -- no cluster barrier
+//   gbest/tbest             runner.hpp:81-91     (every CTA, same decisions)
 //   window push + AT test   planner.hpp:179-187, 138-149
-//   Philox draws + update   swarm.hpp:138-174
+//   step draws + update     swarm.hpp:59-70, 138-174 (mt19937_64 or Philox)
 // A grid of n_swarms clusters batches independent swarms (HSEF candidates,
 // planning queries, benchmark trials) into one launch.
 #pragma once
