@@ -17,8 +17,9 @@
  *  - Hyper matrices are G rows of (c1, c2, c3, omega_init, omega_end, v_limit),
  *    the HyperEncoding flatten order (hsef.hpp:41-55).
  *  - Particles use the reference layout: x-block then y-block (geometry.hpp:75-84).
- *  - Random streams follow the Philox draw contract of DESIGN.md: the draw
- *    ORDER and seeds are the reference's, the generator is Philox4x32-10.
+ *  - Random streams: the reference's draw ORDER and seeds;
+ *    the generator is the reference's own std::mt19937_64 by default
+ *    (SF_RNG_MT19937), or the counter-based Philox4x32-10 (SF_RNG_PHILOX).
  *  - Precision: SF_FP32 is the production engine; SF_FP64 reproduces the
  *    reference's FP64 arithmetic operation for operation (parity mode).
  */
@@ -32,14 +33,15 @@
 extern "C" {
 #endif
 
-#define SEPSO_ABI_VERSION 1
+#define SEPSO_ABI_VERSION 2
 
 typedef enum sf_status {
     SF_OK = 0,
     SF_INVALID_ARGUMENT = 1, /* std::invalid_argument */
     SF_NON_FINITE = 2,       /* NonFiniteFitnessError (runner.hpp:19-33) */
     SF_CUDA_ERROR = 3,
-    SF_UNSUPPORTED = 4       /* problem/shape the device engine does not cover */
+    SF_UNSUPPORTED = 4,      /* problem/shape the device engine does not cover */
+    SF_RUNTIME_ERROR = 5     /* std::runtime_error (e.g. generate_world placement, simenv.hpp:116-118) */
 } sf_status;
 
 typedef enum sf_precision { SF_FP32 = 0, SF_FP64 = 1 } sf_precision;
@@ -198,6 +200,10 @@ int sf_eval_bench_rows(sf_ctx* ctx, int kind, const double* xs, uint32_t rows, u
 int sf_should_truncate(const double* window, uint32_t len, int best_collision_free,
                        const sf_planner_config* cfg, int* result);
 
+/* derive_seed (rng.hpp:52-59): splitmix64(root ^ fnv1a64(tag)), and with an
+ * index splitmix64(derive_seed(root, tag) + index) when has_index != 0. */
+uint64_t sf_derive_seed(uint64_t root, const char* tag, size_t tag_len, int has_index, uint64_t index);
+
 /* ---- scene state (simenv.hpp; host C++) ---------------------------------- */
 typedef struct sf_scenario_config {                          /* ScenarioConfig, simenv.hpp:17-40 */
     double map_size;
@@ -216,9 +222,11 @@ int sf_generate_world(const sf_scenario_config* cfg, uint64_t seed, int rng, sf_
 int sf_step_world(sf_world* world, sf_point* vertices, sf_point* velocities, double dt);
 /* run_scenario (simenv.hpp:239-276): variant 0..5 = sepso, sepso-noat,
  * sepso-nopi, dtpso, dppso, pso; records[frames] out (best paths in
- * best (frames*dim) if not NULL). */
+ * best (frames*dim) if not NULL).  evolved_hypers holds evolved_groups rows;
+ * the variant's hyper matrix must have base->groups rows (priori_init,
+ * planner.hpp:83-84), else SF_INVALID_ARGUMENT. */
 int sf_run_scenario(sf_ctx* ctx, const sf_scenario_config* cfg, int variant, uint32_t frames,
-                    const sf_planner_config* base, const double* evolved_hypers,
+                    const sf_planner_config* base, const double* evolved_hypers, uint32_t evolved_groups,
                     sf_plan_record* records, double* best);
 
 /* ---- device-resident scenarios (run_scenario frame loop on the device) --- */

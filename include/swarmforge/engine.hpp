@@ -5,8 +5,8 @@
 // device SEPSO_DEVICE, default 0, precision SEPSO_PRECISION = fp32 | fp64,
 // default fp32) and maps sf_status codes back to the reference's exception
 // types: SF_INVALID_ARGUMENT -> std::invalid_argument, SF_NON_FINITE ->
-// swarmforge::NonFiniteFitnessError (runner.hpp), anything else ->
-// std::runtime_error.
+// swarmforge::NonFiniteFitnessError (runner.hpp), SF_RUNTIME_ERROR ->
+// std::runtime_error(message), anything else -> std::runtime_error.
 #pragma once
 
 #include <cstdint>
@@ -47,6 +47,7 @@ inline void check(int status, const std::uint64_t* bad = nullptr) {
     const std::string msg = sf_last_error();
     if (status == SF_INVALID_ARGUMENT) throw std::invalid_argument(msg);
     if (status == SF_NON_FINITE && bad) throw NonFiniteFitnessError(bad[0], bad[1], bad[2]);
+    if (status == SF_RUNTIME_ERROR) throw std::runtime_error(msg);
     throw std::runtime_error("sepso engine: " + msg);
 }
 

@@ -90,6 +90,9 @@ inline PlanRecord plan_frame(const PolygonWorld& world, const std::optional<Path
                              std::vector<double>* carried_window = nullptr) {
     config.validate();
     world.validate();
+    hypers.validate();
+    if (hypers.group_count() != config.groups)                      // planner.hpp:83-84
+        throw std::invalid_argument("priori_init: hyper matrix group count != G");
     if (prev_best && prev_best->waypoints.size() != config.waypoints())
         throw std::invalid_argument("priori_init: previous path waypoint count mismatch");
     const WorldView wv(world);

@@ -7,6 +7,6 @@ reference API for Python callers, tests and the benchmark.
 from .engine import (  # noqa: F401
     ABI_SYMBOLS, DEFAULT_GROUP_HYPERS, EVOLVED_PATH_HYPERS, CudaError, Engine,
     NonFiniteFitnessError, PlanRecord, SceneBatch, PlannerConfig, PolygonWorld, ScenarioConfig,
-    default_group_hypers, encode_path, evolved_path_hypers, generate_world, lib,
+    default_group_hypers, derive_seed, encode_path, evolved_path_hypers, generate_world, lib,
     should_truncate, step_world, LIB_PATH,
 )

@@ -51,6 +51,7 @@ extern "C" int sf_measure_fp32_peak(sf_ctx* ctx, double* tflops) {
     return SF_OK;
 }
 
+#ifdef SEPSO_PROFILE   // mt19937 pass-layout probe (tools/mtprobe.py): PROF builds only, not exported by the release library
 #include "mt19937.cuh"
 
 namespace sepso {
@@ -123,3 +124,5 @@ extern "C" int sf_debug_mt_probe(sf_ctx* ctx, long long blocks, int threads, int
     *cycles_per_block = double(h) / double(blocks);
     return SF_OK;
 }
+
+#endif  // SEPSO_PROFILE

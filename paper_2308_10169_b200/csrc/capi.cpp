@@ -961,9 +961,9 @@ int sf_generate_world(const sf_scenario_config* c, uint64_t seed, int rng_kind, 
             verts[4 * i + 3] = {cx - ow / 2.0, cy + oh / 2.0};
             placed = true;
         }
-        if (!placed)
-            return fail(SF_INVALID_ARGUMENT, "generate_world: could not place obstacle " + std::to_string(i) +
-                                                 " clear of start/target");
+        if (!placed)                                                 // simenv.hpp:116-118
+            return fail(SF_RUNTIME_ERROR, "generate_world: could not place obstacle " + std::to_string(i) +
+                                              " clear of start/target");
         offsets[i] = 4 * i;
         if (i < c->dynamic_obstacles) {
             const double speed = c->max_speed * (1.0 - rng.uniform());
@@ -978,7 +978,7 @@ int sf_generate_world(const sf_scenario_config* c, uint64_t seed, int rng_kind, 
     w->vertex_offsets = offsets;
     w->vertices = verts;
     w->velocities = vel;
-    return SF_OK;
+    return validate_world(w);                                        // world.validate(), simenv.hpp:129
 }
 
 static double reflect_axis(double lo, double hi, double limit, double& v) {   // simenv.hpp:139-149
@@ -1022,9 +1022,9 @@ int sf_step_world(sf_world* w, sf_point* verts, sf_point* vel, double dt) {
 
 // simenv.hpp:239-276 with variant wiring (188-234)
 int sf_run_scenario(sf_ctx* ctx, const sf_scenario_config* c, int variant, uint32_t frames,
-                    const sf_planner_config* base, const double* evolved, sf_plan_record* records,
-                    double* best) {
-    if (!ctx || !c || !base || !records) return fail(SF_INVALID_ARGUMENT, "null argument");
+                    const sf_planner_config* base, const double* evolved, uint32_t evolved_groups,
+                    sf_plan_record* records, double* best) {
+    if (!ctx || !c || !base || !records || !evolved) return fail(SF_INVALID_ARGUMENT, "null argument");
     if (frames < 1) return fail(SF_INVALID_ARGUMENT, "run_scenario: frame count must be >= 1");
     if (variant < 0 || variant > 5) return fail(SF_INVALID_ARGUMENT, "unknown planner variant");
     sf_planner_config cfg = *base;
@@ -1034,10 +1034,10 @@ int sf_run_scenario(sf_ctx* ctx, const sf_scenario_config* c, int variant, uint3
                                         2, 1, 2, 0.2, 0.1, 0.3, 2, 1, 2, 0.9, 0.5, 0.5,
                                         1, 2, 2, 0.4, 0.1, 0.8, 1, 2, 2, 0.9, 0.3, 0.3};
     switch (variant) {
-    case 0: hyp.assign(evolved, evolved + 6 * cfg.groups); break;                  // sepso
+    case 0: hyp.assign(evolved, evolved + 6 * size_t(evolved_groups)); break;      // sepso
     case 1: cfg.auto_truncate = 0; cfg.max_iters_per_frame = 30;
-            hyp.assign(evolved, evolved + 6 * cfg.groups); break;                  // sepso-noat
-    case 2: cfg.gamma = 0.0; hyp.assign(evolved, evolved + 6 * cfg.groups); break; // sepso-nopi
+            hyp.assign(evolved, evolved + 6 * size_t(evolved_groups)); break;      // sepso-noat
+    case 2: cfg.gamma = 0.0; hyp.assign(evolved, evolved + 6 * size_t(evolved_groups)); break; // sepso-nopi
     case 3: case 4:                                                                // dtpso / dppso
         cfg.gamma = 0.0; cfg.auto_truncate = 0; cfg.max_iters_per_frame = 30;
         hyp.assign(defaults, defaults + 48);
@@ -1049,6 +1049,12 @@ int sf_run_scenario(sf_ctx* ctx, const sf_scenario_config* c, int variant, uint3
         hyp = {2.0, 2.0, 0.0, 0.9, 0.4, 0.5};
         break;
     }
+    // priori_init's checks (planner.hpp:80-84) before any frame runs
+    int vs = validate_planner(&cfg);
+    if (vs) return vs;
+    if (hyp.size() != 6 * size_t(cfg.groups))
+        return fail(SF_INVALID_ARGUMENT, "priori_init: hyper matrix group count != G");
+    if ((vs = validate_hypers(hyp.data(), cfg.groups))) return vs;
     sf_scenario_config sc = *c;
     sc.frames = std::max<uint32_t>(sc.frames, 1);
     const uint32_t n = c->dynamic_obstacles + c->static_obstacles;
@@ -1083,6 +1089,11 @@ int sf_run_scenario(sf_ctx* ctx, const sf_scenario_config* c, int variant, uint3
     return SF_OK;
 }
 
+uint64_t sf_derive_seed(uint64_t root, const char* tag, size_t tag_len, int has_index, uint64_t index) {
+    const uint64_t d = splitmix64(root ^ fnv1a64(tag ? tag : "", tag ? tag_len : 0));   // rng.hpp:52-54
+    return has_index ? splitmix64(d + index) : d;                                       // rng.hpp:56-59
+}
+
 int sf_comm_unique_id(uint8_t id[128]) {
     if (!id) return fail(SF_INVALID_ARGUMENT, "id is null");
     return comm_unique_id(id);
@@ -1091,6 +1102,7 @@ int sf_comm_unique_id(uint8_t id[128]) {
 int sf_ctx_init_comm(sf_ctx* ctx, const uint8_t id[128], int nranks, int rank) {
     if (!ctx || !id) return fail(SF_INVALID_ARGUMENT, "null argument");
     if (nranks < 1 || rank < 0 || rank >= nranks) return fail(SF_INVALID_ARGUMENT, "bad rank / world size");
+    if (nranks > 64) return fail(SF_INVALID_ARGUMENT, "sharded swarm: at most 64 ranks");   // k_finish candidate table
     DeviceGuard guard(ctx->device);
     if (ctx->comm) comm_destroy(ctx->comm);
     ctx->comm = nullptr;
@@ -1182,6 +1194,8 @@ int sf_scene_batch_create(sf_ctx* ctx, uint32_t n, const sf_scenario_config* cfg
                           const sf_planner_config* cfg, const double* hypers, uint32_t max_frames,
                           sf_scene_batch** out) {
     if (!ctx || !cfgs || !out || n == 0 || max_frames == 0) return fail(SF_INVALID_ARGUMENT, "bad scene batch arguments");
+    for (uint32_t s = 1; s < n; ++s)      // one dt steps every world record of the batch
+        if (cfgs[s].dt != cfgs[0].dt) return fail(SF_INVALID_ARGUMENT, "scene batch: every scenario must share dt");
     DeviceGuard guard(ctx->device);
     int st = validate_planner(cfg);
     if (st) return st;

@@ -374,7 +374,8 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
     const size_t o_trace = take(size_t(r.cap) * 8);
     const bool mt = ctx->rng == SF_RNG_MT19937;
     const size_t o_mt = take(mt ? sizeof(MtPersist) : 0);
-    const size_t o_words = take(mt ? size_t(2) * R * D * 8 : 0);   // init window; steps reuse it
+    // init window (2RD words); each step's 3R draws reuse it, so it holds the larger of the two
+    const size_t o_words = take(mt ? std::max(size_t(2) * R * D, size_t(3) * R) * 8 : 0);
     // long init windows are generated in parallel segments from jumped states
     const long long init_words = 2ll * R * D;
     int jlevels = 0;

@@ -147,12 +147,14 @@ int stage_mt_fill_parallel(MtPersist* g, unsigned long long seed, long long upto
                            unsigned long long* states, const unsigned long long* polys, int levels, long long Q,
                            void* stream) {
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
-    static thread_local bool attr = false;
-    if (!attr) {
+    static thread_local unsigned attr = 0;          // function attributes are per device: one bit each
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 32 || !(attr >> dev & 1u)) {
         const cudaError_t e = cudaFuncSetAttribute(k_mt_jump, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    int(mt_jump_smem_bytes()));
         if (e != cudaSuccess) return int(e);
-        attr = true;
+        if (dev < 32) attr |= 1u << dev;
     }
     k_mt_seed_state<<<1, 32, 0, st>>>(states, seed);
     for (int j = 0; j < levels; ++j) {

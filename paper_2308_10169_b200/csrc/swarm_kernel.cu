@@ -720,6 +720,8 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
 }
 
 // ------------------------------------------------------------------ launcher
+constexpr int kMaxDevices = 64;
+
 template <class T, bool PATH, bool RING>
 static int launch_t(const SwarmParams& p, const ParamPayload* pl, int problem, cudaStream_t st,
                     size_t* smem_out) {
@@ -727,17 +729,21 @@ static int launch_t(const SwarmParams& p, const ParamPayload* pl, int problem, c
     if (smem_out) *smem_out = L.total;
     auto kern = swarm_kernel<T, PATH, RING>;
     cudaError_t e = cudaSuccess;
-    static thread_local size_t smem_set = 0;     // attributes are sticky per function
-    static thread_local bool nonportable = false;
-    if (L.total > smem_set) {
+    // attributes are sticky per function AND per device: cache them per ordinal
+    static thread_local size_t smem_set[kMaxDevices] = {};
+    static thread_local bool nonportable[kMaxDevices] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const bool cached = dev >= 0 && dev < kMaxDevices;
+    if (!cached || L.total > smem_set[dev]) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.total));
         if (e != cudaSuccess) return int(e);
-        smem_set = L.total;
+        if (cached) smem_set[dev] = L.total;
     }
-    if (p.C > 8 && !nonportable) {
+    if (p.C > 8 && (!cached || !nonportable[dev])) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return int(e);
-        nonportable = true;
+        if (cached) nonportable[dev] = true;
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(p.n_swarms * p.C));
@@ -856,10 +862,12 @@ __global__ void k_step_worlds(unsigned char* worlds, int n, long long stride, in
 int launch_step_worlds(unsigned char* worlds, int n, long long stride, int off_offsets,
                        int off_verts, int off_vel, double dt, void* stream) {
     if (n <= 0) return 0;
-    static bool carve = false;       // keep the SM shared-memory split of the planning kernel
-    if (!carve) {
+    static thread_local bool carve[kMaxDevices] = {};   // keep the SM shared-memory split of the planning kernel
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDevices || !carve[dev]) {
         cudaFuncSetAttribute(k_step_worlds, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        carve = true;
+        if (dev >= 0 && dev < kMaxDevices) carve[dev] = true;
     }
     k_step_worlds<<<n, 128, 0, static_cast<cudaStream_t>(stream)>>>(
         worlds, n, stride, off_offsets, off_verts, off_vel, dt);

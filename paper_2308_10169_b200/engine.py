@@ -22,7 +22,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SEPSO_LIB") or os.path.join(_HERE, "lib", "libsepso_cuda.so")
 
-SF_OK, SF_INVALID_ARGUMENT, SF_NON_FINITE, SF_CUDA_ERROR, SF_UNSUPPORTED = range(5)
+SF_OK, SF_INVALID_ARGUMENT, SF_NON_FINITE, SF_CUDA_ERROR, SF_UNSUPPORTED, SF_RUNTIME_ERROR = range(6)
 FP32, FP64 = 0, 1
 PROBLEMS = {"path": 0, "BF1": 1, "BF2": 2, "BF3": 3, "BF4": 4, "ACKLEY": 5,
             "sphere": 1, "rosenbrock": 2, "rastrigin": 3, "griewank": 4, "ackley": 5}
@@ -39,7 +39,7 @@ ABI_SYMBOLS = [
     "sf_scene_batch_run", "sf_scene_batch_records", "sf_scene_batch_destroy",
     "sf_ctx_last_io_bytes", "sf_measure_fp32_peak", "sf_ctx_set_l2_flush",
     "sf_comm_unique_id", "sf_ctx_init_comm", "sf_plan_frame_sharded", "sf_ctx_set_rng",
-    "sf_ctx_rng", "sf_mt_jump_poly",
+    "sf_ctx_rng", "sf_mt_jump_poly", "sf_derive_seed",
 ]
 RNGS = {"philox": 0, "mt19937": 1}
 
@@ -123,6 +123,7 @@ def lib():
     W, P, Pr = C.POINTER(_World), C.POINTER(_PlannerCfg), C.POINTER(_PlanRecord)
     sig = {
         "sf_abi_version": (C.c_int, []),
+        "sf_derive_seed": (C.c_uint64, [C.c_uint64, C.c_char_p, C.c_size_t, C.c_int, C.c_uint64]),
         "sf_last_error": (C.c_char_p, []),
         "sf_ctx_create": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
         "sf_ctx_destroy": (C.c_int, [C.c_void_p]),
@@ -163,7 +164,7 @@ def lib():
                                         C.POINTER(_Point), C.POINTER(_Point)]),
         "sf_step_world": (C.c_int, [W, C.POINTER(_Point), C.POINTER(_Point), C.c_double]),
         "sf_run_scenario": (C.c_int, [C.c_void_p, C.POINTER(_ScenarioCfg), C.c_int, C.c_uint32,
-                                      P, _dp, Pr, _dp]),
+                                      P, _dp, C.c_uint32, Pr, _dp]),
         "sf_scene_batch_create": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(_ScenarioCfg), P,
                                             _dp, C.c_uint32, C.POINTER(C.c_void_p)]),
         "sf_scene_batch_run": (C.c_int, [C.c_void_p, C.c_uint32]),
@@ -205,6 +206,8 @@ def _check(status, bad=None):
         raise NonFiniteFitnessError(b[0], b[1], b[2], msg)
     if status == SF_UNSUPPORTED:
         raise NotImplementedError(msg)
+    if status == SF_RUNTIME_ERROR:
+        raise RuntimeError(msg)
     raise CudaError(msg)
 
 
@@ -348,6 +351,12 @@ def encode_path(waypoints) -> np.ndarray:
     """geometry.hpp:86-94: (W, 2) waypoints -> [x_1..x_W, y_1..y_W]."""
     w = np.asarray(waypoints, dtype=np.float64).reshape(-1, 2)
     return np.concatenate([w[:, 0], w[:, 1]])
+
+
+def derive_seed(root: int, tag: str, index: Optional[int] = None) -> int:
+    """rng.hpp:52-59 (named sub-stream seeds), computed by the engine library."""
+    t = tag.encode()
+    return int(lib().sf_derive_seed(root, t, len(t), 0 if index is None else 1, 0 if index is None else index))
 
 
 def generate_world(config: ScenarioConfig, seed: int, rng: str = "mt19937") -> PolygonWorld:
@@ -656,8 +665,10 @@ class Engine:
         recs = (_PlanRecord * frames)()
         dim = base.dim
         best = np.zeros((frames, dim))
+        if ev.size % 6 != 0:
+            raise ValueError("HyperMatrix: rows of 6 values required")
         _check(self._L.sf_run_scenario(self._h, C.byref(config._c()), VARIANTS.index(variant),
-                                       frames, C.byref(base._c()), _p(ev), recs, _p(best)))
+                                       frames, C.byref(base._c()), _p(ev), ev.size // 6, recs, _p(best)))
         return [PlanRecord._from(recs[i], best[i]) for i in range(frames)]
 
 

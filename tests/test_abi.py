@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert sorted(E.ABI_SYMBOLS) == syms
-    assert lib.sf_abi_version() == 1
+    assert lib.sf_abi_version() == 2
 
 
 def test_library_is_sm100a_cuda():
