@@ -13,6 +13,7 @@ import os
 import numpy as np
 import pytest
 
+from oracle_lib import ROOT
 from oracle_lib import (DEFAULT_GROUP_HYPERS, EVOLVED_PATH_HYPERS, RNG_MT, RNG_PHILOX, WorldBuf,
                         generate_world, oracle, oracle_plan_frame, oracle_run_dtpso, planner_cfg,
                         ptr, rect, ref, ref_plan_frame, u32p)
@@ -320,3 +321,32 @@ def test_live_plan_frames_random_worlds():
             assert (a[1].fitness, a[1].iterations, a[1].truncated) == (b[1].fitness, b[1].iterations, b[1].truncated)
             assert a[2].tolist() == b[2].tolist() and a[3].tolist() == b[3].tolist()
             prev, win_o, win_r = a[2], a[3], b[3]
+
+
+def test_glibc_cos_restatement(tmp_path):
+    """The FP64 engine's cos (csrc/cos_glibc.cuh, the restated glibc 2.39 FMA
+    build of s_sin.c), compiled for the host, equals libm's cos bit for bit on
+    the benchmarks' argument distributions (2*pi*x and x/sqrt(i+1) over the
+    box [-600, 600]) and on every branch of the algorithm."""
+    import shutil
+    import subprocess
+    if shutil.which("g++") is None:
+        pytest.skip("g++ not available")
+    so = str(tmp_path / "libcoscheck.so")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-shared", "-fPIC",
+                    "-I" + os.path.join(ROOT, "paper_2308_10169_b200", "csrc"),
+                    os.path.join(ROOT, "tests", "cpp", "cos_check.cpp"), "-o", so], check=True)
+    ours = C.CDLL(so)
+    libm = C.CDLL("libm.so.6")
+    libm.cos.restype, libm.cos.argtypes = C.c_double, [C.c_double]
+    g = np.random.default_rng(21)
+    n = 400_000
+    p = g.uniform(-600, 600, n)
+    xs = np.concatenate([2.0 * np.pi * p, p / np.sqrt(g.integers(1, 31, n)), g.uniform(-1, 1, n),
+                         g.uniform(-3, 3, n), np.round(p) * 2 * np.pi, g.uniform(-1e5, 1e5, n),
+                         g.uniform(-1e-7, 1e-7, 1000), [0.0, -0.0, 0.126, -0.126, 0.855469, 2.426265]])
+    got = np.zeros_like(xs)
+    ours.cos_glibc_rows(ptr(xs), len(xs), ptr(got))
+    # libm through a vectorised ufunc would be numpy's own cos: call libm itself
+    want = np.array([libm.cos(float(v)) for v in xs[::7]])
+    assert np.array_equal(got[::7], want)
