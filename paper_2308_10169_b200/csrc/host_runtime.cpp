@@ -256,8 +256,15 @@ int launch_fused(sf_ctx* ctx, FusedPlan& fp, int problem) {
         cudaMemsetAsync(prof, 0, sizeof(long long) * nprof, ctx->stream);
         fp.p.prof = prof;
     }
+    cudaEvent_t pe0 = nullptr, pe1 = nullptr;
+    if (prof) {
+        cudaEventCreate(&pe0);
+        cudaEventCreate(&pe1);
+        cudaEventRecord(pe0, ctx->stream);
+    }
     const int e = launch_swarms(fp.p, fp.p.inl ? fp.payload : nullptr, problem, ctx->precision == SF_FP64,
                                 ctx->stream, &smem);
+    if (prof) cudaEventRecord(pe1, ctx->stream);
     if (prof) {
         std::vector<long long> h(size_t(kProfPhases) * (fp.p.cap + 1) + 2 * 16 * size_t(fp.p.cap));
         cudaMemcpyAsync(h.data(), prof, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream);
@@ -286,12 +293,32 @@ int launch_fused(sf_ctx* ctx, FusedPlan& fp, int problem) {
             g0 += double(r[12] - r[8]); g1 += double(r[13] - r[12]); b1 += double(r[14] - r[8]);
         }
         if (gi) std::fprintf(stderr, " | B1work=%.0f gen_start=%.0f gen=%.0f", b1 / gi, g0 / gi, g1 / gi);
+        {   // inside B1 (warp 0): bad-row reduce, gbest scan, tbest reduce, window push, AT
+            double q[5] = {0};
+            int qi = 0;
+            for (int k = 0; k < iters; ++k) {
+                const long long* r = h.data() + size_t(k) * kProfPhases;
+                if (r[15] == 0 || r[16] == 0 || r[17] == 0 || r[18] == 0 || r[14] == 0) continue;
+                ++qi;
+                q[0] += double(r[15] - r[8]); q[1] += double(r[16] - r[15]); q[2] += double(r[17] - r[16]);
+                q[3] += double(r[18] - r[17]); q[4] += double(r[14] - r[18]);
+                if (std::getenv("SEPSO_ATTWICE") && r[20] > r[18])
+                    std::fprintf(stderr, "[at] first=%lld second=%lld\n", r[20] - r[18], r[21] - r[20]);
+            }
+            if (qi) std::fprintf(stderr, " | B1: bad=%.0f gbest=%.0f tbest=%.0f push=%.0f at=%.0f", q[0] / qi,
+                                 q[1] / qi, q[2] / qi, q[3] / qi, q[4] / qi);
+        }
         {   // init marks (row cap): start, consts, seeded, x, v, rest, put, loop
             const long long* r = h.data() + size_t(fp.p.cap) * kProfPhases;
             std::fprintf(stderr, " | init: consts=%lld seed=%lld x=%lld v=%lld rest=%lld sync=%lld",
                          r[1] - r[0], r[2] - r[1], r[3] - r[2], r[4] - r[3], r[5] - r[4], r[6] - r[5]);
             std::fprintf(stderr, " | ns: init=%lld loop=%lld out=%lld exit=%lld total=%lld",
                          r[8] - r[7], r[9] - r[8], r[10] - r[9], r[11] - r[10], r[11] - r[7]);
+            float ev_ms = 0.f;
+            cudaEventElapsedTime(&ev_ms, pe0, pe1);
+            std::fprintf(stderr, " | entry->g7=%lld event=%.0f", r[7] - r[12], 1e6 * double(ev_ms));
+            cudaEventDestroy(pe0);
+            cudaEventDestroy(pe1);
             // per-CTA work before the partial exchange (cycles): spread over CTAs
             const long long* w = h.data() + size_t(kProfPhases) * (fp.p.cap + 1);
             double smin = 0, smax = 0, sown = 0;

@@ -144,11 +144,86 @@ static double at_var_bound(double delta, int tw) {
     return v;
 }
 
-template <class T, bool PATH, bool RING>
-__global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ SwarmParams p,
+// AT statistic of the window (planner.hpp:138-149) by one warp in parallel.
+// The reference sums sequentially: mean_s = (sum w_i) / tw, var_s = sum (w_i -
+// mean_s)^2.  Any summation order of n = tw terms is within gamma_{n-1} sum|w|
+// of the exact sum, so both means are within dl = 1.01 (n + 2) u M of the
+// exact mean mu (M = max |w|, u = 2^-53); with V(m) = V(mu) + n (m - mu)^2 and
+// the squared-difference terms off by <= 3u each, |var_s - var_p| <=
+// 2.04 (n + 3) u (var_p + n dl^2) + 2 n dl^2 < E (a factor 2 to spare).
+// Returns 1 when var_s < bound for certain, 0 when var_s >= bound for certain,
+// -1 when the caller must evaluate the sequential sums.  All lanes return it.
+__device__ __forceinline__ int at_decide_parallel(const double* win, int wh, int tw, double bound, int lane) {
+    double s = 0.0, mx = 0.0;
+    for (int i = lane; i < tw; i += 32) {
+        const int at = wh + i < tw ? wh + i : wh + i - tw;
+        const double w = win[at];
+        s += w;
+        mx = fmax(mx, fabs(w));
+    }
+    for (int off = 16; off; off >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, off);
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    }
+    const double mean = s / double(tw);
+    double v = 0.0;
+    for (int i = lane; i < tw; i += 32) {
+        const int at = wh + i < tw ? wh + i : wh + i - tw;
+        const double d = win[at] - mean;
+        v = fma(d, d, v);
+    }
+    for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    const double n = double(tw), u = 0x1p-53;
+    const double dl = 1.01 * (n + 2.0) * u * mx;
+    const double E = 4.0 * (n + 3.0) * u * (v + n * dl * dl) + 4.0 * n * dl * dl;
+    if (v + E < bound) return 1;
+    if (v - E >= bound) return 0;
+    return -1;
+}
+
+// The same decision from registers (tw <= 32, lane i holds window slot i), in
+// one centred pass: d_i = w_i - c (c = the newest value), S = sum d, Q = sum
+// d^2, V = Q - S^2 / tw.  With X >= max |d_i| (REDUX on the high words) the
+// rounding of this pass stays within 24.5 u n X^2 of the exact V(mu) (d_i and
+// d_i^2 relative 3u, 5-level trees gamma_5, S^2 / n three roundings, the final
+// difference one), and the reference's sequential value within 2.04 (n + 3) u
+// n X^2 + n dl^2 of it (see at_decide_parallel), so E below bounds |var_s - V|
+// with margin.  Returns 1 / 0 when certain, -1 inside the band.
+__device__ __forceinline__ int at_decide_regs(double w, int lane, int tw, double c, double inv_n, double bound) {
+    const bool act = lane < tw;
+    const double d = act ? w - c : 0.0;
+    double s = d, q = d * d;
+    const uint32_t hx = __reduce_max_sync(0xffffffffu, act ? uint32_t(uint64_t(__double_as_longlong(fabs(d))) >> 32) : 0u);
+    const uint32_t hm = __reduce_max_sync(0xffffffffu, act ? uint32_t(uint64_t(__double_as_longlong(fabs(w))) >> 32) : 0u);
+    for (int off = 16; off; off >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, off);
+        q += __shfl_xor_sync(0xffffffffu, q, off);
+    }
+    const double X = __longlong_as_double((long long)((uint64_t(hx) << 32) | 0xffffffffull));
+    const double M = __longlong_as_double((long long)((uint64_t(hm) << 32) | 0xffffffffull));
+    const double n = double(tw), u = 0x1p-53;
+    const double dl = 1.01 * (n + 2.0) * u * M;
+    const double E = (3.0 * n + 40.0) * u * n * X * X + 2.0 * n * dl * dl;
+    const double v = q - s * s * inv_n;
+    if (!(v == v) || !(E == E) || E > 0x1p1000) return -1;   // non-finite window: the sequential sums decide
+    if (v + E < bound) return 1;
+    if (v - E >= bound) return 0;
+    return -1;
+}
+
+// MAXT: the largest block size the instantiation launches with.  The register
+// budget follows from it (64 at 1024 threads, 72 at 896): the latency launch of
+// one paper scene (85 rows x 9 segments + 4 generator warps = 896 threads) gets
+// its own instantiation so its hot loop does not spill at the 1024-thread cap.
+template <class T, bool PATH, bool RING, int MAXT = 1024>
+__global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ SwarmParams p,
                                                         const __grid_constant__ ParamPayload pl,
                                                         const __grid_constant__ LaunchDerived ld, int problem) {
     using A = Ar<T>;
+#ifdef SEPSO_PROFILE
+    unsigned long long g_entry_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry_));
+#endif
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ __align__(16) unsigned char smem[];
     const SmemLayout& L = ld.lay;
@@ -202,6 +277,9 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
 #define SEPSO_GMARK(ph) do { if (kProfiling && prof) { unsigned long long g_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_)); prof[p.cap * kProfPhases + (ph)] = (long long)g_; } } while (0)
     SEPSO_IMARK(0);
     SEPSO_GMARK(7);
+#ifdef SEPSO_PROFILE
+    if (prof) prof[p.cap * kProfPhases + 12] = (long long)g_entry_;
+#endif
 
     // ---------------------------------------------------------- constants
     // With the mt19937 stream, the last warp's lane 0 seeds the generator
@@ -324,6 +402,25 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
 
     // ------------------------------------------------------------ iterations
     if (p.cap < 1) cluster_wait();
+    // Best update fast path (FP32, G <= 32, tw <= 32): warp 0 keeps the bests
+    // and the AT window in registers -- lane g group g's gbest value and Q,
+    // lane i window slot i -- so the chain of the single-warp phase is a few
+    // warp collectives instead of shared-memory round trips; spilled to Misc /
+    // c.win when the loop ends.
+    const bool b1fast = sizeof(T) == 4 && G <= 32 && p.tw <= 32;
+    float r_gbf = __int_as_float(0x7f800000), r_tbf = __int_as_float(0x7f800000);
+    int r_gbq = 0, r_tbq = 0, r_wl = 0, r_wh = 0, r_cf = 0, r_cl = -1, r_s0 = 0;
+    double r_win = 0.0;
+    if (b1fast && warp == 0) {
+        r_wl = c.m->win_len;
+        if (lane < p.tw) r_win = c.win[lane];
+        if (lane < G) {
+            r_cf = c.gtab[2 * lane];
+            r_cl = c.gtab[2 * lane + 1];
+            r_s0 = r_cf * LGM + (lane - c.ctab[r_cf]);
+        }
+    }
+    const double inv_tw = p.tw > 0 ? 1.0 / double(p.tw) : 0.0;
     int k = 1;
     for (; k <= p.cap; ++k) {
         const int buf = k & 1;
@@ -449,13 +546,94 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
 
         // partials were pushed before the barrier: nothing to gather
         SEPSO_MARK(8);
-        if (warp == 0) {
+        if (warp == 0 && b1fast) {
+            Misc<T>* m = c.m;
+            const int bad = int(__reduce_min_sync(0xffffffffu, lane < c.C ? uint32_t(c.allbad[buf * c.C + lane])
+                                                                            : 0xffffffffu));
+            SEPSO_MARK(15);
+            if (bad != INT_MAX) {
+                if (lane == 0) { m->status = 2; m->bad_min = bad; m->stop = 1; }
+            } else {
+                // gbest, lane g: the owning CTAs' partials in row order, strict
+                // '<' vs the incumbent (runner.hpp:81-87).  Later CTAs of a
+                // group start inside it, so its partial is their local group 0.
+                const Part* parts = c.part + size_t(buf) * c.C * LGM;
+                double bf = double(A::inf());
+                int bslot = -1, bq = 0;
+                for (int cc = r_cf; cc <= r_cl; ++cc) {
+                    const int slot = cc == r_cf ? r_s0 : cc * LGM;
+                    const Part pt = parts[slot];
+                    if (pt.f < bf) { bf = pt.f; bslot = slot; bq = pt.q; }
+                }
+                if (lane < G) {
+                    int ch = -1;
+                    if (float(bf) < r_gbf) { r_gbf = float(bf); r_gbq = bq; ch = bslot; }
+                    c.chg[lane] = ch;
+                }
+                SEPSO_MARK(16);
+                // tbest: (gbest_f, g) lexicographic min, strict '<' vs the
+                // incumbent (runner.hpp:88-91): one REDUX on ordered keys, the
+                // lowest lane holding the minimum
+                const uint32_t key = lane < G ? order_key(r_gbf) : 0xffffffffu;
+                const uint32_t kmin = __reduce_min_sync(0xffffffffu, key);
+                const int tg = __ffs(__ballot_sync(0xffffffffu, key == kmin)) - 1;
+                const float tv = __shfl_sync(0xffffffffu, r_gbf, tg);
+                const int tq = __shfl_sync(0xffffffffu, r_gbq, tg);
+                const bool tnew = tv < r_tbf;
+                if (tnew) { r_tbf = tv; r_tbq = tq; }
+                const double tb = double(r_tbf);
+                SEPSO_MARK(17);
+                // trace, window push + trim to tw (planner.hpp:179-180): lane
+                // `at` takes the new value
+                const int tw = p.tw;
+                if (lane == 0) {
+                    m->tsrc_slot = tnew ? tg : -1;
+                    if (c.crank == 0) p.trace[size_t(swarm) * p.cap + (k - 1)] = tb;
+                }
+                if (tw > 0) {
+                    int at = r_wh + r_wl;
+                    if (r_wl == tw) at = r_wh;
+                    else if (at >= tw) at -= tw;
+                    if (lane == at) r_win = tb;
+                    if (r_wl < tw) ++r_wl;
+                    else if (++r_wh == tw) r_wh = 0;
+                }
+                SEPSO_MARK(18);
+                // auto truncation (planner.hpp:181-187, 138-149): the exact
+                // range pre-test, then the certified parallel estimate, then
+                // -- only inside its error band -- the reference's sequential
+                // sums in window order, oldest first
+                if (p.auto_truncate && r_wl >= tw && r_tbq == 0) {
+                    const double oldest = __shfl_sync(0xffffffffu, r_win, r_wh);
+                    const double newest = __shfl_sync(0xffffffffu, r_win, r_wh == 0 ? tw - 1 : r_wh - 1);
+                    if (!(fabs(newest - oldest) >= p.at_gap)) {
+                        int dec = at_decide_regs(r_win, lane, tw, newest, inv_tw, ld.at_var_bound);
+                        if (dec < 0) {
+                            double mean = 0.0;
+                            for (int i = 0; i < tw; ++i)
+                                mean = __dadd_rn(mean, __shfl_sync(0xffffffffu, r_win, r_wh + i < tw ? r_wh + i : r_wh + i - tw));
+                            mean = __ddiv_rn(mean, double(tw));
+                            double var = 0.0;
+                            for (int i = 0; i < tw; ++i) {
+                                const double dv = __dsub_rn(__shfl_sync(0xffffffffu, r_win, r_wh + i < tw ? r_wh + i : r_wh + i - tw), mean);
+                                var = __dadd_rn(var, __dmul_rn(dv, dv));
+                            }
+                            dec = var < ld.at_var_bound ? 1 : 0;
+                        }
+                        if (dec > 0 && lane == 0) { m->truncated = 1; m->stop = 1; }
+                    }
+                }
+            }
+            if (lane == 0) m->k_done = k;
+            SEPSO_MARK(14);
+        } else if (warp == 0) {
             // gbest, one lane per group: scan the owning CTAs in row order,
             // strict '<' vs the incumbent (runner.hpp:81-87)
             Misc<T>* m = c.m;
             int bad = INT_MAX;
             for (int cc = lane; cc < c.C; cc += 32) bad = min(bad, c.allbad[buf * c.C + cc]);
             bad = int(__reduce_min_sync(0xffffffffu, uint32_t(bad)));
+            SEPSO_MARK(15);
             if (bad != INT_MAX) {
                 if (lane == 0) { m->status = 2; m->bad_min = bad; m->stop = 1; }
             } else {
@@ -474,6 +652,7 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
                     else c.chg[g] = -1;
                     if (c.gbf[g] < tv) { tv = c.gbf[g]; tg = g; }       // per-lane, g ascending
                 }
+                SEPSO_MARK(16);
                 // tbest: (gbest_f, g) lexicographic min over groups, strict '<'
                 // vs the incumbent (runner.hpp:88-91)
                 if (sizeof(T) == 4) {          // ordered keys: two warp reductions
@@ -488,6 +667,7 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
                         if (ov < tv || (ov == tv && og < tg)) { tv = ov; tg = og; }
                     }
                 }
+                SEPSO_MARK(17);
                 // tbest update, trace, window push + trim to tw (planner.hpp:179-180)
                 const bool tnew = tv < m->tbf;
                 const double tb = double(tnew ? tv : m->tbf);
@@ -513,31 +693,40 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
                     m->win_head = wh;
                 }
                 __syncwarp();
+                SEPSO_MARK(18);
                 // auto truncation (planner.hpp:181-187, 138-149) with Q(tbest)
-                // tracked: lane 0, the sums sequential in window order as in the
-                // reference (oldest first); each slot index comes from i alone so
-                // the loads run ahead of the add chain.  The exact pre-test
-                // (std >= range / sqrt(2 tw)) skips hopeless windows.
-                if (p.auto_truncate && wl >= p.tw && tbq == 0 && lane == 0) {
+                // tracked.  The exact pre-test (std >= range / sqrt(2 tw))
+                // skips hopeless windows.  Otherwise the warp estimates the
+                // statistic in parallel (tree sums) and decides whenever the
+                // estimate clears the threshold by more than a rigorous bound
+                // on its distance from the reference's sequential value; only
+                // inside that band (|var - bound| ~ 1e-14 relative) does lane 0
+                // redo the sums sequentially in window order, oldest first, as
+                // the reference does.
+                if (p.auto_truncate && wl >= p.tw && tbq == 0) {
                     const int tw = p.tw;
                     const double oldest = c.win[wh];
                     const double newest = c.win[wh == 0 ? tw - 1 : wh - 1];
                     if (!(fabs(newest - oldest) >= p.at_gap)) {
-                        double mean = 0.0;
+                        const int dec = at_decide_parallel(c.win, wh, tw, ld.at_var_bound, lane);
+                        if (dec > 0 && lane == 0) { m->truncated = 1; m->stop = 1; }
+                        if (dec < 0 && lane == 0) {
+                            double mean = 0.0;
 #pragma unroll 4
-                        for (int i = 0; i < tw; ++i) {
-                            const int at = wh + i < tw ? wh + i : wh + i - tw;
-                            mean = __dadd_rn(mean, c.win[at]);
-                        }
-                        mean = __ddiv_rn(mean, double(tw));
-                        double var = 0.0;
+                            for (int i = 0; i < tw; ++i) {
+                                const int at = wh + i < tw ? wh + i : wh + i - tw;
+                                mean = __dadd_rn(mean, c.win[at]);
+                            }
+                            mean = __ddiv_rn(mean, double(tw));
+                            double var = 0.0;
 #pragma unroll 4
-                        for (int i = 0; i < tw; ++i) {
-                            const int at = wh + i < tw ? wh + i : wh + i - tw;
-                            const double dv = __dsub_rn(c.win[at], mean);
-                            var = __dadd_rn(var, __dmul_rn(dv, dv));
+                            for (int i = 0; i < tw; ++i) {
+                                const int at = wh + i < tw ? wh + i : wh + i - tw;
+                                const double dv = __dsub_rn(c.win[at], mean);
+                                var = __dadd_rn(var, __dmul_rn(dv, dv));
+                            }
+                            if (var < ld.at_var_bound) { m->truncated = 1; m->stop = 1; }
                         }
-                        if (var < ld.at_var_bound) { m->truncated = 1; m->stop = 1; }
                     }
                 }
             }
@@ -662,6 +851,15 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
         SEPSO_MARK(11);
     }
 
+    if (b1fast && warp == 0) {             // the fast path's registers -> Misc / c.win
+        if (lane == 0) {
+            c.m->tbf = r_tbf; c.m->tbq = r_tbq;
+            c.m->win_len = r_wl; c.m->win_head = r_wh;
+        }
+        if (lane < p.tw) c.win[lane] = r_win;
+        __syncwarp();
+    }
+
     // ---------------------------------------------------------------- results
     SEPSO_GMARK(9);
     // record length = path_length(best) in FP64 (planner.hpp:194): warp 0 of
@@ -722,12 +920,12 @@ __global__ void __launch_bounds__(1024, 1) swarm_kernel(const __grid_constant__ 
 // ------------------------------------------------------------------ launcher
 constexpr int kMaxDevices = 64;
 
-template <class T, bool PATH, bool RING>
+template <class T, bool PATH, bool RING, int MAXT = 1024>
 static int launch_t(const SwarmParams& p, const ParamPayload* pl, int problem, cudaStream_t st,
                     size_t* smem_out) {
     const SmemLayout L = smem_layout(p, sizeof(T), PATH);
     if (smem_out) *smem_out = L.total;
-    auto kern = swarm_kernel<T, PATH, RING>;
+    auto kern = swarm_kernel<T, PATH, RING, MAXT>;
     cudaError_t e = cudaSuccess;
     // attributes are sticky per function AND per device: cache them per ordinal
     static thread_local size_t smem_set[kMaxDevices] = {};
@@ -790,6 +988,7 @@ int launch_swarms(const SwarmParams& p, const ParamPayload* pl, int problem, boo
     if (fp64) return path ? (ring ? launch_t<double, true, true>(p, pl, problem, st, smem)
                                   : launch_t<double, true, false>(p, pl, problem, st, smem))
                           : launch_t<double, false, false>(p, pl, problem, st, smem);
+    if (path && !ring && p.nthreads <= 896) return launch_t<float, true, false, 896>(p, pl, problem, st, smem);
     return path ? (ring ? launch_t<float, true, true>(p, pl, problem, st, smem)
                         : launch_t<float, true, false>(p, pl, problem, st, smem))
                 : launch_t<float, false, false>(p, pl, problem, st, smem);
