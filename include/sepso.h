@@ -166,7 +166,9 @@ int sf_lfv_batch(sf_ctx* ctx, const sf_problem* problem, uint32_t m, const doubl
                  uint32_t inner_iterations, double* lfv_out);
 
 /* evolve (hsef.hpp:125-171): outer PSO on the host, each evolution's
- * outer_groups*outer_per_group inner runs batched in one sf_lfv_batch launch.
+ * outer_groups*outer_per_group inner runs batched in one sf_lfv_batch launch
+ * (split over the context's ranks when it is sharded, sf_ctx_set_exchange /
+ * sf_ctx_init_comm).
  * best_trace/round_trace: E values; best_hypers: inner_groups*6. */
 typedef void (*sf_evolution_cb)(uint32_t evolution, double best_lfv, void* user);
 int sf_evolve(sf_ctx* ctx, const sf_problem* problem, uint32_t inner_groups,
@@ -250,12 +252,27 @@ int sf_scene_batch_destroy(sf_scene_batch* b);
 
 /* FP32 FFMA throughput of the device (TFLOP/s): roofline denominator probe. */
 int sf_measure_fp32_peak(sf_ctx* ctx, double* tflops);
+/* K1 roofline probe: the staged FP32 update kernel (step, swarm.hpp:138-174)
+ * on a synthetic groups x per_group x dim swarm, L2 evicted before every
+ * launch; mean CUDA-event milliseconds per launch and the algorithmic bytes
+ * of one launch (20 B per element). */
+int sf_measure_step_kernel(sf_ctx* ctx, uint32_t groups, uint32_t per_group, uint32_t dim, uint32_t reps,
+                           double* ms_per_launch, double* bytes_per_launch);
 
 /* ---- multi-GPU: one large swarm sharded by group (BASELINE config 4) ------ */
 /* NCCL communicator owned by the context (one process per GPU).  Rank 0 makes
  * the id, the caller broadcasts it, every rank attaches.  */
 int sf_comm_unique_id(uint8_t id[128]);
 int sf_ctx_init_comm(sf_ctx* ctx, const uint8_t id[128], int nranks, int rank);
+/* The same sharding over a host all-gather instead of NCCL (a gloo / MPI
+ * process group, or ranks that share a device): fn(user, send, recv, bytes)
+ * must fill recv with every rank's `bytes`-long block in rank order and
+ * return 0.  Used by sf_plan_frame_sharded (the per-iteration tbest
+ * candidates) and by sf_evolve (HSEF: each rank scores its share of the
+ * outer candidates; the LFVs are all-gathered and the outer PSO runs
+ * identically everywhere).  nranks = 1 and fn = NULL reset to one rank. */
+typedef int (*sf_allgather_fn)(void* user, const void* send, void* recv, size_t bytes);
+int sf_ctx_set_exchange(sf_ctx* ctx, int nranks, int rank, sf_allgather_fn fn, void* user);
 /* plan_frame (planner.hpp:156-199) for one large swarm whose groups are split
  * across the communicator's ranks: rank r evaluates and updates groups
  * [r*G/n, (r+1)*G/n) in HBM with the stage kernels; per iteration the ranks

@@ -2,8 +2,11 @@
 // kernel's FP32 roofline (MEASURED_PEAKS.json carries HBM and bf16 only).
 #include <cuda_runtime.h>
 
+#include <vector>
+
 #include "../../include/sepso.h"
 #include "host_runtime.hpp"
+#include "stage_kernels.cuh"
 
 namespace sepso {
 
@@ -48,6 +51,91 @@ extern "C" int sf_measure_fp32_peak(sf_ctx* ctx, double* tflops) {
     cudaFree(out);
     if (e != cudaSuccess) return cuda_fail(e, "calib run");
     *tflops = 2.0 * 8.0 * double(iters) * blocks * 256.0 / (double(ms) * 1e-3) / 1e12;
+    return SF_OK;
+}
+
+// K1 (k_step, the staged TOF update, swarm.hpp:138-174) on a synthetic FP32
+// swarm of groups x per_group rows of dim values, the shape of the HBM-staged
+// path (config 4): the mean device time of one launch over `reps` launches,
+// each after a 256 MiB write that evicts the 126 MB L2 (CUDA events around
+// write + K1 minus events around the write alone), and the
+// algorithmic bytes of one launch (20 B per element: x, v, pbest read, x, v
+// written).  The step draws come from a pre-generated window of words, as
+// in the staged mt19937 path.
+extern "C" int sf_measure_step_kernel(sf_ctx* ctx, uint32_t groups, uint32_t per_group, uint32_t dim,
+                                      uint32_t reps, double* ms_per_launch, double* bytes_per_launch) {
+    using namespace sepso;
+    if (!ctx || !ms_per_launch || !bytes_per_launch || groups == 0 || per_group == 0 || dim == 0 || reps == 0)
+        return fail(SF_INVALID_ARGUMENT, "measure_step_kernel: bad argument");
+    cudaSetDevice(ctx->device);
+    const size_t R = size_t(groups) * per_group, E = R * dim;
+    float *x = nullptr, *v = nullptr, *pb = nullptr, *gb = nullptr, *tb = nullptr, *lo = nullptr, *hi = nullptr;
+    double* hyp = nullptr;
+    unsigned long long* words = nullptr;
+    IterState* gate = nullptr;
+    unsigned char* flush = nullptr;
+    const size_t flush_bytes = size_t(256) << 20;
+    cudaError_t e = cudaMalloc(&x, E * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&v, E * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&pb, E * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&gb, size_t(groups) * dim * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&tb, size_t(dim) * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&lo, size_t(dim) * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&hi, size_t(dim) * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&hyp, size_t(groups) * 6 * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&words, 3 * R * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&gate, sizeof(IterState));
+    if (e == cudaSuccess) e = cudaMalloc(&flush, flush_bytes);
+    double ms_total = 0.0;
+    if (e == cudaSuccess) {
+        std::vector<float> hl(dim, 0.f), hh(dim, 1000.f);
+        std::vector<double> hy(size_t(groups) * 6);
+        for (uint32_t g = 0; g < groups; ++g) {
+            const double row[6] = {1.5, 1.3, 1.2, 0.6, 0.3, 0.4};
+            for (int j = 0; j < 6; ++j) hy[size_t(g) * 6 + j] = row[j];
+        }
+        cudaMemcpyAsync(lo, hl.data(), dim * 4, cudaMemcpyHostToDevice, ctx->stream);
+        cudaMemcpyAsync(hi, hh.data(), dim * 4, cudaMemcpyHostToDevice, ctx->stream);
+        cudaMemcpyAsync(hyp, hy.data(), hy.size() * 8, cudaMemcpyHostToDevice, ctx->stream);
+        cudaMemsetAsync(x, 0x44, E * 4, ctx->stream);      // ~785 (inside the box)
+        cudaMemsetAsync(v, 0, E * 4, ctx->stream);
+        cudaMemsetAsync(pb, 0x43, E * 4, ctx->stream);     // ~130
+        cudaMemsetAsync(gb, 0x43, size_t(groups) * dim * 4, ctx->stream);
+        cudaMemsetAsync(tb, 0x43, size_t(dim) * 4, ctx->stream);
+        cudaMemsetAsync(words, 0x5a, 3 * R * 8, ctx->stream);
+        cudaMemsetAsync(gate, 0, sizeof(IterState), ctx->stream);
+        StageShape sh{int(groups), int(per_group), int(dim), 0, int(R)};
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        // per rep: [eviction write + K1] and [eviction write] alone, each between
+        // an event pair; their difference is K1 without the event and launch
+        // overheads of a single short kernel (~6 us event-to-event here)
+        for (uint32_t r = 0; r <= reps && e == cudaSuccess; ++r) {   // r = 0: warm-up
+            float ms_fs = 0.f, ms_f = 0.f;
+            cudaEventRecord(a, ctx->stream);
+            cudaMemsetAsync(flush, int(r & 0xff), flush_bytes, ctx->stream);
+            const int st = stage_step(false, sh, hyp, lo, hi, x, v, pb, gb, tb, 1, 0, 2, 30, gate,
+                                      ctx->stream, words, 0);
+            cudaEventRecord(b, ctx->stream);
+            e = cudaEventSynchronize(b);
+            if (st != 0 && e == cudaSuccess) e = cudaErrorLaunchFailure;
+            cudaEventElapsedTime(&ms_fs, a, b);
+            cudaEventRecord(a, ctx->stream);
+            cudaMemsetAsync(flush, int((r + 1) & 0xff), flush_bytes, ctx->stream);
+            cudaEventRecord(b, ctx->stream);
+            if (e == cudaSuccess) e = cudaEventSynchronize(b);
+            cudaEventElapsedTime(&ms_f, a, b);
+            if (r > 0) ms_total += double(ms_fs) - double(ms_f);
+        }
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+    }
+    cudaFree(x); cudaFree(v); cudaFree(pb); cudaFree(gb); cudaFree(tb); cudaFree(lo); cudaFree(hi);
+    cudaFree(hyp); cudaFree(words); cudaFree(gate); cudaFree(flush);
+    if (e != cudaSuccess) return cuda_fail(e, "measure_step_kernel");
+    *ms_per_launch = ms_total / reps;
+    *bytes_per_launch = 20.0 * double(E);
     return SF_OK;
 }
 

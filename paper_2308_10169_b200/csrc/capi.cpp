@@ -624,10 +624,30 @@ int sf_evolve(sf_ctx* ctx, const sf_problem* pr, uint32_t iG, uint32_t iN, uint3
     std::vector<double> fit(cand);
     std::vector<uint64_t> seeds(cand);
     uint64_t eval_index = 0;
+    // sharded (a communicator or a host exchange): rank r scores candidates
+    // [r*cand/n, (r+1)*cand/n), the LFVs are all-gathered, and every rank runs
+    // the same outer update -- identical to the unsharded run
+    const int nr = std::max(1, ctx->nranks), rk = ctx->rank;
+    const uint32_t c0 = uint32_t(uint64_t(rk) * cand / uint32_t(nr)), c1 = uint32_t(uint64_t(rk + 1) * cand / uint32_t(nr));
+    const uint32_t slot = (cand + uint32_t(nr) - 1) / uint32_t(nr);
+    std::vector<double> mine(slot), all(size_t(slot) * nr);
     for (uint32_t e = 1; e <= E; ++e) {
         for (uint32_t r = 0; r < cand; ++r) seeds[r] = derive_seed(lfv_root, "lfv", eval_index++);
-        st = sf_lfv_batch(ctx, pr, cand, s.x.data(), seeds.data(), iG, iN, iT, fit.data());
-        if (st) return st;
+        if (nr == 1) {
+            st = sf_lfv_batch(ctx, pr, cand, s.x.data(), seeds.data(), iG, iN, iT, fit.data());
+            if (st) return st;
+        } else {
+            if (c1 > c0) {
+                st = sf_lfv_batch(ctx, pr, c1 - c0, s.x.data() + size_t(c0) * dim, seeds.data() + c0, iG, iN, iT,
+                                  mine.data());
+                if (st) return st;
+            }
+            if ((st = exchange_allgather(ctx, mine.data(), all.data(), size_t(slot) * 8))) return st;
+            for (int q = 0; q < nr; ++q) {
+                const uint32_t q0 = uint32_t(uint64_t(q) * cand / uint32_t(nr)), q1 = uint32_t(uint64_t(q + 1) * cand / uint32_t(nr));
+                std::copy(all.begin() + size_t(q) * slot, all.begin() + size_t(q) * slot + (q1 - q0), fit.begin() + q0);
+            }
+        }
         double round_best = std::numeric_limits<double>::infinity();
         for (uint32_t r = 0; r < cand; ++r) round_best = std::min(round_best, fit[r]);
         host_update_bests(s, fit.data());
@@ -1110,6 +1130,19 @@ int sf_ctx_init_comm(sf_ctx* ctx, const uint8_t id[128], int nranks, int rank) {
     if (st) return st;
     ctx->rank = rank;
     ctx->nranks = nranks;
+    return SF_OK;
+}
+
+int sf_ctx_set_exchange(sf_ctx* ctx, int nranks, int rank, sf_allgather_fn fn, void* user) {
+    if (!ctx) return fail(SF_INVALID_ARGUMENT, "ctx is null");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(SF_INVALID_ARGUMENT, "bad rank / world size");
+    if (nranks > 64) return fail(SF_INVALID_ARGUMENT, "sharded swarm: at most 64 ranks");
+    if (nranks > 1 && !fn) return fail(SF_INVALID_ARGUMENT, "an exchange callback is required for nranks > 1");
+    if (ctx->comm) return fail(SF_INVALID_ARGUMENT, "the context already has an NCCL communicator");
+    ctx->xfn = nranks > 1 ? fn : nullptr;
+    ctx->xuser = nranks > 1 ? user : nullptr;
+    ctx->nranks = nranks;
+    ctx->rank = rank;
     return SF_OK;
 }
 

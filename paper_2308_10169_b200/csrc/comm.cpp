@@ -70,6 +70,28 @@ int comm_allgather(void* comm, const void* send, void* recv, size_t bytes, cudaS
     return r == ncclSuccess ? 0 : 1;
 }
 
+int exchange_allgather(sf_ctx* ctx, const void* send, void* recv, size_t bytes) {
+    if (ctx->nranks <= 1) {
+        std::memcpy(recv, send, bytes);
+        return SF_OK;
+    }
+    if (ctx->xfn) {
+        const int r = ctx->xfn(ctx->xuser, send, recv, bytes);
+        return r == 0 ? SF_OK : fail(SF_RUNTIME_ERROR, "host all-gather callback failed");
+    }
+    if (!ctx->comm) return fail(SF_INVALID_ARGUMENT, "sharded run without an exchange");
+    unsigned char* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, bytes * size_t(ctx->nranks + 1));
+    if (e != cudaSuccess) return cuda_fail(e, "exchange staging");
+    e = cudaMemcpyAsync(d, send, bytes, cudaMemcpyHostToDevice, ctx->stream);
+    int st = e == cudaSuccess ? comm_allgather(ctx->comm, d, d + bytes, bytes, ctx->stream) : 1;
+    if (st == 0) e = cudaMemcpyAsync(recv, d + bytes, bytes * size_t(ctx->nranks), cudaMemcpyDeviceToHost, ctx->stream);
+    if (st == 0 && e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(d);
+    if (st) return fail(SF_CUDA_ERROR, "ncclAllGather failed");
+    return e == cudaSuccess ? SF_OK : cuda_fail(e, "exchange");
+}
+
 void comm_destroy(void* comm) {
     if (comm && nccl().comm_destroy) nccl().comm_destroy(static_cast<ncclComm_t>(comm));
 }

@@ -498,9 +498,18 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
                               reinterpret_cast<int*>(dev + o_pq), dev + o_pb, dev + o_gbx, dev + o_gbf,
                               reinterpret_cast<int*>(dev + o_gbq), dev + o_cand + cstride * r.rank, dst, st, dst);
         if (e) return cuda_fail(cudaError_t(e), "stage_group_bests");
-        if (nranks > 1) {   // the only cross-GPU traffic: each rank's tbest candidate
+        if (nranks > 1 && r.comm) {   // the only cross-GPU traffic: each rank's tbest candidate
             e = comm_allgather(r.comm, dev + o_cand + cstride * r.rank, dev + o_cand, cstride, st);
             if (e) return fail(SF_CUDA_ERROR, "ncclAllGather of tbest candidates failed");
+        } else if (nranks > 1) {      // host exchange (sf_ctx_set_exchange): the same bytes through the host
+            std::vector<unsigned char> mine(cstride), all(cstride * size_t(nranks));
+            ce = cudaMemcpyAsync(mine.data(), dev + o_cand + cstride * r.rank, cstride, cudaMemcpyDeviceToHost, st);
+            if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+            if (ce != cudaSuccess) return cuda_fail(ce, "candidate D2H");
+            if ((e = exchange_allgather(ctx, mine.data(), all.data(), cstride))) return e;
+            ce = cudaMemcpyAsync(dev + o_cand, all.data(), all.size(), cudaMemcpyHostToDevice, st);
+            if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);   // `all` is a pageable temporary
+            if (ce != cudaSuccess) return cuda_fail(ce, "candidates H2D");
         }
         e = stage_finish(fp64, D, dev + o_cand, nranks, dev + o_tbx, dst,
                          r.tw > 0 ? reinterpret_cast<double*>(dev + o_win) : nullptr, r.tw,

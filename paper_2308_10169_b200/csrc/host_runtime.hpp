@@ -51,6 +51,8 @@ struct sf_ctx {
     uint64_t l2_flush = 0;
     void* comm = nullptr;
     int rank = 0, nranks = 1;
+    sf_allgather_fn xfn = nullptr;   // host all-gather (sf_ctx_set_exchange) when there is no NCCL communicator
+    void* xuser = nullptr;
     sepso::DevBuf io, scratch, flush;
     sepso::PinnedBuf hio;
 };
@@ -118,6 +120,10 @@ int run_staged(sf_ctx* ctx, StagedRun& r);
 int comm_unique_id(unsigned char id[128]);
 int comm_init(void** comm, const unsigned char id[128], int nranks, int rank);
 int comm_allgather(void* comm, const void* send, void* recv, size_t bytes, cudaStream_t st);
+// All ranks' equal-size host blocks in rank order (recv: nranks * bytes) over
+// the context's exchange: the host callback, else NCCL through device staging,
+// else (one rank) a copy.
+int exchange_allgather(sf_ctx* ctx, const void* send, void* recv, size_t bytes);
 void comm_destroy(void* comm);
 
 bool force_staged();

@@ -39,8 +39,10 @@ ABI_SYMBOLS = [
     "sf_scene_batch_run", "sf_scene_batch_records", "sf_scene_batch_destroy",
     "sf_ctx_last_io_bytes", "sf_measure_fp32_peak", "sf_ctx_set_l2_flush",
     "sf_comm_unique_id", "sf_ctx_init_comm", "sf_plan_frame_sharded", "sf_ctx_set_rng",
-    "sf_ctx_rng", "sf_mt_jump_poly", "sf_derive_seed",
+    "sf_ctx_rng", "sf_mt_jump_poly", "sf_derive_seed", "sf_measure_step_kernel", "sf_ctx_set_exchange",
 ]
+# sf_allgather_fn: int (*)(void* user, const void* send, void* recv, size_t bytes)
+_ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
 RNGS = {"philox": 0, "mt19937": 1}
 
 
@@ -172,6 +174,8 @@ def lib():
         "sf_scene_batch_destroy": (C.c_int, [C.c_void_p]),
         "sf_ctx_last_io_bytes": (C.c_int, [C.c_void_p, _u64p, _u64p]),
         "sf_measure_fp32_peak": (C.c_int, [C.c_void_p, _dp]),
+        "sf_measure_step_kernel": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _dp, _dp]),
+        "sf_ctx_set_exchange": (C.c_int, [C.c_void_p, C.c_int, C.c_int, _ALLGATHER_FN, C.c_void_p]),
         "sf_mt_jump_poly": (C.c_int, [C.c_uint64, _u64p]),
         "sf_ctx_set_l2_flush": (C.c_int, [C.c_void_p, C.c_uint64]),
         "sf_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
@@ -444,6 +448,26 @@ class Engine:
         buf = (C.c_uint8 * 128)(*uid)
         _check(self._L.sf_ctx_init_comm(self._h, buf, nranks, rank))
 
+    def set_exchange(self, nranks: int, rank: int, allgather=None):
+        """Shard plan_frame_sharded / evolve over a host all-gather instead of
+        NCCL: allgather(bytes) -> every rank's bytes concatenated in rank order
+        (e.g. a gloo process group).  set_exchange(1, 0) resets."""
+        if allgather is None:
+            fn = _ALLGATHER_FN()
+        else:
+            def cb(user, send, recv, nbytes):
+                try:
+                    out = allgather(C.string_at(send, nbytes))
+                    if len(out) != nbytes * nranks:
+                        return 1
+                    C.memmove(recv, out, len(out))
+                    return 0
+                except Exception:
+                    return 1
+            fn = _ALLGATHER_FN(cb)
+        self._xfn = fn                     # the library keeps the pointer: keep the callback alive
+        _check(self._L.sf_ctx_set_exchange(self._h, nranks, rank, fn, None))
+
     def plan_frame_sharded(self, world: PolygonWorld, prev_best, hypers, config: PlannerConfig,
                            seed: int, carried_window: Optional[list] = None):
         """plan_frame for one large swarm split by group over the communicator."""
@@ -476,6 +500,12 @@ class Engine:
         t = C.c_double(0)
         _check(self._L.sf_measure_fp32_peak(self._h, C.byref(t)))
         return t.value
+
+    def measure_step_kernel(self, groups, per_group, dim, reps=5):
+        """K1 alone on a synthetic FP32 swarm: (ms per launch, algorithmic bytes per launch)."""
+        ms, by = C.c_double(0), C.c_double(0)
+        _check(self._L.sf_measure_step_kernel(self._h, groups, per_group, dim, reps, C.byref(ms), C.byref(by)))
+        return ms.value, by.value
 
     def last_io_bytes(self):
         a, b = C.c_uint64(0), C.c_uint64(0)
