@@ -29,6 +29,16 @@ if len(r) > 2:
         if n in ("dram__bytes_read.sum", "dram__bytes_write.sum",
                  "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
                  "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
-                 "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"):
+                 "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+                 "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+                 "smsp__issue_active.avg.pct_of_peak_sustained_active"):
             print(f"| {n} | {v[i]} | {u[i]} |")
+    # warp-stall reasons, as warps stalled per issued instruction (largest first)
+    st = [(n.split("issue_stalled_")[1].replace("_per_issue_active.ratio", ""), float(v[i]))
+          for i, n in enumerate(h) if n.startswith("smsp__average_warps_issue_stalled_")
+          and n.endswith("_per_issue_active.ratio") and v[i] not in ("", "n/a")]
+    st.sort(key=lambda t: -t[1])
+    tot = sum(x for _, x in st) or 1.0
+    print("\nStall reasons (share of stalled-warp samples per issue): " +
+          ", ".join(f"{n} {100 * x / tot:.0f}%" for n, x in st[:7] if x > 0))
 print(f"\nkernel: `{kernel}`\n")
