@@ -37,6 +37,10 @@ struct PinnedBuf {
 
 } // namespace sepso
 
+namespace sepso {
+struct Resident;   // resident planner of sf_plan_frame (capi.cpp)
+}
+
 struct sf_ctx {
     int device = 0;
     int precision = SF_FP32;
@@ -54,6 +58,7 @@ struct sf_ctx {
     sf_allgather_fn xfn = nullptr;   // host all-gather (sf_ctx_set_exchange) when there is no NCCL communicator
     void* xuser = nullptr;
     sepso::DevBuf io, scratch, flush;
+    sepso::Resident* resident = nullptr;
     sepso::PinnedBuf hio;
 };
 

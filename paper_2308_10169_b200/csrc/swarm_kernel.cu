@@ -144,6 +144,54 @@ static double at_var_bound(double delta, int tw) {
     return v;
 }
 
+// ---- resident planner: job hand-off with the host (ServerCtl, pinned memory)
+__device__ __forceinline__ uint32_t ld_acquire_sys(const volatile uint32_t* a) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// Every thread of every CTA of the cluster: wait for the next job.  Rank 0's
+// thread 0 polls the host words; rank 0's threads then read the job's input
+// bytes from pinned host memory once (one round trip over the bus) and store
+// them, with the decision word, into every rank's shared memory; one cluster
+// barrier publishes both.  Returns the job's sequence number, 0 = exit.
+__device__ uint32_t server_next_job(ServerCtl* srv, uint32_t last, uint32_t* cmd, unsigned char* jobsm,
+                                    int crank, int C) {
+    if (crank == 0) {
+        if (threadIdx.x == 0) {
+            const unsigned long long t0 = global_ns();
+            uint32_t d = 0;
+            for (;;) {
+                const uint32_t s = ld_acquire_sys(&srv->job_seq);
+                if (s != last) { d = s; srv->t_pick = global_ns(); break; }
+                if (srv->quit) break;
+                if (global_ns() - t0 > srv->idle_ns) break;
+            }
+            *cmd = d;
+        }
+        __syncthreads();
+        const uint32_t d = *cmd;
+        const int nb = d ? int(srv->job_bytes) / 16 : 0;
+        const uint32_t js = smem_addr(jobsm), cs = smem_addr(cmd);
+        for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+            const uint4 v = __ldcv(reinterpret_cast<const uint4*>(srv->job) + i);
+            for (int r = 0; r < C; ++r)
+                asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};"
+                             ::"r"(peer_addr(js + 16 * i, r)), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+        }
+        if (int(threadIdx.x) > 0 && int(threadIdx.x) < C)
+            asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(peer_addr(cs, int(threadIdx.x))), "r"(d) : "memory");
+    }
+    cluster_arrive();            // release: the job bytes and the word are in every rank's memory
+    cluster_wait();
+    return *reinterpret_cast<volatile uint32_t*>(cmd);
+}
+
 // AT statistic of the window (planner.hpp:138-149) by one warp in parallel.
 // The reference sums sequentially: mean_s = (sum w_i) / tw, var_s = sum (w_i -
 // mean_s)^2.  Any summation order of n = tw terms is within gamma_{n-1} sum|w|
@@ -263,9 +311,26 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
     c.edge = (T*)S8(L.edge); c.list = p.entry_cap > 0 ? (uint32_t*)S8(L.list) : nullptr; c.m = (Misc<T>*)S8(L.misc);
     const int LGM = p.max_local_groups;
     const uint32_t xbytes = ld.xbytes;
+    // resident planner (p.srv): the cluster serves one frame per posted job,
+    // its inputs copied from pinned host memory into shared memory; otherwise
+    // the loop body runs once on the launch's own inputs
+    ServerCtl* const srv = p.srv;
+    unsigned char* const jobsm = srv ? S8(L.job) : nullptr;
+    const unsigned char* const jb = srv ? jobsm : pl.bytes;
+    uint32_t jseq = 0;
+    if (srv) jseq = srv->done_seq;  // the last job served before this launch (the host is not posting while it reads)
+    long long kg = 0;              // iterations over all jobs: mbarrier buffer and phase parity
+    bool cl_waited = false;        // the launch's cluster_arrive has been matched
+    for (;;) {
+    if (srv) {
+        if (!cl_waited) { cluster_wait(); cl_waited = true; }
+        jseq = server_next_job(srv, jseq, reinterpret_cast<uint32_t*>(S8(L.srvcmd)), jobsm, c.crank, c.C);
+        if (jseq == 0) break;
+        if (c.crank == 0 && tid == 0) { srv->t_ready = global_ns(); srv->c_ready = clock64(); }
+    }
     const uint64_t seed =
         p.roots ? splitmix64(splitmix64(p.roots[swarm] ^ p.tag_hash) + uint64_t(p.frame_index))
-                : (p.inl ? reinterpret_cast<const unsigned long long*>(pl.bytes + p.in_seed) : p.seeds)[swarm];
+                : (p.inl ? reinterpret_cast<const unsigned long long*>(jb + p.in_seed) : p.seeds)[swarm];
     const int G = c.G, N = c.N, D = c.D, R = c.R;
     long long* const prof = (kProfiling && p.prof != nullptr && swarm == 0 && c.crank == 0 && tid == 0) ? p.prof : nullptr;
     // per-CTA (thread 0) work before the exchange: [(k * 16 + crank) * 2] = cycles, [+1] = wait
@@ -289,21 +354,21 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
     const bool mt_on = p.rng == kMt19937;
     const int cw = (mt_on && nthr >= 64) ? nthr - 32 : nthr;
     const unsigned char* wrec =
-        PATH ? (p.inl ? pl.bytes + p.in_world : p.worlds) + size_t(swarm) * size_t(p.world_stride) : nullptr;
+        PATH ? (p.inl ? jb + p.in_world : p.worlds) + size_t(swarm) * size_t(p.world_stride) : nullptr;
     c.O = 0;
     if (tid >= cw) {
         if (tid == cw) mt_seed_words(mtbuf + 312, seed);
         if (PATH) world_regs(c, wrec);
     } else {
-        const double* hyp_src = (p.inl ? reinterpret_cast<const double*>(pl.bytes + p.in_hyp) : p.hypers) +
+        const double* hyp_src = (p.inl ? reinterpret_cast<const double*>(jb + p.in_hyp) : p.hypers) +
                                 size_t(swarm) * size_t(p.hypers_stride);
         for (int i = tid; i < G * 6; i += cw) c.hyp[i] = T(hyp_src[i]);
         if (PATH) {
             world_regs(c, wrec);
             load_world(c, wrec, p.off_offsets, p.off_verts, tid, cw, cw == nthr ? 0 : 2);
         } else {
-            const double* lo_src = p.inl ? reinterpret_cast<const double*>(pl.bytes + p.in_lo) : p.lo;
-            const double* hi_src = p.inl ? reinterpret_cast<const double*>(pl.bytes + p.in_hi) : p.hi;
+            const double* lo_src = p.inl ? reinterpret_cast<const double*>(jb + p.in_lo) : p.lo;
+            const double* hi_src = p.inl ? reinterpret_cast<const double*>(jb + p.in_hi) : p.hi;
             for (int d = tid; d < D; d += cw) { c.lo[d] = T(lo_src[d]); c.hi[d] = T(hi_src[d]); }
         }
         if (tid == 0) {
@@ -312,14 +377,14 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
             m->status = 0; m->bad_row = INT_MAX; m->bad_min = INT_MAX; m->n_pair = 0; m->n_cont = 0;
             m->k_done = 0;
             m->cont_cap = 0;
-            const int wl = p.carry ? (p.inl ? reinterpret_cast<const int*>(pl.bytes + p.in_win_len) : p.win_len)[swarm] : 0;
+            const int wl = p.carry ? (p.inl ? reinterpret_cast<const int*>(jb + p.in_win_len) : p.win_len)[swarm] : 0;
             m->win_len = wl < p.tw ? wl : p.tw;
             m->win_head = 0;
             if (mt_on && cw == nthr) mt_seed_words(mtbuf + 312, seed);
         }
         if (p.carry)
             for (int i = tid; i < p.tw; i += cw)
-                c.win[i] = (p.inl ? reinterpret_cast<const double*>(pl.bytes + p.in_win) : p.win_vals)[size_t(swarm) * p.tw + i];
+                c.win[i] = (p.inl ? reinterpret_cast<const double*>(jb + p.in_win) : p.win_vals)[size_t(swarm) * p.tw + i];
         for (int g = tid; g < G; g += cw) {
             c.gbf[g] = A::inf(); c.gbq[g] = 0; c.chg[g] = -1;
             c.gtab[2 * g] = (g * N) / p.rows_per_cta;               // CTAs owning group g
@@ -334,9 +399,9 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
     // ------------------------------------------------------- initialisation
     // swarm.hpp:94-132 / planner.hpp:77-133: x draws [0, R*D), v draws [R*D, 2*R*D)
     {
-        const unsigned char* hp = p.inl ? (p.has_prev ? pl.bytes + p.in_has_prev : nullptr) : p.has_prev;
+        const unsigned char* hp = p.inl ? (p.has_prev ? jb + p.in_has_prev : nullptr) : p.has_prev;
         const bool warm_on = hp != nullptr && hp[swarm] != 0;
-        const double* prev = warm_on ? (p.inl ? reinterpret_cast<const double*>(pl.bytes + p.in_prev) : p.prev) +
+        const double* prev = warm_on ? (p.inl ? reinterpret_cast<const double*>(jb + p.in_prev) : p.prev) +
                                            size_t(swarm) * D
                                      : nullptr;
         const T rad = T(p.pi_radius);
@@ -399,9 +464,10 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
     __syncthreads();
     SEPSO_IMARK(6);
     SEPSO_GMARK(8);
+    if (srv && c.crank == 0 && tid == 0) srv->t_init = global_ns();
 
     // ------------------------------------------------------------ iterations
-    if (p.cap < 1) cluster_wait();
+    if (p.cap < 1 && !cl_waited) { cluster_wait(); cl_waited = true; }
     // Best update fast path (FP32, G <= 32, tw <= 32): warp 0 keeps the bests
     // and the AT window in registers -- lane g group g's gbest value and Q,
     // lane i window slot i -- so the chain of the single-warp phase is a few
@@ -423,7 +489,8 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
     const double inv_tw = p.tw > 0 ? 1.0 / double(p.tw) : 0.0;
     int k = 1;
     for (; k <= p.cap; ++k) {
-        const int buf = k & 1;
+        ++kg;
+        const int buf = int(kg & 1);
         SEPSO_MARK(0);
         if (wprof) wt0 = clock64();
         // fitness (geometry.hpp:262-267 / benchmarks.hpp:45-53)
@@ -467,7 +534,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
         }
         SEPSO_MARK(5);
         if (tid == 0) mbar_expect(mbar0 + 8 * buf, xbytes);
-        if (k == 1) cluster_wait();       // every peer is running, its mbarriers initialised
+        if (!cl_waited) { cluster_wait(); cl_waited = true; }   // every peer is running, its mbarriers initialised
         // per-CTA group partials: (pbest_f, row) lexicographic min, one warp per group
         for (int lg = warp; lg < c.LG; lg += nthr >> 5) {
             const int g = gfirst + lg;
@@ -537,7 +604,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
         }
         long long wt1 = 0;
         if (wprof) wt1 = clock64();
-        if (warp == 0) mbar_wait(mbar0 + 8 * buf, uint32_t(((k - 1) >> 1) & 1));   // every CTA's partials
+        if (warp == 0) mbar_wait(mbar0 + 8 * buf, uint32_t(((kg - 1) >> 1) & 1));   // every CTA's partials
         if (wprof) {
             wprof[(size_t(k - 1) * 16 + c.crank) * 2] = wt1 - wt0;
             wprof[(size_t(k - 1) * 16 + c.crank) * 2 + 1] = clock64() - wt1;
@@ -862,6 +929,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
 
     // ---------------------------------------------------------------- results
     SEPSO_GMARK(9);
+    if (srv && c.crank == 0 && tid == 0) srv->t_loop = global_ns();
     // record length = path_length(best) in FP64 (planner.hpp:194): warp 0 of
     // rank 0 computes the S segment hypots in parallel, summed in path order
     double path_len = 0.0;
@@ -912,9 +980,26 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
             step_world_part(const_cast<unsigned char*>(p.worlds) + size_t(swarm) * size_t(p.world_stride),
                             p.off_offsets, p.off_verts, p.off_vel, p.step_dt, t);
     SEPSO_GMARK(10);
+    SEPSO_GMARK(11);
+    if (!srv) break;
+    // resident planner: rank 0's record is complete (its threads stored it)
+    // before thread 0 publishes the job as done
+    if (c.crank == 0) {
+        __syncthreads();
+        if (tid == 0) {
+            srv->t_done = global_ns();
+            srv->c_done = clock64();
+            __threadfence_system();
+            srv->done_seq = jseq;
+        }
+    }
+    }   // jobs
+    if (srv && c.crank == 0 && tid == 0) {
+        __threadfence_system();
+        srv->alive = 0;
+    }
     // No closing cluster barrier: a CTA only ever reads its own shared memory,
     // and every st.async into it completed before its last best update.
-    SEPSO_GMARK(11);
 }
 
 // ------------------------------------------------------------------ launcher

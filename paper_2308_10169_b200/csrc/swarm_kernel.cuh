@@ -62,6 +62,28 @@ struct SwarmOut {
     uint32_t bad_g, bad_n, bad_k, window_len;
 };
 
+// Resident planner (sf_plan_frame's fast path): the host posts a job -- the
+// frame's input bytes, laid out as the ParamPayload inline block -- into
+// pinned, device-mapped memory and bumps job_seq; the resident cluster copies
+// the bytes into shared memory, plans the frame, stores the record into the
+// pinned output block and sets done_seq = job_seq.  The cluster exits on
+// `quit` or after idle_ns without a job, clearing `alive` (the host then
+// relaunches it for the next job; a job posted in the race is served by the
+// new cluster, which starts from done_seq).
+struct ServerCtl {
+    volatile uint32_t job_seq;     // host: the latest posted job
+    volatile uint32_t quit;        // host: 1 = exit now
+    volatile uint32_t done_seq;    // device: the latest finished job
+    volatile uint32_t alive;       // host sets 1 before a launch, device clears on exit
+    unsigned long long idle_ns;    // device exits after this long without a job
+    uint32_t job_bytes;            // bytes of job[] a job uses
+    uint32_t pad[3];
+    unsigned long long t_pick, t_ready, t_done;   // %globaltimer of the last job: seen, inputs staged, published
+    long long c_ready, c_done;                    // clock64 at staged / published (the SM clock over the frame)
+    unsigned long long t_init, t_loop;            // %globaltimer after the initialisation / after the iterations
+    alignas(16) unsigned char job[3328];   // = kInlineBytes
+};
+
 struct SwarmParams {
     // shape
     int n_swarms, G, N, D, C, rows_per_cta, max_local_groups;
@@ -93,6 +115,8 @@ struct SwarmParams {
     // in_* are their byte offsets there (seeds, worlds, hypers, prev, has_prev,
     // lo, hi, window values, window lengths)
     int inl, in_seed, in_world, in_hyp, in_prev, in_has_prev, in_lo, in_hi, in_win, in_win_len;
+    // resident planner (inl layout, one swarm): jobs from here; nullptr = one pass
+    ServerCtl* srv;
 };
 
 // Small host-buffer launches (one paper scene: ~1.8 KB of inputs) pass their
@@ -101,6 +125,7 @@ constexpr int kInlineBytes = 3328;
 struct ParamPayload {
     unsigned char bytes[kInlineBytes];
 };
+static_assert(sizeof(ServerCtl::job) == kInlineBytes, "resident planner job block = the inline payload");
 // Phase profiler (SEPSO_PHASE_PROF=1 at run time) exists only in builds with
 // -DSEPSO_PROFILE (make PROF=1): the release kernel carries none of its code.
 #ifdef SEPSO_PROFILE
@@ -119,7 +144,8 @@ struct Part {
 
 struct SmemLayout {
     size_t x, v, pb, pbf, pbq, q, fit, imp, seglen, coef, lo, hi, hyp, gbx, gbf, gbq, chg, tbx,
-        win, part, px, allpart, allbad, gtab, ctab, obb, ooff, ofl, vert, edge, list, mt, mbar, misc, total;
+        win, part, px, allpart, allbad, gtab, ctab, obb, ooff, ofl, vert, edge, list, mt, mbar, misc, job,
+        srvcmd, total;
 };
 
 #ifdef __CUDACC__
@@ -171,6 +197,8 @@ SEPSO_LHD SmemLayout smem_layout(const SwarmParams& p, size_t tsz, bool path) {
     L.vert = take(V * 2 * tsz);
     L.edge = take(V * 4 * tsz);
     L.list = take(path ? size_t(p.entry_cap) * 4 : 0);
+    L.job = take(p.srv ? size_t(kInlineBytes) : 0);     // resident planner: this job's input bytes
+    L.srvcmd = take(p.srv ? 16 : 0);                    // resident planner: rank 0's decision
     o = (o + 127) & ~size_t(127);          // generator state on a 128-byte boundary
     L.mt = take(p.rng == 1 ? 4 * 312 * 8 : 0);
     L.total = o;
