@@ -290,8 +290,9 @@ int resident_run(sf_ctx* ctx, const SwarmParams& fp_p, int problem, const unsign
     std::atomic_thread_fence(std::memory_order_acquire);
     static const bool trace = std::getenv("SEPSO_RESIDENT_TRACE") != nullptr;
     if (trace)
-        std::fprintf(stderr, "[resident] init %.1f us loop %.1f us out %.1f us\n", 1e-3 * double(R.ctl->t_init - R.ctl->t_ready),
-                     1e-3 * double(R.ctl->t_loop - R.ctl->t_init), 1e-3 * double(R.ctl->t_done - R.ctl->t_loop));
+        std::fprintf(stderr, "[resident] init %.1f us loop %.1f us rec %.1f us out %.1f us\n",
+                     1e-3 * double(R.ctl->t_init - R.ctl->t_ready), 1e-3 * double(R.ctl->t_iter - R.ctl->t_init),
+                     1e-3 * double(R.ctl->t_loop - R.ctl->t_iter), 1e-3 * double(R.ctl->t_done - R.ctl->t_loop));
     if (trace)
         std::fprintf(stderr, "[resident] host wait %.1f us | device: stage %.1f us, frame %.1f us, SM %.0f MHz, iters %u\n",
                      1e6 * (now_seconds() - t0), 1e-3 * double(R.ctl->t_ready - R.ctl->t_pick),

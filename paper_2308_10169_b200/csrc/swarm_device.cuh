@@ -40,6 +40,7 @@ template <class T> struct Misc {
     int win_len, win_head, k_done, cont_cap;
     int mt_cur;                 // mt19937_64 generator bookkeeping (MtState outside generation)
     long long mt_blocks;
+    int q64;                    // FP32 engine: Q of the final best path on the FP64 world
 };
 
 // alpha * q^beta (geometry.hpp:240): exact repeated product for small integer
@@ -178,6 +179,7 @@ template <class T> struct Ctx {
     Part *part, *allpart;
     T *obb, *vert, *edge;
     double* win;
+    double* vert64;               // FP32 path swarms: the caller's FP64 vertices and endpoints (final record)
     uint32_t* list;
     Misc<T>* m;
     // path constants
@@ -434,6 +436,13 @@ __device__ void load_world(Ctx<T>& c, const unsigned char* wrec, int off_offsets
     }
     for (int i = tid; i <= c.O; i += nthr) c.ooff[i] = int(woff[i]);
     for (int i = tid; i < 2 * nv; i += nthr) c.vert[i] = T(wv[i]);
+    if (c.vert64 != nullptr) {      // FP64 copy: vertices, then start and target
+        for (int i = tid; i < 2 * nv; i += nthr) c.vert64[i] = wv[i];
+        if (tid == 0) {
+            c.vert64[2 * nv] = wh->sx; c.vert64[2 * nv + 1] = wh->sy;
+            c.vert64[2 * nv + 2] = wh->tx; c.vert64[2 * nv + 3] = wh->ty;
+        }
+    }
     if (bar == 0) __syncthreads();
     else asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nthr) : "memory");
     for (int o = tid; o < c.O; o += nthr) {                  // bbox_of, geometry.hpp:167-177

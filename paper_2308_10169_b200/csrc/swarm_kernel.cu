@@ -192,6 +192,36 @@ __device__ uint32_t server_next_job(ServerCtl* srv, uint32_t last, uint32_t* cmd
     return *reinterpret_cast<volatile uint32_t*>(cmd);
 }
 
+// FP32 engine's final record: this thread's share of Q of the best path
+// (tbx) on the caller's FP64 world staged in shared memory (vert64 = vertices
+// then start, target): reference predicates (geometry.hpp:196-220), one
+// (segment, edge) pair or one first-waypoint containment test per task.  Out
+// of line: it runs once per frame and keeps its registers out of the loop's.
+__device__ __noinline__ int rec64_hits(const double* wv, const int* woff, int O, const float* tbx, int W, int S,
+                                       int tid, int nthr) {
+    const int nv = woff[O];
+    const double sx = wv[2 * nv], sy = wv[2 * nv + 1], tx = wv[2 * nv + 2], ty = wv[2 * nv + 3];
+    auto wpx = [&](int j) { return j == 0 ? sx : (j <= W ? double(tbx[j - 1]) : tx); };
+    auto wpy = [&](int j) { return j == 0 ? sy : (j <= W ? double(tbx[W + j - 1]) : ty); };
+    int hits = 0;
+    for (int t = tid; t < S * nv + O; t += nthr) {
+        if (t < S * nv) {
+            const int sg = t / nv, e = t - sg * nv;
+            int o = 0;
+            while (woff[o + 1] <= e) ++o;
+            const int e2 = e + 1 == woff[o + 1] ? woff[o] : e + 1;
+            hits += segments_intersect_ref(wpx(sg), wpy(sg), wpx(sg + 1), wpy(sg + 1), wv[2 * e], wv[2 * e + 1],
+                                           wv[2 * e2], wv[2 * e2 + 1]) ? 1 : 0;
+        } else {
+            const int o = t - S * nv, v0 = woff[o];
+            hits += point_strictly_inside_ref(wpx(1), wpy(1), woff[o + 1] - v0,
+                                              [&](int i) { return wv[2 * (v0 + i)]; },
+                                              [&](int i) { return wv[2 * (v0 + i) + 1]; }) ? 1 : 0;
+        }
+    }
+    return hits;
+}
+
 // AT statistic of the window (planner.hpp:138-149) by one warp in parallel.
 // The reference sums sequentially: mean_s = (sum w_i) / tw, var_s = sum (w_i -
 // mean_s)^2.  Any summation order of n = tw terms is within gamma_{n-1} sum|w|
@@ -309,6 +339,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
     c.allbad = (int*)S8(L.allbad); c.gtab = (int*)S8(L.gtab); c.ctab = (int*)S8(L.ctab);
     c.obb = (T*)S8(L.obb); c.ooff = (int*)S8(L.ooff); c.ofl = (int*)S8(L.ofl); c.vert = (T*)S8(L.vert);
     c.edge = (T*)S8(L.edge); c.list = p.entry_cap > 0 ? (uint32_t*)S8(L.list) : nullptr; c.m = (Misc<T>*)S8(L.misc);
+    c.vert64 = (PATH && sizeof(T) == 4) ? (double*)S8(L.vert64) : nullptr;
     const int LGM = p.max_local_groups;
     const uint32_t xbytes = ld.xbytes;
     // resident planner (p.srv): the cluster serves one frame per posted job,
@@ -929,19 +960,38 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
 
     // ---------------------------------------------------------------- results
     SEPSO_GMARK(9);
+    // FP32 engine, path problems: the record is the reference's evaluation of
+    // the returned path -- Q of the best path counted on the caller's FP64
+    // world with the reference's predicates (geometry.hpp:196-220), not on the
+    // FP32-rounded world the swarm planned on; fitness = length + alpha Q^beta
+    // below.  CTA 0, one (segment, edge) pair or first-waypoint containment
+    // test per thread.
+    if (srv && c.crank == 0 && tid == 0) srv->t_iter = global_ns();
+    const bool rec64 = PATH && sizeof(T) == 4 && c.crank == 0 && c.m->status == 0;
+    if (rec64) {
+        if (tid == 0) c.m->q64 = 0;
+        __syncthreads();
+        const int hits = rec64_hits(c.vert64, c.ooff, c.O, reinterpret_cast<const float*>(c.tbx), c.W, c.S, tid, nthr);
+        if (hits) atomicAdd(&c.m->q64, hits);
+        __syncthreads();
+    }
     if (srv && c.crank == 0 && tid == 0) srv->t_loop = global_ns();
     // record length = path_length(best) in FP64 (planner.hpp:194): warp 0 of
     // rank 0 computes the S segment hypots in parallel, summed in path order
     double path_len = 0.0;
     if (PATH && c.crank == 0 && warp == 0) {
+        // endpoints: the caller's FP64 values (the FP32 engine staged rounded ones)
+        const double* e64 = rec64 ? c.vert64 + 2 * c.ooff[c.O] : nullptr;
+        const double sx = e64 ? e64[0] : double(c.sx), sy = e64 ? e64[1] : double(c.sy);
+        const double tx = e64 ? e64[2] : double(c.tx), ty = e64 ? e64[3] : double(c.ty);
         for (int j0 = 0; j0 < c.S; j0 += 32) {
             const int j = j0 + lane;
             double h = 0.0;
             if (j < c.S) {
-                const double px = j == 0 ? double(c.sx) : double(c.tbx[j - 1]);
-                const double py = j == 0 ? double(c.sy) : double(c.tbx[c.W + j - 1]);
-                const double nx = j < c.W ? double(c.tbx[j]) : double(c.tx);
-                const double ny = j < c.W ? double(c.tbx[c.W + j]) : double(c.ty);
+                const double px = j == 0 ? sx : double(c.tbx[j - 1]);
+                const double py = j == 0 ? sy : double(c.tbx[c.W + j - 1]);
+                const double nx = j < c.W ? double(c.tbx[j]) : tx;
+                const double ny = j < c.W ? double(c.tbx[c.W + j]) : ty;
                 h = hypot_glibc(__dsub_rn(nx, px), __dsub_rn(ny, py));
             }
             for (int i = 0; i < 32 && j0 + i < c.S; ++i) path_len = __dadd_rn(path_len, __shfl_sync(0xffffffffu, h, i));
@@ -958,6 +1008,10 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
             o.bad_g = uint32_t(m->bad_min / N);
             o.bad_n = uint32_t(m->bad_min % N);
             o.bad_k = uint32_t(m->k_done);
+        } else if (rec64) {
+            o.q = uint32_t(m->q64);
+            o.length = path_len;
+            o.fitness = __dadd_rn(path_len, penalty(p.alpha, p.beta, p.beta_int, m->q64));   // geometry.hpp:234-241
         } else {
             o.fitness = double(m->tbf);
             o.q = uint32_t(m->tbq);

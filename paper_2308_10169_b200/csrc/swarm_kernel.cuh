@@ -80,7 +80,7 @@ struct ServerCtl {
     uint32_t pad[3];
     unsigned long long t_pick, t_ready, t_done;   // %globaltimer of the last job: seen, inputs staged, published
     long long c_ready, c_done;                    // clock64 at staged / published (the SM clock over the frame)
-    unsigned long long t_init, t_loop;            // %globaltimer after the initialisation / after the iterations
+    unsigned long long t_init, t_loop, t_iter;    // %globaltimer after the initialisation / the record / the iterations
     alignas(16) unsigned char job[3328];   // = kInlineBytes
 };
 
@@ -145,7 +145,7 @@ struct Part {
 struct SmemLayout {
     size_t x, v, pb, pbf, pbq, q, fit, imp, seglen, coef, lo, hi, hyp, gbx, gbf, gbq, chg, tbx,
         win, part, px, allpart, allbad, gtab, ctab, obb, ooff, ofl, vert, edge, list, mt, mbar, misc, job,
-        srvcmd, total;
+        srvcmd, vert64, total;
 };
 
 #ifdef __CUDACC__
@@ -197,6 +197,7 @@ SEPSO_LHD SmemLayout smem_layout(const SwarmParams& p, size_t tsz, bool path) {
     L.vert = take(V * 2 * tsz);
     L.edge = take(V * 4 * tsz);
     L.list = take(path ? size_t(p.entry_cap) * 4 : 0);
+    L.vert64 = take(path && tsz == 4 ? (V * 2 + 4) * 8 : 0);   // FP32 engine: FP64 world for the final record
     L.job = take(p.srv ? size_t(kInlineBytes) : 0);     // resident planner: this job's input bytes
     L.srvcmd = take(p.srv ? 16 : 0);                    // resident planner: rank 0's decision
     o = (o + 127) & ~size_t(127);          // generator state on a 128-byte boundary

@@ -231,3 +231,30 @@ def test_run_scenario_variant_fp64_equals_reference(variant, eng64mt):
         assert (got.iterations, got.intersections, got.truncated, got.collision_free) == \
             (want.iterations, want.intersections, bool(want.truncated), bool(want.collision_free)), (variant, f)
         assert got.fitness == want.fitness and got.length == want.length, (variant, f)
+
+
+# ------------------------------------------- FP32 records on the FP64 world
+def test_fp32_record_is_the_reference_evaluation_of_its_path(eng32mt):
+    """The FP32 engine plans on the FP32-rounded world, but its PlanRecord is
+    the reference's own evaluation of the returned path on the caller's FP64
+    world: Q with the reference's predicates, length with its hypot, fitness
+    = length + 30 Q^4 (geometry.hpp:196-241) -- bit for bit."""
+    o = oracle()
+    planner = pe.PlannerConfig(max_iters_per_frame=30, window_carryover=True)
+    recs = eng32mt.run_scenario(pe.ScenarioConfig(root_seed=9), "sepso", 12, planner)
+    w = pe.generate_world(pe.ScenarioConfig(root_seed=9), o.or_derive_seed(9, b"world"), "mt19937")
+    for f, r in enumerate(recs):
+        best = pe.encode_path(r.best_path).astype(np.float64)
+        wb = world_from_engine(w)
+        fit, q, ln = np.zeros(1), np.zeros(1, dtype=np.uint32), np.zeros(1)
+        from oracle_lib import u32p
+        _ref().ref_eval_path_rows(C.byref(wb.struct()), ptr(best), 1, 16, 30.0, 4.0, ptr(fit), ptr(q, u32p), ptr(ln))
+        assert r.intersections == q[0] and r.collision_free == (q[0] == 0), f
+        assert r.length == ln[0] and r.fitness == fit[0], f
+        w = pe.step_world(w, 1.0)
+    # scene batches (device-resident frames, world stepped in the same launch) agree
+    sb = pe.SceneBatch(eng32mt, [pe.ScenarioConfig(root_seed=9)], planner, pe.EVOLVED_PATH_HYPERS, 12)
+    sb.run(12)
+    rb, _ = sb.records(0, 12)
+    sb.close()
+    assert [(r.fitness, r.intersections) for r in rb] == [(r.fitness, r.intersections) for r in recs]
