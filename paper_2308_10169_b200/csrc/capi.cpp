@@ -494,6 +494,12 @@ int sf_ctx_destroy(sf_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     resident_destroy(ctx);
+    if (ctx->side) {
+        cudaStreamSynchronize(ctx->side);
+        cudaStreamDestroy(ctx->side);
+        cudaEventDestroy(ctx->ev_free);
+        cudaEventDestroy(ctx->ev_fill);
+    }
     ctx->io.release();
     ctx->scratch.release();
     ctx->flush.release();

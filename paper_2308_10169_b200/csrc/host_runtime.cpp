@@ -479,8 +479,27 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
                        r.prev ? reinterpret_cast<double*>(dev + o_prev) : nullptr, r.warm, r.pi_radius,
                        dev + o_x, dev + o_v, dev + o_pb, st, words, 0);
     if (e) return cuda_fail(cudaError_t(e), "stage_init");
+    // mt19937: step k's 3R draws are generated on a side stream while the
+    // fitness and best kernels of iteration k run (the generator is one CTA
+    // and sequential); the word window is free again once the previous step
+    // (or the initialisation) has read it
+    if (mt && !ctx->side) {
+        ce = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
+        if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&ctx->ev_free, cudaEventDisableTiming);
+        if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&ctx->ev_fill, cudaEventDisableTiming);
+        if (ce != cudaSuccess) return cuda_fail(ce, "side stream");
+    }
+    if (mt) cudaEventRecord(ctx->ev_free, st);
     const WorldLayout& wl = wp.lay;
     for (int k = 1; k <= r.cap; ++k) {
+        if (mt && k < r.cap) {   // draws of step k (the generator persists across iterations)
+            const uint64_t first = 2ull * uint64_t(R) * D + uint64_t(k - 1) * 3ull * R;
+            cudaStreamWaitEvent(ctx->side, ctx->ev_free, 0);
+            const int fe = stage_mt_fill(mtg, r.seed, false, (long long)first, (long long)first + 3ll * R, words,
+                                         ctx->side);
+            if (fe) return cuda_fail(cudaError_t(fe), "stage_mt_fill");
+            cudaEventRecord(ctx->ev_fill, ctx->side);
+        }
         if (path)
             e = stage_eval_path(fp64, dev + o_world, wl.max_obs, wl.max_verts, int(wl.off_offsets),
                                 int(wl.off_verts), D, RL, dev + o_x, r.alpha, r.beta, dev + o_fit,
@@ -517,14 +536,12 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
         if (e) return cuda_fail(cudaError_t(e), "stage_finish");
         if (k < r.cap) {
             const uint64_t first = 2ull * uint64_t(R) * D + uint64_t(k - 1) * 3ull * R;
-            if (mt) {   // draws of step k (the generator persists across iterations)
-                const int fe = stage_mt_fill(mtg, r.seed, false, (long long)first, (long long)first + 3ll * R, words, st);
-                if (fe) return cuda_fail(cudaError_t(fe), "stage_mt_fill");
-            }
+            if (mt) cudaStreamWaitEvent(st, ctx->ev_fill, 0);
             e = stage_step(fp64, s, reinterpret_cast<double*>(dev + o_hyp), dev + o_lo, dev + o_hi,
                            dev + o_x, dev + o_v, dev + o_pb, dev + o_gbx, dev + o_tbx, r.seed, first,
                            k, r.cap, dst, st, words, (long long)first);
             if (e) return cuda_fail(cudaError_t(e), "stage_step");
+            if (mt) cudaEventRecord(ctx->ev_free, st);
         }
     }
     if (ctx->timing) {

@@ -222,6 +222,27 @@ __device__ __noinline__ int rec64_hits(const double* wv, const int* woff, int O,
     return hits;
 }
 
+// path_length (geometry.hpp:223-231) of the best path start -> w_1..w_W ->
+// target in FP64: one warp, the S hypots in parallel, summed in path order.
+template <class T>
+__device__ __noinline__ double path_length64(const T* tbx, int W, int S, double sx, double sy, double tx, double ty,
+                                             int lane) {
+    double len = 0.0;
+    for (int j0 = 0; j0 < S; j0 += 32) {
+        const int j = j0 + lane;
+        double h = 0.0;
+        if (j < S) {
+            const double px = j == 0 ? sx : double(tbx[j - 1]);
+            const double py = j == 0 ? sy : double(tbx[W + j - 1]);
+            const double nx = j < W ? double(tbx[j]) : tx;
+            const double ny = j < W ? double(tbx[W + j]) : ty;
+            h = hypot_glibc(__dsub_rn(nx, px), __dsub_rn(ny, py));
+        }
+        for (int i = 0; i < 32 && j0 + i < S; ++i) len = __dadd_rn(len, __shfl_sync(0xffffffffu, h, i));
+    }
+    return len;
+}
+
 // AT statistic of the window (planner.hpp:138-149) by one warp in parallel.
 // The reference sums sequentially: mean_s = (sum w_i) / tw, var_s = sum (w_i -
 // mean_s)^2.  Any summation order of n = tw terms is within gamma_{n-1} sum|w|
@@ -404,7 +425,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
         }
         if (tid == 0) {
             Misc<T>* m = c.m;
-            m->tbf = A::inf(); m->tbq = 0; m->tsrc_slot = -1; m->stop = 0; m->truncated = 0;
+            m->tbf = A::inf(); m->tbq = 0; m->tsrc_slot = -1; m->stop = 0; m->truncated = 0; m->q64 = 0;
             m->status = 0; m->bad_row = INT_MAX; m->bad_min = INT_MAX; m->n_pair = 0; m->n_cont = 0;
             m->k_done = 0;
             m->cont_cap = 0;
@@ -482,6 +503,15 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
                 mt_generate(mt, grp, 2 * RD, 2 * RD, [&](int, unsigned long long) {});
                 SEPSO_IMARK(5);
                 if (tid == 0) { c.m->mt_cur = mt.cur; c.m->mt_blocks = mt.blocks; }
+            } else if (PATH && sizeof(T) == 4 && c.crank == 0 && tid < grp.n + 32) {
+                // rank 0's first idle warp runs the final record's code once on
+                // dummy input while the generator walks the stream: after an
+                // L2 flush that code would otherwise be fetched from DRAM on
+                // the frame's critical path (its result is discarded)
+                const int h = rec64_hits(c.vert64, c.ooff, c.O, reinterpret_cast<const float*>(c.tbx), c.W, c.S,
+                                         tid - grp.n, 32);
+                const double len = path_length64(c.tbx, c.W, c.S, 0.0, 0.0, 1.0, 1.0, tid - grp.n);
+                if (h < 0 || len < 0.0) c.m->q64 = h;
             }
         } else {
             ElemWalk w(c.fD, tid, nthr, D);
@@ -968,12 +998,10 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
     // test per thread.
     if (srv && c.crank == 0 && tid == 0) srv->t_iter = global_ns();
     const bool rec64 = PATH && sizeof(T) == 4 && c.crank == 0 && c.m->status == 0;
-    if (rec64) {
-        if (tid == 0) c.m->q64 = 0;
-        __syncthreads();
-        const int hits = rec64_hits(c.vert64, c.ooff, c.O, reinterpret_cast<const float*>(c.tbx), c.W, c.S, tid, nthr);
+    if (rec64 && warp != 0) {       // warps 1.. count Q while warp 0 sums the length below
+        const int hits = rec64_hits(c.vert64, c.ooff, c.O, reinterpret_cast<const float*>(c.tbx), c.W, c.S, tid - 32,
+                                    nthr - 32);
         if (hits) atomicAdd(&c.m->q64, hits);
-        __syncthreads();
     }
     if (srv && c.crank == 0 && tid == 0) srv->t_loop = global_ns();
     // record length = path_length(best) in FP64 (planner.hpp:194): warp 0 of
@@ -982,21 +1010,10 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
     if (PATH && c.crank == 0 && warp == 0) {
         // endpoints: the caller's FP64 values (the FP32 engine staged rounded ones)
         const double* e64 = rec64 ? c.vert64 + 2 * c.ooff[c.O] : nullptr;
-        const double sx = e64 ? e64[0] : double(c.sx), sy = e64 ? e64[1] : double(c.sy);
-        const double tx = e64 ? e64[2] : double(c.tx), ty = e64 ? e64[3] : double(c.ty);
-        for (int j0 = 0; j0 < c.S; j0 += 32) {
-            const int j = j0 + lane;
-            double h = 0.0;
-            if (j < c.S) {
-                const double px = j == 0 ? sx : double(c.tbx[j - 1]);
-                const double py = j == 0 ? sy : double(c.tbx[c.W + j - 1]);
-                const double nx = j < c.W ? double(c.tbx[j]) : tx;
-                const double ny = j < c.W ? double(c.tbx[c.W + j]) : ty;
-                h = hypot_glibc(__dsub_rn(nx, px), __dsub_rn(ny, py));
-            }
-            for (int i = 0; i < 32 && j0 + i < c.S; ++i) path_len = __dadd_rn(path_len, __shfl_sync(0xffffffffu, h, i));
-        }
+        path_len = path_length64(c.tbx, c.W, c.S, e64 ? e64[0] : double(c.sx), e64 ? e64[1] : double(c.sy),
+                                 e64 ? e64[2] : double(c.tx), e64 ? e64[3] : double(c.ty), lane);
     }
+    if (rec64) __syncthreads();
     if (c.crank == 0 && tid == 0) {
         const Misc<T>* m = c.m;
         SwarmOut o{};
