@@ -228,6 +228,44 @@ int ref_run_dtpso(int kind, const or_world* w, std::size_t D, double alpha, doub
     }
 }
 
+// runner.hpp:135-239 -- the reference's per-particle DPPSO oracle (the `scale`
+// harness's second code path, proj/tools/swarmforge.cpp:202-255); wall =
+// its RunReport.wall_seconds
+int ref_run_dppso_reference(int kind, const or_world* w, std::size_t D, double alpha, double beta,
+                            const double* hypers, std::size_t G, std::size_t N, std::size_t T,
+                            std::uint64_t seed, double* trace, double* final_point, double* final_f,
+                            double* wall) {
+    try {
+        const auto p = make_problem(kind, D, w, alpha, beta);
+        const RunReport r = run_dppso_reference(*p, to_hypers(hypers, G), G, N, T, seed);
+        if (trace) std::copy(r.trace.begin(), r.trace.end(), trace);
+        if (final_point) std::copy(r.final_point.begin(), r.final_point.end(), final_point);
+        *final_f = r.final_fitness;
+        if (wall) *wall = r.wall_seconds;
+        return 0;
+    } catch (const std::exception&) {
+        return 1;
+    }
+}
+
+// runner.hpp:244-329 -- the classic single-swarm PSO baseline (default
+// PsoParams), population particles for T iterations
+int ref_run_pso_reference(int kind, const or_world* w, std::size_t D, double alpha, double beta,
+                          std::size_t T, std::size_t population, std::uint64_t seed, double* trace,
+                          double* final_point, double* final_f, double* wall) {
+    try {
+        const auto p = make_problem(kind, D, w, alpha, beta);
+        const RunReport r = run_pso_reference(*p, T, population, seed);
+        if (trace) std::copy(r.trace.begin(), r.trace.end(), trace);
+        if (final_point) std::copy(r.final_point.begin(), r.final_point.end(), final_point);
+        *final_f = r.final_fitness;
+        if (wall) *wall = r.wall_seconds;
+        return 0;
+    } catch (const std::exception&) {
+        return 1;
+    }
+}
+
 // planner.hpp:77-133
 int ref_priori_init(const double* prev, const double* hypers, const or_planner_cfg* c,
                     const double* lo, const double* hi, std::uint64_t seed, double* x, double* v) {

@@ -209,6 +209,11 @@ def ref(kind: str = "philox"):
     _sig(lib, "ref_run_dtpso", C.c_int,
          [C.c_int, W, C.c_size_t, C.c_double, C.c_double, dp, C.c_size_t, C.c_size_t,
           C.c_size_t, C.c_uint64, dp, dp, dp, szp])
+    _sig(lib, "ref_run_dppso_reference", C.c_int,
+         [C.c_int, W, C.c_size_t, C.c_double, C.c_double, dp, C.c_size_t, C.c_size_t, C.c_size_t, C.c_uint64,
+          dp, dp, dp, dp])
+    _sig(lib, "ref_run_pso_reference", C.c_int,
+         [C.c_int, W, C.c_size_t, C.c_double, C.c_double, C.c_size_t, C.c_size_t, C.c_uint64, dp, dp, dp, dp])
     _sig(lib, "ref_priori_init", C.c_int,
          [dp, dp, C.POINTER(PlannerCfg), dp, dp, C.c_uint64, dp, dp])
     _sig(lib, "ref_should_truncate", C.c_int, [dp, C.c_size_t, C.c_int, C.POINTER(PlannerCfg)])

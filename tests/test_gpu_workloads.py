@@ -258,3 +258,18 @@ def test_fp32_record_is_the_reference_evaluation_of_its_path(eng32mt):
     rb, _ = sb.records(0, 12)
     sb.close()
     assert [(r.fitness, r.intersections) for r in rb] == [(r.fitness, r.intersections) for r in recs]
+
+
+# --------------------------------------- the `scale` harness (8(f) 4)
+@pytest.mark.parametrize("shape", [(8, 64, 32, 12), (8, 2048, 64, 4)])
+def test_engine_equals_per_particle_oracle(shape, eng64mt):
+    """proj/tools/swarmforge.cpp:202-255 compares the batched run_dtpso with the
+    per-particle run_dppso_reference (runner.hpp:135-239); the FP64 engine --
+    fused cluster for the small shape, the HBM-staged path for the large one --
+    equals the per-particle oracle's trace and final point bit for bit."""
+    G, N, D, T = shape
+    r = eng64mt.run_dtpso("BF3", DEFAULT_GROUP_HYPERS, G, N, T, 1, dim=D)
+    tr, fp, ff, wall = np.zeros(T), np.zeros(D), C.c_double(0), C.c_double(0)
+    assert _ref().ref_run_dppso_reference(3, None, D, 30.0, 4.0, ptr(np.ascontiguousarray(DEFAULT_GROUP_HYPERS)),
+                                          G, N, T, 1, ptr(tr), ptr(fp), C.byref(ff), C.byref(wall)) == 0
+    assert np.array_equal(r["trace"], tr) and np.array_equal(r["final_point"], fp) and r["final_fitness"] == ff.value

@@ -350,3 +350,28 @@ def test_glibc_cos_restatement(tmp_path):
     # libm through a vectorised ufunc would be numpy's own cos: call libm itself
     want = np.array([libm.cos(float(v)) for v in xs[::7]])
     assert np.array_equal(got[::7], want)
+
+
+# ------------------------------------------- per-particle oracles (8(f) 4)
+def test_scale_harness_batched_equals_per_particle():
+    """The reference's `scale` check (proj/tools/swarmforge.cpp:202-255): the
+    batched run_dtpso and the per-particle run_dppso_reference give identical
+    traces from the same seed -- the wrapped oracle is the reference's own."""
+    r = ref("mt")
+    if r is None:
+        pytest.skip("oracle/_ref not built")
+    G, N, D, T = 8, 16, 8, 25
+    h = np.ascontiguousarray(DEFAULT_GROUP_HYPERS)
+    for kind in (1, 3):
+        ta, fa, ffa = np.zeros(T), np.zeros(D), C.c_double(0)
+        tb, fb, ffb, wall = np.zeros(T), np.zeros(D), C.c_double(0), C.c_double(0)
+        bad = (C.c_size_t * 3)()
+        assert r.ref_run_dtpso(kind, None, D, 30.0, 4.0, ptr(h), G, N, T, 77, ptr(ta), ptr(fa), C.byref(ffa), bad) == 0
+        assert r.ref_run_dppso_reference(kind, None, D, 30.0, 4.0, ptr(h), G, N, T, 77, ptr(tb), ptr(fb),
+                                         C.byref(ffb), C.byref(wall)) == 0
+        assert np.array_equal(ta, tb) and np.array_equal(fa, fb) and ffa.value == ffb.value
+        assert wall.value > 0.0
+    # the classic PSO baseline runs and reports a non-increasing trace
+    tp, fp, ffp, wall = np.zeros(T), np.zeros(D), C.c_double(0), C.c_double(0)
+    assert r.ref_run_pso_reference(1, None, D, 30.0, 4.0, T, 40, 5, ptr(tp), ptr(fp), C.byref(ffp), C.byref(wall)) == 0
+    assert np.all(np.diff(tp) <= 0) and ffp.value == tp[-1]
