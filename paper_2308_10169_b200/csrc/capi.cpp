@@ -162,6 +162,9 @@ constexpr unsigned long long kResidentIdleNs = 1000000ull;   // 1 ms
 bool resident_enabled(sf_ctx* ctx) {
     static const bool off = [] {
         const char* e = std::getenv("SEPSO_RESIDENT");
+#ifdef SEPSO_CHECK
+        return true;        // the consistency build checks each normal launch
+#endif
         return (e && e[0] == '0') || std::getenv("SEPSO_PHASE_PROF") != nullptr;
     }();
     return !off && !ctx->timing;

@@ -256,6 +256,13 @@ int launch_fused(sf_ctx* ctx, FusedPlan& fp, int problem) {
         cudaMemsetAsync(prof, 0, sizeof(long long) * nprof, ctx->stream);
         fp.p.prof = prof;
     }
+#ifdef SEPSO_CHECK
+    long long* dbg = nullptr;
+    const size_t ndbg = size_t(fp.p.n_swarms) * fp.p.C * std::max(fp.p.cap, 1);
+    cudaMalloc(&dbg, ndbg * 8);
+    cudaMemsetAsync(dbg, 0xff, ndbg * 8, ctx->stream);
+    fp.p.dbg = dbg;
+#endif
     cudaEvent_t pe0 = nullptr, pe1 = nullptr;
     if (prof) {
         cudaEventCreate(&pe0);
@@ -343,6 +350,28 @@ int launch_fused(sf_ctx* ctx, FusedPlan& fp, int problem) {
         }
         std::fprintf(stderr, "\n");
     }
+#ifdef SEPSO_CHECK
+    {   // every CTA of a cluster must have taken the same decision at every iteration it ran
+        std::vector<long long> h(ndbg);
+        cudaMemcpyAsync(h.data(), dbg, ndbg * 8, cudaMemcpyDeviceToHost, ctx->stream);
+        cudaStreamSynchronize(ctx->stream);
+        cudaFree(dbg);
+        fp.p.dbg = nullptr;
+        const int C = fp.p.C, cap = std::max(fp.p.cap, 1);
+        if (std::getenv("SEPSO_CHECK_SELFTEST") && ndbg > 1) h[1] ^= 1;   // the comparison must catch this
+        for (int sw = 0; sw < fp.p.n_swarms; ++sw) {
+            if (fp.p.cap > 0 && h[size_t(sw) * C * cap] == -1)
+                return fail(SF_RUNTIME_ERROR, "consistency check: no decision logged");
+            for (int k = 0; k < cap; ++k) {
+                const long long r0 = h[(size_t(sw) * C) * cap + k];
+                for (int cc = 1; cc < C; ++cc)
+                    if (h[(size_t(sw) * C + cc) * cap + k] != r0)
+                        return fail(SF_RUNTIME_ERROR, "consistency check: CTA decisions differ in swarm " +
+                                                          std::to_string(sw) + " iteration " + std::to_string(k + 1));
+            }
+        }
+    }
+#endif
     if (e != 0) return cuda_fail(cudaError_t(e), "fused swarm launch");
     if (ctx->timing) {
         cudaEventRecord(ctx->ev1, ctx->stream);

@@ -888,6 +888,18 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
         }
         __syncthreads();
         SEPSO_MARK(9);
+#ifdef SEPSO_CHECK
+        // consistency build: every CTA logs its iteration decision (stop,
+        // status, new-tbest group, the changed slots) for the host to compare
+        // across the cluster -- the exchange has no closing barrier and relies
+        // on identical decisions everywhere
+        if (tid == 0 && p.dbg) {
+            unsigned long long h = (unsigned long long)(c.m->stop & 1) | ((unsigned long long)(c.m->status & 3) << 1) |
+                                   ((unsigned long long)(c.m->tsrc_slot + 1) << 3) | ((unsigned long long)k << 16);
+            for (int g = 0; g < G && g < 8; ++g) h ^= (unsigned long long)(c.chg[g] + 1) << (24 + 5 * g);
+            p.dbg[(size_t(swarm) * p.C + c.crank) * p.cap + (k - 1)] = (long long)h;
+        }
+#endif
         if (c.m->status) break;
         SEPSO_MARK(10);
         const int tg = c.m->tsrc_slot;                     // new tbest's group or -1

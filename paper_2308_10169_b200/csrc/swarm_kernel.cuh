@@ -117,6 +117,8 @@ struct SwarmParams {
     int inl, in_seed, in_world, in_hyp, in_prev, in_has_prev, in_lo, in_hi, in_win, in_win_len;
     // resident planner (inl layout, one swarm): jobs from here; nullptr = one pass
     ServerCtl* srv;
+    // consistency build (-DSEPSO_CHECK): per swarm, CTA and iteration decision words
+    long long* dbg;
 };
 
 // Small host-buffer launches (one paper scene: ~1.8 KB of inputs) pass their
