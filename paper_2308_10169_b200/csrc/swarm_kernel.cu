@@ -314,7 +314,9 @@ __device__ __forceinline__ int at_decide_regs(double w, int lane, int tw, double
 // budget follows from it (64 at 1024 threads, 72 at 896): the latency launch of
 // one paper scene (85 rows x 9 segments + 4 generator warps = 896 threads) gets
 // its own instantiation so its hot loop does not spill at the 1024-thread cap.
-template <class T, bool PATH, bool RING, int MAXT = 1024>
+// SERVER: the resident-planner instantiation (jobs loop, p.srv); the one-pass
+// instantiations carry none of its state, so their hot loop keeps its registers.
+template <class T, bool PATH, bool RING, int MAXT = 1024, bool SERVER = false>
 __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ SwarmParams p,
                                                         const __grid_constant__ ParamPayload pl,
                                                         const __grid_constant__ LaunchDerived ld, int problem) {
@@ -366,16 +368,21 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
     // resident planner (p.srv): the cluster serves one frame per posted job,
     // its inputs copied from pinned host memory into shared memory; otherwise
     // the loop body runs once on the launch's own inputs
-    ServerCtl* const srv = p.srv;
+    ServerCtl* const srv = SERVER ? p.srv : nullptr;
     unsigned char* const jobsm = srv ? S8(L.job) : nullptr;
     const unsigned char* const jb = srv ? jobsm : pl.bytes;
     uint32_t jseq = 0;
     if (srv) jseq = srv->done_seq;  // the last job served before this launch (the host is not posting while it reads)
-    long long kg = 0;              // iterations over all jobs: mbarrier buffer and phase parity
-    bool cl_waited = false;        // the launch's cluster_arrive has been matched
+    if (srv) cluster_wait();       // the resident cluster matches the launch's cluster_arrive up front
     for (;;) {
     if (srv) {
-        if (!cl_waited) { cluster_wait(); cl_waited = true; }
+        // every job starts its exchange mbarriers at phase 0 (all phases of the
+        // last job completed); the cluster barrier inside publishes the init
+        if (tid == 0) {
+            mbar_init(mbar0, 1);
+            mbar_init(mbar0 + 8, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
         jseq = server_next_job(srv, jseq, reinterpret_cast<uint32_t*>(S8(L.srvcmd)), jobsm, c.crank, c.C);
         if (jseq == 0) break;
         if (c.crank == 0 && tid == 0) { srv->t_ready = global_ns(); srv->c_ready = clock64(); }
@@ -528,7 +535,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
     if (srv && c.crank == 0 && tid == 0) srv->t_init = global_ns();
 
     // ------------------------------------------------------------ iterations
-    if (p.cap < 1 && !cl_waited) { cluster_wait(); cl_waited = true; }
+    if (p.cap < 1 && !srv) cluster_wait();
     // Best update fast path (FP32, G <= 32, tw <= 32): warp 0 keeps the bests
     // and the AT window in registers -- lane g group g's gbest value and Q,
     // lane i window slot i -- so the chain of the single-warp phase is a few
@@ -550,8 +557,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
     const double inv_tw = p.tw > 0 ? 1.0 / double(p.tw) : 0.0;
     int k = 1;
     for (; k <= p.cap; ++k) {
-        ++kg;
-        const int buf = int(kg & 1);
+        const int buf = k & 1;
         SEPSO_MARK(0);
         if (wprof) wt0 = clock64();
         // fitness (geometry.hpp:262-267 / benchmarks.hpp:45-53)
@@ -595,7 +601,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
         }
         SEPSO_MARK(5);
         if (tid == 0) mbar_expect(mbar0 + 8 * buf, xbytes);
-        if (!cl_waited) { cluster_wait(); cl_waited = true; }   // every peer is running, its mbarriers initialised
+        if (k == 1 && !srv) cluster_wait();    // every peer is running, its mbarriers initialised
         // per-CTA group partials: (pbest_f, row) lexicographic min, one warp per group
         for (int lg = warp; lg < c.LG; lg += nthr >> 5) {
             const int g = gfirst + lg;
@@ -665,7 +671,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
         }
         long long wt1 = 0;
         if (wprof) wt1 = clock64();
-        if (warp == 0) mbar_wait(mbar0 + 8 * buf, uint32_t(((kg - 1) >> 1) & 1));   // every CTA's partials
+        if (warp == 0) mbar_wait(mbar0 + 8 * buf, uint32_t(((k - 1) >> 1) & 1));   // every CTA's partials
         if (wprof) {
             wprof[(size_t(k - 1) * 16 + c.crank) * 2] = wt1 - wt0;
             wprof[(size_t(k - 1) * 16 + c.crank) * 2 + 1] = clock64() - wt1;
@@ -1088,12 +1094,12 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
 // ------------------------------------------------------------------ launcher
 constexpr int kMaxDevices = 64;
 
-template <class T, bool PATH, bool RING, int MAXT = 1024>
+template <class T, bool PATH, bool RING, int MAXT = 1024, bool SERVER = false>
 static int launch_t(const SwarmParams& p, const ParamPayload* pl, int problem, cudaStream_t st,
                     size_t* smem_out) {
     const SmemLayout L = smem_layout(p, sizeof(T), PATH);
     if (smem_out) *smem_out = L.total;
-    auto kern = swarm_kernel<T, PATH, RING, MAXT>;
+    auto kern = swarm_kernel<T, PATH, RING, MAXT, SERVER>;
     cudaError_t e = cudaSuccess;
     // attributes are sticky per function AND per device: cache them per ordinal
     static thread_local size_t smem_set[kMaxDevices] = {};
@@ -1153,10 +1159,19 @@ int launch_swarms(const SwarmParams& p, const ParamPayload* pl, int problem, boo
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const bool path = problem == kPath;
     const bool ring = p.entry_cap > 0;
+    const bool lat = p.nthreads <= 896;
+    if (p.srv) {                      // resident planner: one path swarm, latency shapes
+        if (!path || ring) return int(cudaErrorInvalidValue);
+        if (fp64) return lat ? launch_t<double, true, false, 896, true>(p, pl, problem, st, smem)
+                             : launch_t<double, true, false, 1024, true>(p, pl, problem, st, smem);
+        return lat ? launch_t<float, true, false, 896, true>(p, pl, problem, st, smem)
+                   : launch_t<float, true, false, 1024, true>(p, pl, problem, st, smem);
+    }
+    if (fp64 && path && !ring && lat) return launch_t<double, true, false, 896>(p, pl, problem, st, smem);
     if (fp64) return path ? (ring ? launch_t<double, true, true>(p, pl, problem, st, smem)
                                   : launch_t<double, true, false>(p, pl, problem, st, smem))
                           : launch_t<double, false, false>(p, pl, problem, st, smem);
-    if (path && !ring && p.nthreads <= 896) return launch_t<float, true, false, 896>(p, pl, problem, st, smem);
+    if (path && !ring && lat) return launch_t<float, true, false, 896>(p, pl, problem, st, smem);
     return path ? (ring ? launch_t<float, true, true>(p, pl, problem, st, smem)
                         : launch_t<float, true, false>(p, pl, problem, st, smem))
                 : launch_t<float, false, false>(p, pl, problem, st, smem);

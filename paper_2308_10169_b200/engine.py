@@ -184,6 +184,8 @@ def lib():
                                             C.c_uint32, Pr, _dp, _u64p]),
     }
     for name, (res, args) in sig.items():
+        if os.environ.get("SEPSO_LIB") and not hasattr(L, name):
+            continue            # an older experiment build (A/B timing): bind what it has
         f = getattr(L, name)
         f.restype, f.argtypes = res, args
     _LIB = L
