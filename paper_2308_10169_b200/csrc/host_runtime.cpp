@@ -314,6 +314,17 @@ int launch_fused(sf_ctx* ctx, FusedPlan& fp, int problem) {
             }
             if (qi) std::fprintf(stderr, " | B1: bad=%.0f gbest=%.0f tbest=%.0f push=%.0f at=%.0f", q[0] / qi,
                                  q[1] / qi, q[2] / qi, q[3] / qi, q[4] / qi);
+            double pp[4] = {0};
+            int pn = 0;
+            for (int k = 0; k < iters; ++k) {
+                const long long* r = h.data() + size_t(k) * kProfPhases;
+                if (r[19] == 0 || r[20] == 0 || r[21] == 0 || r[5] == 0 || r[6] == 0) continue;
+                ++pn;
+                pp[0] += double(r[19] - r[5]); pp[1] += double(r[20] - r[19]); pp[2] += double(r[21] - r[20]);
+                pp[3] += double(r[6] - r[21]);
+            }
+            if (pn) std::fprintf(stderr, " | part: reduce=%.0f push_part=%.0f push_rows=%.0f push_bad=%.0f", pp[0] / pn,
+                                 pp[1] / pn, pp[2] / pn, pp[3] / pn);
         }
         {   // init marks (row cap): start, consts, seeded, x, v, rest, put, loop
             const long long* r = h.data() + size_t(fp.p.cap) * kProfPhases;

@@ -1,0 +1,15 @@
+// swarm_inst_fp64.cu -- instantiations of the fused kernel (see swarm_inst.hpp).
+#include "swarm_kernel_body.cuh"
+#include "swarm_inst.hpp"
+
+namespace sepso {
+template <class T, bool PATH, bool RING, int MAXT, bool SERVER>
+int launch_inst(const SwarmParams& p, const ParamPayload* pl, int problem, cudaStream_t st, size_t* smem_out) {
+    return launch_t<T, PATH, RING, MAXT, SERVER>(p, pl, problem, st, smem_out);
+}
+template int launch_inst<double, true, false, 896, false>(const SwarmParams&, const ParamPayload*, int, cudaStream_t, size_t*);
+template int launch_inst<double, true, false, 896, true>(const SwarmParams&, const ParamPayload*, int, cudaStream_t, size_t*);
+template int launch_inst<double, true, false, 1024, true>(const SwarmParams&, const ParamPayload*, int, cudaStream_t, size_t*);
+template int launch_inst<double, true, true, 1024, false>(const SwarmParams&, const ParamPayload*, int, cudaStream_t, size_t*);
+template int launch_inst<double, true, false, 1024, false>(const SwarmParams&, const ParamPayload*, int, cudaStream_t, size_t*);
+}  // namespace sepso

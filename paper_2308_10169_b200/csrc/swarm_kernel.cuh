@@ -135,7 +135,7 @@ constexpr bool kProfiling = true;
 #else
 constexpr bool kProfiling = false;
 #endif
-constexpr int kProfPhases = 22;   // 0..11 phase marks, 12/13 generator start/end, 14 B1 end, 15..18 inside B1
+constexpr int kProfPhases = 24;   // 0..11 phase marks, 12/13 generator start/end, 14 B1 end, 15..18 inside B1, 19..21 inside the partials
 
 // One CTA's best (pbest_f, row) of one group, read by its peers over DSMEM in
 // a single 16-byte load.
