@@ -8,6 +8,5 @@ int launch_inst(const SwarmParams& p, const ParamPayload* pl, int problem, cudaS
     return launch_t<T, PATH, RING, MAXT, SERVER>(p, pl, problem, st, smem_out);
 }
 template int launch_inst<float, true, true, 1024, false>(const SwarmParams&, const ParamPayload*, int, cudaStream_t, size_t*);
-template int launch_inst<float, true, true, 512, false>(const SwarmParams&, const ParamPayload*, int, cudaStream_t, size_t*);
 template int launch_inst<float, true, false, 1024, false>(const SwarmParams&, const ParamPayload*, int, cudaStream_t, size_t*);
 }  // namespace sepso

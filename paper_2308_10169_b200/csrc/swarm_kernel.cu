@@ -26,8 +26,7 @@ int launch_swarms(const SwarmParams& p, const ParamPayload* pl, int problem, boo
                    : launch_inst<double, true, false, 1024, false>(p, pl, problem, st, smem);
     }
     if (!path) return launch_inst<float, false, false, 1024, false>(p, pl, problem, st, smem);
-    if (ring) return p.nthreads <= 512 ? launch_inst<float, true, true, 512, false>(p, pl, problem, st, smem)
-                                       : launch_inst<float, true, true, 1024, false>(p, pl, problem, st, smem);
+    if (ring) return launch_inst<float, true, true, 1024, false>(p, pl, problem, st, smem);
     return lat ? launch_inst<float, true, false, 896, false>(p, pl, problem, st, smem)
                : launch_inst<float, true, false, 1024, false>(p, pl, problem, st, smem);
 }
