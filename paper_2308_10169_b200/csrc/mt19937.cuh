@@ -142,7 +142,28 @@ __device__ inline void mt_generate(MtState& s, const MtGroup& g, long long from,
     long long rel = 312 * s.blocks - from;        // offset of the next new word
     bool pend = s.blocks > 0 && rel > 0 && rel - 624 < len;   // the latest pair
     long long prel = rel - 624;
-    if (FN >= 128 || g.n >= 128) {
+    if (FN == 96) {
+        // three warps (the step generator off the first SM sub-partition, whose
+        // warp runs the serial best update): lanes 0..95 take positions
+        // 0..95, lanes 0..59 also 96..155
+        const int lt = g.lt;
+        const bool second = lt < 60;
+        const int t2 = second ? 96 + lt : 96;
+        while (rel < len) {
+            const unsigned long long* o = s.buf + s.cur * 624 + 312;
+            unsigned long long* nb = s.buf + (s.cur ^ 1) * 624;
+            const MtQuad q1 = mt_quad(o, lt, o[lt + 157], o[lt + 158]);
+            if (second) mt_store_quad(nb, t2, mt_quad_any(o, t2));
+            mt_store_quad(nb, lt, q1);
+            if (pend) mt_deliver_pair<RAW>(s.buf + s.cur * 624, prel, len, g, sink);
+            mt_sync(g);
+            s.cur ^= 1;
+            s.blocks += 2;
+            prel = rel;
+            pend = rel + 624 > 0;
+            rel += 624;
+        }
+    } else if (FN >= 128 || g.n >= 128) {
         const int lt = g.lt;
         const bool act = lt < 128;
         const int w = lt >> 5, l = lt & 31;

@@ -578,9 +578,12 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
         const int gw0 = (nthr >> 5) - 4;
         const bool gen_first = gen_early && gw0 * 32 >= c.P && c.LG <= gw0;
         if (gen_first && warp >= gw0) {
-            long long* gprof = (kProfiling && p.prof != nullptr && swarm == 0 && c.crank == 0 && tid == gw0 * 32) ? p.prof : nullptr;
+            // three of the four warps generate (SM sub-partitions 1-3): the
+            // ALU-bound generator then never competes with warp 0's serial
+            // partial / best-update chain on sub-partition 0
+            long long* gprof = (kProfiling && p.prof != nullptr && swarm == 0 && c.crank == 0 && tid == (gw0 + 1) * 32) ? p.prof : nullptr;
             if (gprof) gprof[(k - 1) * kProfPhases + 12] = clock64();
-            mt_step_draws<128>(c, mtbuf, MtGroup{tid - gw0 * 32, 128, 1}, k, row1);
+            if (warp > gw0) mt_step_draws<96>(c, mtbuf, MtGroup{tid - (gw0 + 1) * 32, 96, 1}, k, row1);
             if (gprof) gprof[(k - 1) * kProfPhases + 13] = clock64();
         } else {
         for (int pl = tid; pl < c.P; pl += nthr) {
