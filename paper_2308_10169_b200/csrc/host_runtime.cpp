@@ -325,6 +325,25 @@ int launch_fused(sf_ctx* ctx, FusedPlan& fp, int problem) {
             }
             if (pn) std::fprintf(stderr, " | part: reduce=%.0f push_part=%.0f push_rows=%.0f push_bad=%.0f", pp[0] / pn,
                                  pp[1] / pn, pp[2] / pn, pp[3] / pn);
+            double e1 = 0, e2 = 0;
+            int en = 0;
+            for (int k = 0; k < iters; ++k) {
+                const long long* r = h.data() + size_t(k) * kProfPhases;
+                if (r[22] == 0 || r[23] == 0 || r[5] == 0) continue;
+                ++en;
+                e1 += double(r[22] - r[5]); e2 += double(r[23] - r[22]);
+            }
+            if (en) std::fprintf(stderr, " | expect=%.0f scan=%.0f", e1 / en, e2 / en);
+            if (std::getenv("SEPSO_SCAN2")) {
+                double a = 0, b = 0;
+                int n2 = 0;
+                for (int k = 0; k < iters; ++k) {
+                    const long long* r = h.data() + size_t(k) * kProfPhases;
+                    if (r[22] == 0 || r[23] == 0 || r[1] == 0) continue;
+                    ++n2; a += double(r[23] - r[22]); b += double(r[1] - r[23]);
+                }
+                if (n2) std::fprintf(stderr, " | scan first=%.0f second=%.0f", a / n2, b / n2);
+            }
         }
         {   // init marks (row cap): start, consts, seeded, x, v, rest, put, loop
             const long long* r = h.data() + size_t(fp.p.cap) * kProfPhases;

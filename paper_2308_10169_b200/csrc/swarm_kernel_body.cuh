@@ -586,6 +586,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
             if (warp > gw0) mt_step_draws<96>(c, mtbuf, MtGroup{tid - (gw0 + 1) * 32, 96, 1}, k, row1);
             if (gprof) gprof[(k - 1) * kProfPhases + 13] = clock64();
         } else {
+        #pragma unroll 1   // serial per-iteration path: compact code (I-cache)
         for (int pl = tid; pl < c.P; pl += nthr) {
             const T f = c.fit[pl];
             if (!isfinite(f)) atomicMin(&c.m->bad_row, c.row0 + pl);
@@ -608,6 +609,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
         }
         SEPSO_MARK(5);
         if (tid == 0) mbar_expect(mbar0 + 8 * buf, xbytes);
+        SEPSO_MARK(22);
         if (k == 1 && !srv) cluster_wait();    // every peer is running, its mbarriers initialised
         // per-CTA group partials: (pbest_f, row) lexicographic min, one warp per group
         for (int lg = warp; lg < c.LG; lg += nthr >> 5) {
@@ -615,10 +617,23 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
             const int l0 = max(c.row0, g * N) - c.row0, l1 = min(row1, (g + 1) * N) - c.row0;
             T bf = A::inf();
             int br = INT_MAX;
+#ifdef SEPSO_EXP_SCAN2
+#pragma unroll 1
+            for (int rep = 0; rep < 2; ++rep) {
+            if (rep == 1 && lg == 0) SEPSO_MARK(23);
+            bf = A::inf(); br = INT_MAX;
+#endif
+            #pragma unroll 1   // serial per-iteration path: compact code (I-cache)
             for (int pl = l0 + lane; pl < l1; pl += 32) {
                 const T f = c.pbf[pl];
                 if (f < bf) { bf = f; br = pl; }                    // lanes scan ascending
             }
+#ifdef SEPSO_EXP_SCAN2
+            }
+            if (lg == 0) SEPSO_MARK(1);
+#else
+            if (lg == 0) SEPSO_MARK(23);
+#endif
             if (sizeof(T) == 4) {
                 const uint32_t key = order_key(float(bf));
                 const uint32_t kmin = __reduce_min_sync(0xffffffffu, key);
@@ -643,6 +658,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
             pt.q = br == INT_MAX ? 0 : c.pbq[br];
             const int brow = br == INT_MAX ? 0 : br;
             const uint32_t mb = mbar0 + 8 * buf;
+            #pragma unroll 1   // serial per-iteration path: compact code (I-cache)
             for (int r = lane; r < c.C; r += 32) {
                 const uint4 v = *reinterpret_cast<const uint4*>(&pt);
                 st_async_v4(peer_addr(smem_addr(c.part + buf * c.C * LGM + slot), r), v, peer_addr(mb, r));
@@ -652,6 +668,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
             if ((D * int(sizeof(T))) % 16 == 0) {                         // 16-byte vectors
                 const int V4 = (D * int(sizeof(T))) / 16;
                 const uint4* src = reinterpret_cast<const uint4*>(c.pb + brow * D);
+                #pragma unroll 1   // serial per-iteration path: compact code (I-cache)
                 for (int t = lane; t < c.C * V4; t += 32) {
                     const int r = int(c.fV.div(uint32_t(t))), q4 = t - r * V4;
                     st_async_v4(peer_addr(dst0 + 16 * q4, r), src[q4], peer_addr(mb, r));
@@ -659,6 +676,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
             } else {                                                      // 4-byte words
                 const int V1 = (D * int(sizeof(T))) / 4;
                 const uint32_t* src = reinterpret_cast<const uint32_t*>(c.pb + brow * D);
+                #pragma unroll 1   // serial per-iteration path: compact code (I-cache)
                 for (int t = lane; t < c.C * V1; t += 32) {
                     const int r = int(c.fV.div(uint32_t(t))), q1 = t - r * V1;
                     st_async_b32(peer_addr(dst0 + 4 * q1, r), src[q1], peer_addr(mb, r));
@@ -704,6 +722,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
                 const Part* parts = c.part + size_t(buf) * c.C * LGM;
                 double bf = double(A::inf());
                 int bslot = -1, bq = 0;
+                #pragma unroll 1   // serial per-iteration path: compact code (I-cache)
                 for (int cc = r_cf; cc <= r_cl; ++cc) {
                     const int slot = cc == r_cf ? r_s0 : cc * LGM;
                     const Part pt = parts[slot];
