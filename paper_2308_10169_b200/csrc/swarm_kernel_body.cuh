@@ -325,6 +325,12 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
                                                         const __grid_constant__ ParamPayload pl,
                                                         const __grid_constant__ LaunchDerived ld, int problem) {
     using A = Ar<T>;
+    // kLat: the FP32 latency instantiation, launched only for the reference's
+    // mt19937 stream, G <= 32, tw <= 32 and a generator-first shape
+    // (launch_swarms checks): the branches it can never take are compiled out,
+    // which keeps the per-iteration code -- fetched again every iteration by
+    // the single-warp phases -- small.
+    constexpr bool kLat = MAXT == 896 && sizeof(T) == 4 && PATH && !RING;
 #ifdef SEPSO_PROFILE
     unsigned long long g_entry_;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry_));
@@ -414,7 +420,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
     // (a 311-step sequential recurrence) while the other warps stage the
     // constants; they synchronise on named barrier 2.
     unsigned long long* const mtbuf = (unsigned long long*)S8(L.mt);
-    const bool mt_on = p.rng == kMt19937;
+    const bool mt_on = kLat || p.rng == kMt19937;
     const int cw = (mt_on && nthr >= 64) ? nthr - 32 : nthr;
     const unsigned char* wrec =
         PATH ? (p.inl ? jb + p.in_world : p.worlds) + size_t(swarm) * size_t(p.world_stride) : nullptr;
@@ -490,7 +496,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
             const T vlo = -vmax;
             c.v[pl * D + d] = A::add(vlo, A::mul(uv, A::sub(vmax, vlo)));
         };
-        if (p.rng == kMt19937) {
+        if (kLat || p.rng == kMt19937) {
             // The reference's sequential stream (mt19937.cuh), walked by warps
             // 0..3 (one per SM sub-partition; named barrier 3) through all 2RD
             // init words; only the words of this CTA's rows are tempered and
@@ -545,7 +551,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
     // lane i window slot i -- so the chain of the single-warp phase is a few
     // warp collectives instead of shared-memory round trips; spilled to Misc /
     // c.win when the loop ends.
-    const bool b1fast = sizeof(T) == 4 && G <= 32 && p.tw <= 32;
+    const bool b1fast = kLat || (sizeof(T) == 4 && G <= 32 && p.tw <= 32);
     float r_gbf = __int_as_float(0x7f800000), r_tbf = __int_as_float(0x7f800000);
     int r_gbq = 0, r_tbq = 0, r_wl = 0, r_wh = 0, r_cf = 0, r_cl = -1, r_s0 = 0;
     double r_win = 0.0;
@@ -574,9 +580,9 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
         // (draw_step_randoms, swarm.hpp:59-70).  When they own no pbest rows and
         // no group partial they start right after the fitness barrier, outside
         // the pbest barrier.
-        const bool gen_early = p.rng == kMt19937 && k < p.cap && nthr >= 192;
+        const bool gen_early = (kLat || (p.rng == kMt19937 && nthr >= 192)) && k < p.cap;
         const int gw0 = (nthr >> 5) - 4;
-        const bool gen_first = gen_early && gw0 * 32 >= c.P && c.LG <= gw0;
+        const bool gen_first = gen_early && (kLat || (gw0 * 32 >= c.P && c.LG <= gw0));
         if (gen_first && warp >= gw0) {
             // three of the four warps generate (SM sub-partitions 1-3): the
             // ALU-bound generator then never competes with warp 0's serial
@@ -691,7 +697,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
         // otherwise the last four warps generate while the partials arrive and
         // warp 0 updates the bests; the factors are read after the barrier that
         // follows B1
-        if (gen_early && !gen_first && warp >= gw0) {
+        if (!kLat && gen_early && !gen_first && warp >= gw0) {
             long long* gprof = (kProfiling && p.prof != nullptr && swarm == 0 && c.crank == 0 && tid == gw0 * 32) ? p.prof : nullptr;
             if (gprof) gprof[(k - 1) * kProfPhases + 12] = clock64();
             mt_step_draws<128>(c, mtbuf, MtGroup{tid - gw0 * 32, 128, 1}, k, row1);
@@ -789,7 +795,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
             }
             if (lane == 0) m->k_done = k;
             SEPSO_MARK(14);
-        } else if (warp == 0) {
+        } else if (!kLat && warp == 0) {
             // gbest, one lane per group: scan the owning CTAs in row order,
             // strict '<' vs the incumbent (runner.hpp:81-87)
             Misc<T>* m = c.m;
@@ -895,11 +901,11 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
             }
             if (lane == 0) m->k_done = k;
             SEPSO_MARK(14);
-        } else if (k < p.cap && p.rng == kMt19937 && !gen_early) {
+        } else if (!kLat && k < p.cap && p.rng == kMt19937 && !gen_early) {
             // small CTAs: warps 1.. walk the stream to this step's factors
             // while warp 0 updates the bests
             if (nthr >= 64) mt_step_draws<0>(c, mtbuf, MtGroup{tid - 32, nthr - 32, 1}, k, row1);
-        } else if (k < p.cap && p.rng == kPhilox) {
+        } else if (!kLat && k < p.cap && p.rng == kPhilox) {
             // meanwhile: this step's draws (draw_step_randoms, swarm.hpp:59-70) --
             // they depend only on (seed, k, row), not on the bests
             const uint64_t base = 2ull * uint64_t(R) * uint64_t(D) + uint64_t(k - 1) * 3ull * uint64_t(R);
@@ -910,9 +916,9 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
                 c.coef[j * c.P + pl] = A::mul(c.hyp[g * 6 + j], u);   // a_j = c_j * r_j
             }
         }
-        if (nthr == 32 && k < p.cap && p.rng == kMt19937)     // single-warp CTA: draws after the bests
+        if (!kLat && nthr == 32 && k < p.cap && p.rng == kMt19937)     // single-warp CTA: draws after the bests
             mt_step_draws<0>(c, mtbuf, MtGroup{tid, 32, 0}, k, row1);
-        if (nthr == 32 && k < p.cap && p.rng == kPhilox) {
+        if (!kLat && nthr == 32 && k < p.cap && p.rng == kPhilox) {
             const uint64_t base = 2ull * uint64_t(R) * uint64_t(D) + uint64_t(k - 1) * 3ull * uint64_t(R);
             for (int t = tid; t < 3 * c.P; t += 32) {
                 const int j = t >= 2 * c.P ? 2 : (t >= c.P ? 1 : 0), pl = t - j * c.P;
