@@ -481,9 +481,30 @@ __device__ void load_world(Ctx<T>& c, const unsigned char* wrec, int off_offsets
 //   A3  fitness = sum of lengths in chain order + alpha * Q^beta.
 // RING: compacted pair tests (throughput launches, stage evaluation); the
 // latency launch instantiates the in-place variant only (smaller hot loop).
+// pbest (runner.hpp:73-80) of local row pl with this iteration's fitness f,
+// incl. the x -> pbest_x row copy and the non-finite detection (runner.hpp:56-61)
+template <class T>
+__device__ __forceinline__ void pbest_row(Ctx<T>& c, int pl, T f) {
+    if (!isfinite(f)) atomicMin(&c.m->bad_row, c.row0 + pl);
+    if (f < c.pbf[pl]) {
+        c.pbf[pl] = f;
+        c.pbq[pl] = c.q[pl];
+        const T* xs = c.x + pl * c.D;
+        T* ps = c.pb + pl * c.D;
+        if (sizeof(T) == 4 && (c.D & 3) == 0) {
+#pragma unroll 1
+            for (int d = 0; d < c.D; d += 4)
+                *reinterpret_cast<float4*>(ps + d) = *reinterpret_cast<const float4*>(xs + d);
+        } else {
+            for (int d = 0; d < c.D; ++d) ps[d] = xs[d];
+        }
+    }
+    c.q[pl] = 0;
+}
+
 template <class T, bool RING = true>
 __device__ void path_fitness_phase(const SwarmParams& p, Ctx<T>& c, long long* prof_ = nullptr,
-                                   int k = 0) {
+                                   int k = 0, bool fuse_pbest = false) {
     long long* const prof = kProfiling ? prof_ : nullptr;
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int S = c.S, items = c.P * S, O = c.O;
@@ -598,12 +619,14 @@ __device__ void path_fitness_phase(const SwarmParams& p, Ctx<T>& c, long long* p
         if (prof) prof[(k - 1) * kProfPhases + 3] = clock64();
     }
     __syncthreads();
-    // ---- A3
+    // ---- A3 (+ the pbest update of the row, by the same thread, when fused)
     for (int pl = tid; pl < c.P; pl += nthr) {
         T len = T(0);
         for (int s = 0; s < S; ++s) len = Ar<T>::add(len, c.seglen[pl * S + s]);
         const double pen = penalty(p.alpha, p.beta, p.beta_int, c.q[pl]);
-        c.fit[pl] = Ar<T>::add(len, T(pen));
+        const T f = Ar<T>::add(len, T(pen));
+        if (fuse_pbest) pbest_row(c, pl, f);
+        else c.fit[pl] = f;
     }
 }
 

@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
         SEPSO_MARK(0);
         if (wprof) wt0 = clock64();
         // fitness (geometry.hpp:262-267 / benchmarks.hpp:45-53)
-        if (PATH) path_fitness_phase<T, RING>(p, c, prof, k);
+        if (PATH) path_fitness_phase<T, RING>(p, c, prof, k, true);     // A3 thread also updates the pbest
         else bench_fitness_phase(problem, c);
         SEPSO_MARK(4);
         // pbest (runner.hpp:73-80) incl. the x -> pbest_x row copy; non-finite
@@ -592,24 +592,8 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
             if (warp > gw0) mt_step_draws<96>(c, mtbuf, MtGroup{tid - (gw0 + 1) * 32, 96, 1}, k, row1);
             if (gprof) gprof[(k - 1) * kProfPhases + 13] = clock64();
         } else {
-        #pragma unroll 1   // serial per-iteration path: compact code (I-cache)
-        for (int pl = tid; pl < c.P; pl += nthr) {
-            const T f = c.fit[pl];
-            if (!isfinite(f)) atomicMin(&c.m->bad_row, c.row0 + pl);
-            if (f < c.pbf[pl]) {
-                c.pbf[pl] = f;
-                c.pbq[pl] = c.q[pl];
-                const T* xs = c.x + pl * D;
-                T* ps = c.pb + pl * D;
-                if (sizeof(T) == 4 && (D & 3) == 0) {
-                    for (int d = 0; d < D; d += 4)
-                        *reinterpret_cast<float4*>(ps + d) = *reinterpret_cast<const float4*>(xs + d);
-                } else {
-                    for (int d = 0; d < D; ++d) ps[d] = xs[d];
-                }
-            }
-            if (PATH) c.q[pl] = 0;
-        }
+        if (!PATH)                                   // path swarms: fused into A3 above
+            for (int pl = tid; pl < c.P; pl += nthr) pbest_row(c, pl, c.fit[pl]);
         if (gen_first) asm volatile("bar.sync 2, %0;" ::"r"(gw0 * 32) : "memory");   // pbest done (not the generator)
         else __syncthreads();
         }
