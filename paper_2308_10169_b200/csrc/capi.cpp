@@ -39,11 +39,22 @@ struct DeviceGuard {
 size_t al(size_t v) { return (v + 15) & ~size_t(15); }
 
 struct Io {
-    size_t world, hyp, seed, prev, has_prev, lo, hi, win, win_len, out, best, trace, end;
+    size_t world, hyp, seed, prev, has_prev, lo, hi, win, win_len, mtst, out, best, trace, end;
 };
 
+// std::mt19937_64(seed)'s state (the standard's seeding recurrence,
+// rng.hpp:13-28 constructs the engine from the seed): 312 words
+void mt_seeded_state(uint64_t seed, uint64_t* st) {
+    uint64_t x = seed;
+    st[0] = x;
+    for (int i = 1; i < 312; ++i) {
+        x = 6364136223846793005ull * (x ^ (x >> 62)) + uint64_t(i);
+        st[i] = x;
+    }
+}
+
 Io io_layout(uint32_t n, size_t world_stride, uint32_t G, uint32_t D, uint32_t cap, uint32_t tw,
-             bool per_swarm_hypers) {
+             bool per_swarm_hypers, bool mt_state = false) {
     Io o{};
     size_t at = 0;
     auto take = [&](size_t b) { const size_t r = at; at = al(at + b); return r; };
@@ -56,6 +67,7 @@ Io io_layout(uint32_t n, size_t world_stride, uint32_t G, uint32_t D, uint32_t c
     o.hi = take(size_t(D) * 8);
     o.win = take(size_t(n) * std::max<uint32_t>(tw, 1) * 8);
     o.win_len = take(size_t(n) * 4);
+    o.mtst = take(mt_state ? size_t(n) * 312 * 8 : 0);
     o.out = take(size_t(n) * sizeof(SwarmOut));
     o.best = take(size_t(n) * D * 8);
     o.trace = take(size_t(n) * cap * 8);
@@ -348,7 +360,12 @@ int run_batch(sf_ctx* ctx, const BatchIn& b, BatchOut& r) {
         return SF_OK;
     }
     SwarmParams& p = fp.p;
-    const Io io = io_layout(b.n, path ? wp.lay.stride : 0, b.G, b.D, b.cap, b.tw, b.per_swarm_hypers);
+    // the seeded generator state travels with the inputs when they go inline
+    // (one scene): ~0.3 us on the host instead of ~6 us on one device thread
+    const bool mt = ctx->rng == SF_RNG_MT19937;
+    Io io = io_layout(b.n, path ? wp.lay.stride : 0, b.G, b.D, b.cap, b.tw, b.per_swarm_hypers, mt);
+    if (mt && io.out > size_t(kInlineBytes))
+        io = io_layout(b.n, path ? wp.lay.stride : 0, b.G, b.D, b.cap, b.tw, b.per_swarm_hypers, false);
     int st = ensure_io(ctx, io.end);
     if (st != SF_OK) return st;
     unsigned char* h = static_cast<unsigned char*>(ctx->hio.p);
@@ -414,12 +431,17 @@ int run_batch(sf_ctx* ctx, const BatchIn& b, BatchOut& r) {
     // block instead of a separate H2D copy; larger ones take the copy
     static thread_local ParamPayload payload;
     cudaError_t ce = cudaSuccess;
+    p.in_mtst = -1;
     if (io.out <= size_t(kInlineBytes) && std::getenv("SEPSO_NO_INLINE") == nullptr) {
+        if (io.mtst != io.out)
+            for (uint32_t sw = 0; sw < b.n; ++sw)
+                mt_seeded_state(b.seeds[sw], reinterpret_cast<uint64_t*>(h + io.mtst) + size_t(sw) * 312);
         std::memcpy(payload.bytes, h, io.out);
         p.inl = 1;
         p.in_seed = int(io.seed); p.in_world = int(io.world); p.in_hyp = int(io.hyp);
         p.in_prev = int(io.prev); p.in_has_prev = int(io.has_prev); p.in_lo = int(io.lo);
         p.in_hi = int(io.hi); p.in_win = int(io.win); p.in_win_len = int(io.win_len);
+        p.in_mtst = io.mtst != io.out ? int(io.mtst) : -1;
         fp.payload = &payload;
     } else {
         p.inl = 0;

@@ -347,8 +347,9 @@ int launch_fused(sf_ctx* ctx, FusedPlan& fp, int problem) {
         }
         {   // init marks (row cap): start, consts, seeded, x, v, rest, put, loop
             const long long* r = h.data() + size_t(fp.p.cap) * kProfPhases;
-            std::fprintf(stderr, " | init: consts=%lld seed=%lld x=%lld v=%lld rest=%lld sync=%lld",
-                         r[1] - r[0], r[2] - r[1], r[3] - r[2], r[4] - r[3], r[5] - r[4], r[6] - r[5]);
+            std::fprintf(stderr, " | init: consts=%lld seed=%lld x=%lld v=%lld rest=%lld sync=%lld (seeded at %lld, staged at %lld)",
+                         r[1] - r[0], r[2] - r[1], r[3] - r[2], r[4] - r[3], r[5] - r[4], r[6] - r[5],
+                         r[13] - r[0], r[14] - r[0]);
             std::fprintf(stderr, " | ns: init=%lld loop=%lld out=%lld exit=%lld total=%lld",
                          r[8] - r[7], r[9] - r[8], r[10] - r[9], r[11] - r[10], r[11] - r[7]);
             float ev_ms = 0.f;

@@ -81,7 +81,7 @@ struct ServerCtl {
     unsigned long long t_pick, t_ready, t_done;   // %globaltimer of the last job: seen, inputs staged, published
     long long c_ready, c_done;                    // clock64 at staged / published (the SM clock over the frame)
     unsigned long long t_init, t_loop, t_iter;    // %globaltimer after the initialisation / the record / the iterations
-    alignas(16) unsigned char job[3328];   // = kInlineBytes
+    alignas(16) unsigned char job[4608];   // = kInlineBytes
 };
 
 struct SwarmParams {
@@ -115,6 +115,10 @@ struct SwarmParams {
     // in_* are their byte offsets there (seeds, worlds, hypers, prev, has_prev,
     // lo, hi, window values, window lengths)
     int inl, in_seed, in_world, in_hyp, in_prev, in_has_prev, in_lo, in_hi, in_win, in_win_len;
+    // inline inputs may carry each swarm's seeded mt19937_64 state (312 words,
+    // computed by the host from the seed: the standard's 311-step sequential
+    // recurrence, ~6 us on one device thread); -1 = seed on the device
+    int in_mtst;
     // resident planner (inl layout, one swarm): jobs from here; nullptr = one pass
     ServerCtl* srv;
     // consistency build (-DSEPSO_CHECK): per swarm, CTA and iteration decision words
@@ -123,7 +127,7 @@ struct SwarmParams {
 
 // Small host-buffer launches (one paper scene: ~1.8 KB of inputs) pass their
 // inputs as a kernel parameter block, copied with the launch itself.
-constexpr int kInlineBytes = 3328;
+constexpr int kInlineBytes = 4608;   // one paper scene: 1,760 B of inputs + the 2,496 B seeded mt19937 state
 struct ParamPayload {
     unsigned char bytes[kInlineBytes];
 };

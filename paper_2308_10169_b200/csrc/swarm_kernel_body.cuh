@@ -425,8 +425,17 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
     const unsigned char* wrec =
         PATH ? (p.inl ? jb + p.in_world : p.worlds) + size_t(swarm) * size_t(p.world_stride) : nullptr;
     c.O = 0;
+    const unsigned long long* seeded =
+        (p.inl && p.in_mtst >= 0) ? reinterpret_cast<const unsigned long long*>(jb + p.in_mtst) + size_t(swarm) * 312
+                                  : nullptr;
     if (tid >= cw) {
-        if (tid == cw) mt_seed_words(mtbuf + 312, seed);
+        if (seeded) {                         // the host's seeded state, one warp copies it
+            for (int i = tid - cw; i < 312; i += nthr - cw) mtbuf[312 + i] = seeded[i];
+        } else if (tid == cw) {
+            mt_seed_words(mtbuf + 312, seed);
+        }
+        if (kProfiling && tid == cw && p.prof != nullptr && swarm == 0 && c.crank == 0)
+            p.prof[p.cap * kProfPhases + 13] = clock64();
         if (PATH) world_regs(c, wrec);
     } else {
         const double* hyp_src = (p.inl ? reinterpret_cast<const double*>(jb + p.in_hyp) : p.hypers) +
@@ -449,7 +458,10 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
             const int wl = p.carry ? (p.inl ? reinterpret_cast<const int*>(jb + p.in_win_len) : p.win_len)[swarm] : 0;
             m->win_len = wl < p.tw ? wl : p.tw;
             m->win_head = 0;
-            if (mt_on && cw == nthr) mt_seed_words(mtbuf + 312, seed);
+            if (mt_on && cw == nthr) {
+                if (seeded) for (int i = 0; i < 312; ++i) mtbuf[312 + i] = seeded[i];
+                else mt_seed_words(mtbuf + 312, seed);
+            }
         }
         if (p.carry)
             for (int i = tid; i < p.tw; i += cw)
@@ -461,6 +473,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
         }
         for (int cc = tid; cc < c.C; cc += cw) c.ctab[cc] = (cc * p.rows_per_cta) / N;
         for (int pl = tid; pl < c.P; pl += cw) { c.pbf[pl] = A::inf(); c.pbq[pl] = 0; c.q[pl] = 0; }
+        SEPSO_IMARK(14);
     }
     __syncthreads();
     SEPSO_IMARK(1);
