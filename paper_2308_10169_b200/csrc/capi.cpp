@@ -1430,6 +1430,7 @@ struct sf_scene_batch {
     WorldLayout lay{};
     FusedPlan fp;
     DevBuf worlds, hyp, roots, ones, win_vals, win_len, out, best, trace;
+    DevBuf mtst[2];          // seeded mt19937 states: frame f reads [f & 1], leaves frame f + 1's in the other
     bool staged = false;
 };
 
@@ -1485,6 +1486,10 @@ int sf_scene_batch_create(sf_ctx* ctx, uint32_t n, const sf_scenario_config* cfg
     alloc(b->out, size_t(max_frames) * n * sizeof(SwarmOut));
     alloc(b->best, size_t(max_frames) * n * D * 8);
     alloc(b->trace, size_t(n) * cap * 8);
+    if (ctx->rng == SF_RNG_MT19937) {
+        alloc(b->mtst[0], size_t(n) * 312 * 8);
+        alloc(b->mtst[1], size_t(n) * 312 * 8);
+    }
     if (e != cudaSuccess) {
         delete b;
         return cuda_fail(e, "scene batch allocation");
@@ -1546,6 +1551,9 @@ int sf_scene_batch_run(sf_scene_batch* b, uint32_t frames) {
         p.out = static_cast<SwarmOut*>(b->out.p) + size_t(f) * b->n;
         p.off_vel = int(b->lay.off_vel);
         p.step_dt = b->dt;                       // the world step rides on the planning launch
+        const bool mtp = b->mtst[0].p != nullptr;
+        p.mt_pre = (mtp && f > 0) ? static_cast<const unsigned long long*>(b->mtst[f & 1].p) : nullptr;
+        p.mt_next = mtp ? static_cast<unsigned long long*>(b->mtst[(f + 1) & 1].p) : nullptr;
         int st = launch_fused(ctx, b->fp, kPath);
         if (st) return st;
     }
@@ -1580,7 +1588,7 @@ int sf_scene_batch_destroy(sf_scene_batch* b) {
     cudaSetDevice(b->ctx->device);
     cudaStreamSynchronize(b->ctx->stream);
     for (DevBuf* d : {&b->worlds, &b->hyp, &b->roots, &b->ones, &b->win_vals, &b->win_len, &b->out, &b->best,
-                      &b->trace})
+                      &b->trace, &b->mtst[0], &b->mtst[1]})
         d->release();
     delete b;
     return SF_OK;

@@ -119,6 +119,12 @@ struct SwarmParams {
     // computed by the host from the seed: the standard's 311-step sequential
     // recurrence, ~6 us on one device thread); -1 = seed on the device
     int in_mtst;
+    // scene batches: this frame's seeded states, computed by the previous
+    // frame's launch (nullptr: seed here), and where to leave the next frame's
+    // (derive_seed(root, "plan", frame + 1), seeded by an idle warp during the
+    // init walk); n_swarms x 312 words each
+    const unsigned long long* mt_pre;
+    unsigned long long* mt_next;
     // resident planner (inl layout, one swarm): jobs from here; nullptr = one pass
     ServerCtl* srv;
     // consistency build (-DSEPSO_CHECK): per swarm, CTA and iteration decision words

@@ -426,8 +426,9 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
         PATH ? (p.inl ? jb + p.in_world : p.worlds) + size_t(swarm) * size_t(p.world_stride) : nullptr;
     c.O = 0;
     const unsigned long long* seeded =
-        (p.inl && p.in_mtst >= 0) ? reinterpret_cast<const unsigned long long*>(jb + p.in_mtst) + size_t(swarm) * 312
-                                  : nullptr;
+        p.mt_pre ? p.mt_pre + size_t(swarm) * 312
+                 : ((p.inl && p.in_mtst >= 0) ? reinterpret_cast<const unsigned long long*>(jb + p.in_mtst) + size_t(swarm) * 312
+                                              : nullptr);
     if (tid >= cw) {
         if (seeded) {                         // the host's seeded state, one warp copies it
             for (int i = tid - cw; i < 312; i += nthr - cw) mtbuf[312 + i] = seeded[i];
@@ -533,6 +534,11 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
                 mt_generate(mt, grp, 2 * RD, 2 * RD, [&](int, unsigned long long) {});
                 SEPSO_IMARK(5);
                 if (tid == 0) { c.m->mt_cur = mt.cur; c.m->mt_blocks = mt.blocks; }
+            } else if (p.mt_next && p.roots && c.crank == 0 && tid == grp.n + 32 && nthr > grp.n + 32) {
+                // scene batches: the next frame's seeded generator state, off the
+                // critical path (the walk above takes ~4x as long)
+                const uint64_t next = splitmix64(splitmix64(p.roots[swarm] ^ p.tag_hash) + uint64_t(p.frame_index + 1));
+                mt_seed_words(p.mt_next + size_t(swarm) * 312, next);
             } else if (PATH && sizeof(T) == 4 && c.crank == 0 && tid < grp.n + 32) {
                 // rank 0's first idle warp runs the final record's code once on
                 // dummy input while the generator walks the stream: after an
