@@ -43,6 +43,9 @@ struct WorldLayout {
     size_t off_offsets, off_verts, off_vel, stride;
 };
 
+#ifdef __CUDACC__
+__host__ __device__
+#endif
 inline WorldLayout world_layout(int max_obs, int max_verts) {
     WorldLayout w{max_obs, max_verts, 0, 0, 0, 0};
     w.off_offsets = 96;
@@ -157,7 +160,7 @@ struct Part {
 struct SmemLayout {
     size_t x, v, pb, pbf, pbq, q, fit, imp, seglen, coef, lo, hi, hyp, gbx, gbf, gbq, chg, tbx,
         win, part, px, allpart, allbad, gtab, ctab, obb, ooff, ofl, vert, edge, list, mt, mbar, misc, job,
-        srvcmd, vert64, total;
+        srvcmd, vert64, wcopy, total;
 };
 
 #ifdef __CUDACC__
@@ -210,6 +213,9 @@ SEPSO_LHD SmemLayout smem_layout(const SwarmParams& p, size_t tsz, bool path) {
     L.edge = take(V * 4 * tsz);
     L.list = take(path ? size_t(p.entry_cap) * 4 : 0);
     L.vert64 = take(path && tsz == 4 ? (V * 2 + 4) * 8 : 0);   // FP32 engine: FP64 world for the final record
+    // the world record, staged from HBM in one copy (sized from the shape, so
+    // the fit check at planning time and the launch agree)
+    L.wcopy = take(path ? world_layout(p.max_obs, p.max_verts).stride : 0);
     L.job = take(p.srv ? size_t(kInlineBytes) : 0);     // resident planner: this job's input bytes
     L.srvcmd = take(p.srv ? 16 : 0);                    // resident planner: rank 0's decision
     o = (o + 127) & ~size_t(127);          // generator state on a 128-byte boundary

@@ -424,6 +424,17 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
     const int cw = (mt_on && nthr >= 64) ? nthr - 32 : nthr;
     const unsigned char* wrec =
         PATH ? (p.inl ? jb + p.in_world : p.worlds) + size_t(swarm) * size_t(p.world_stride) : nullptr;
+    if (PATH && !p.inl) {
+        // world record in HBM (scene batches, large inputs): one parallel copy of
+        // the whole fixed-stride record into shared memory, so the header ->
+        // offsets -> vertices reads below are not a chain of DRAM round trips
+        const int nv4 = int(p.world_stride / 16);          // <= the layout's allocation (max_obs, max_verts)
+        unsigned char* wsm = S8(L.wcopy);
+        for (int i = tid; i < nv4; i += nthr)
+            reinterpret_cast<uint4*>(wsm)[i] = __ldcg(reinterpret_cast<const uint4*>(wrec) + i);
+        __syncthreads();
+        wrec = wsm;
+    }
     c.O = 0;
     const unsigned long long* seeded =
         p.mt_pre ? p.mt_pre + size_t(swarm) * 312
