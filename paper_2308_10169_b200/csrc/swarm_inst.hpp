@@ -8,6 +8,6 @@
 #include "swarm_kernel.cuh"
 
 namespace sepso {
-template <class T, bool PATH, bool RING, int MAXT, bool SERVER>
+template <class T, bool PATH, bool RING, int MAXT, bool SERVER, bool FAST>
 int launch_inst(const SwarmParams& p, const ParamPayload* pl, int problem, cudaStream_t st, size_t* smem_out);
 }  // namespace sepso

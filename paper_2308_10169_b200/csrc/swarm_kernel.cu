@@ -17,25 +17,27 @@ int launch_swarms(const SwarmParams& p, const ParamPayload* pl, int problem, boo
     // (swarm_kernel_body.cuh kLat); anything else takes the generic one
     const int gw0 = p.nthreads / 32 - 4;
     const int lgmax = p.max_local_groups;
-    const bool lat32 = lat && p.rng == kMt19937 && p.G <= 32 && p.tw <= 32 && p.nthreads >= 192 &&
-                       gw0 * 32 >= p.rows_per_cta && lgmax <= gw0;
+    const bool fastok = p.rng == kMt19937 && p.G <= 32 && p.tw <= 32 && p.nthreads >= 192 &&
+                        gw0 * 32 >= p.rows_per_cta && lgmax <= gw0;
+    const bool lat32 = lat && fastok;
     if (p.srv) {                      // resident planner: one path swarm, latency shapes
         if (!path || ring) return int(cudaErrorInvalidValue);
-        if (fp64) return lat ? launch_inst<double, true, false, 896, true>(p, pl, problem, st, smem)
-                             : launch_inst<double, true, false, 1024, true>(p, pl, problem, st, smem);
-        return lat32 ? launch_inst<float, true, false, 896, true>(p, pl, problem, st, smem)
-                     : launch_inst<float, true, false, 1024, true>(p, pl, problem, st, smem);
+        if (fp64) return lat ? launch_inst<double, true, false, 896, true, false>(p, pl, problem, st, smem)
+                             : launch_inst<double, true, false, 1024, true, false>(p, pl, problem, st, smem);
+        return lat32 ? launch_inst<float, true, false, 896, true, true>(p, pl, problem, st, smem)
+                     : launch_inst<float, true, false, 1024, true, false>(p, pl, problem, st, smem);
     }
     if (fp64) {
-        if (!path) return launch_inst<double, false, false, 1024, false>(p, pl, problem, st, smem);
-        if (ring) return launch_inst<double, true, true, 1024, false>(p, pl, problem, st, smem);
-        return lat ? launch_inst<double, true, false, 896, false>(p, pl, problem, st, smem)
-                   : launch_inst<double, true, false, 1024, false>(p, pl, problem, st, smem);
+        if (!path) return launch_inst<double, false, false, 1024, false, false>(p, pl, problem, st, smem);
+        if (ring) return launch_inst<double, true, true, 1024, false, false>(p, pl, problem, st, smem);
+        return lat ? launch_inst<double, true, false, 896, false, false>(p, pl, problem, st, smem)
+                   : launch_inst<double, true, false, 1024, false, false>(p, pl, problem, st, smem);
     }
-    if (!path) return launch_inst<float, false, false, 1024, false>(p, pl, problem, st, smem);
-    if (ring) return launch_inst<float, true, true, 1024, false>(p, pl, problem, st, smem);
-    return lat32 ? launch_inst<float, true, false, 896, false>(p, pl, problem, st, smem)
-                 : launch_inst<float, true, false, 1024, false>(p, pl, problem, st, smem);
+    if (!path) return launch_inst<float, false, false, 1024, false, false>(p, pl, problem, st, smem);
+    if (ring) return fastok ? launch_inst<float, true, true, 1024, false, true>(p, pl, problem, st, smem)
+                            : launch_inst<float, true, true, 1024, false, false>(p, pl, problem, st, smem);
+    return lat32 ? launch_inst<float, true, false, 896, false, true>(p, pl, problem, st, smem)
+                 : launch_inst<float, true, false, 1024, false, false>(p, pl, problem, st, smem);
 }
 
 int swarm_smem_bytes(const SwarmParams& p, int problem, bool fp64, size_t* bytes) {
