@@ -509,7 +509,9 @@ def main():
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": K,                        # one fused launch per frame (world step included)
+            # one fused launch per frame (world step included) + the next
+            # frame's init walk (prewalk.cu, side stream) launched with it
+            "gpu_launches": K + (K - 1 if os.environ.get("SEPSO_PREWALK", "1") != "0" else 0),
             "clocks": clk,
             "host_threads": cores,
         }

@@ -11,6 +11,7 @@
 #include <climits>
 #include <cstdio>
 #include <cmath>
+#include <functional>
 #include <limits>
 #include <string>
 #include <vector>
@@ -39,7 +40,7 @@ struct DeviceGuard {
 size_t al(size_t v) { return (v + 15) & ~size_t(15); }
 
 struct Io {
-    size_t world, hyp, seed, prev, has_prev, lo, hi, win, win_len, mtst, out, best, trace, end;
+    size_t world, hyp, seed, prev, has_prev, lo, hi, win, win_len, mtst, pre, out, best, trace, end;
 };
 
 // std::mt19937_64(seed)'s state (the standard's seeding recurrence,
@@ -68,6 +69,7 @@ Io io_layout(uint32_t n, size_t world_stride, uint32_t G, uint32_t D, uint32_t c
     o.win = take(size_t(n) * std::max<uint32_t>(tw, 1) * 8);
     o.win_len = take(size_t(n) * 4);
     o.mtst = take(mt_state ? size_t(n) * 312 * 8 : 0);
+    o.pre = take(mt_state ? sizeof(PreRec) : 0);
     o.out = take(size_t(n) * sizeof(SwarmOut));
     o.best = take(size_t(n) * D * 8);
     o.trace = take(size_t(n) * cap * 8);
@@ -171,6 +173,116 @@ struct sepso::Resident {
 namespace {
 constexpr unsigned long long kResidentIdleNs = 1000000ull;   // 1 ms
 
+// ------------------------------------------------ init walk ahead of time
+// (prewalk.cu).  sf_run_scenario knows the next frame's seed; while frame f
+// plans on its cluster, one CTA on a spare SM walks frame f+1's 2RD init
+// words into the slot frame f does not read.  Frame f+1 finds its seed in a
+// slot and reads the words instead of walking (waiting, bounded, for the
+// walk's flag).  SEPSO_PREWALK=0 turns it off.
+bool prewalk_enabled() {
+    static const bool off = [] {
+        const char* e = std::getenv("SEPSO_PREWALK");
+        return e && e[0] == '0';
+    }();
+    return !off;
+}
+
+// test hook: announce walks but never run them (the planning kernel's fallback)
+bool prewalk_late() {
+    static const bool late = [] {
+        const char* e = std::getenv("SEPSO_PREWALK_TEST");
+        return e && std::string(e) == "late";
+    }();
+    return late;
+}
+
+int prewalk_setup(PreWalk*& W, int n, long long nwords) {
+    if (!W) {
+        W = new PreWalk();
+        cudaError_t e = cudaStreamCreateWithFlags(&W->st, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&W->ev, cudaEventDisableTiming);
+        if (e != cudaSuccess) return cuda_fail(e, "init walk stream");
+    }
+    const size_t wb = size_t(n) * size_t(nwords) * 8, pb = size_t(n) * kPrePairWords * 8;
+    if (W->n < n || W->words[0].n < wb || W->pairs[0].n < pb) {
+        cudaStreamSynchronize(W->st);
+        cudaError_t e = cudaSuccess;
+        for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+            e = W->words[k].ensure(wb);
+            if (e == cudaSuccess) e = W->pairs[k].ensure(pb);
+        }
+        if (e == cudaSuccess && W->flags.n < size_t(2 * n) * 4) {
+            e = W->flags.ensure(size_t(2 * n) * 4);
+            if (e == cudaSuccess) e = cudaMemset(W->flags.p, 0, W->flags.n);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "init walk buffers");
+        W->n = std::max(W->n, n);
+        W->nwords[0] = W->nwords[1] = 0;
+    }
+    return SF_OK;
+}
+
+// the slot holding seed's walk (one swarm), or -1; the slot is consumed
+int prewalk_take(sf_ctx* ctx, uint64_t seed, long long nwords, PreRec* r) {
+    PreWalk* W = ctx->pre;
+    r->valid = 0;
+    if (!W) return -1;
+    for (int k = 0; k < 2; ++k) {
+        if (W->nwords[k] == nwords && W->seed[k] == seed) {
+            r->words = reinterpret_cast<unsigned long long>(W->words[k].p);
+            r->pair = reinterpret_cast<unsigned long long>(W->pairs[k].p);
+            r->flag = reinterpret_cast<unsigned long long>(static_cast<int*>(W->flags.p) + k * W->n);
+            r->seq = W->seq[k];
+            r->valid = 1;
+            W->nwords[k] = 0;
+            return k;
+        }
+    }
+    return -1;
+}
+
+// start the walk of ctx's hinted next seed into the slot the current frame
+// does not read (used: the slot it reads, -1 none)
+int prewalk_kick(sf_ctx* ctx, long long nwords, int used) {
+    PreWalk* W = ctx->pre;
+    if (!W || !ctx->hint_valid) return SF_OK;
+    const int k = used >= 0 ? used ^ 1 : 0;
+    if (++W->next_seq <= 0) W->next_seq = 1;
+    W->seq[k] = W->next_seq;
+    if (prewalk_late()) {
+        W->seed[k] = ctx->hint_seed;
+        W->nwords[k] = nwords;
+        return SF_OK;
+    }
+    const int e = launch_init_walk(1, nullptr, nullptr, 0, 0, ctx->hint_seed, nwords,
+                                   static_cast<unsigned long long*>(W->words[k].p),
+                                   static_cast<unsigned long long*>(W->pairs[k].p),
+                                   static_cast<int*>(W->flags.p) + k * W->n, W->seq[k], W->st);
+    if (e != 0) {
+        W->nwords[k] = 0;
+        return cuda_fail(cudaError_t(e), "init walk launch");
+    }
+    W->seed[k] = ctx->hint_seed;
+    W->nwords[k] = nwords;
+    return SF_OK;
+}
+
+void prewalk_destroy(PreWalk*& W) {
+    if (!W) return;
+    if (W->st) {
+        cudaStreamSynchronize(W->st);
+        cudaStreamDestroy(W->st);
+    }
+    if (W->ev) cudaEventDestroy(W->ev);
+    for (int k = 0; k < 2; ++k) {
+        W->words[k].release();
+        W->pairs[k].release();
+    }
+    W->flags.release();
+    delete W;
+    W = nullptr;
+}
+
 bool resident_enabled(sf_ctx* ctx) {
     static const bool off = [] {
         const char* e = std::getenv("SEPSO_RESIDENT");
@@ -225,7 +337,8 @@ namespace {
 // [0, in_bytes)); the record / best / trace land in the resident output
 // block at the io layout's offsets relative to io.out.
 int resident_run(sf_ctx* ctx, const SwarmParams& fp_p, int problem, const unsigned char* h, size_t in_bytes,
-                 size_t out_off_best, size_t out_off_trace, size_t out_bytes, const unsigned char** results) {
+                 size_t out_off_best, size_t out_off_trace, size_t out_bytes, const unsigned char** results,
+                 const std::function<int()>& after_post) {
     Resident*& Rp = ctx->resident;
     if (!Rp) {
         Rp = new Resident();
@@ -279,6 +392,10 @@ int resident_run(sf_ctx* ctx, const SwarmParams& fp_p, int problem, const unsign
     R.ctl->job_seq = s;
     std::atomic_thread_fence(std::memory_order_seq_cst);
     const double t0 = now_seconds();
+    if (after_post) {                  // host work that overlaps the frame (the next init walk's launch)
+        const int st = after_post();
+        if (st) return st;
+    }
     for (uint64_t spin = 1;; ++spin) {
         if (R.ctl->done_seq == s) break;
         if (R.ctl->alive == 0) {          // the cluster exited (idle) before taking this job: relaunch it
@@ -432,10 +549,25 @@ int run_batch(sf_ctx* ctx, const BatchIn& b, BatchOut& r) {
     static thread_local ParamPayload payload;
     cudaError_t ce = cudaSuccess;
     p.in_mtst = -1;
+    p.in_pre = -1;
+    p.pre_words = nullptr;
+    const long long nwords = 2ll * b.G * b.N * b.D;
+    int pre_used = -1;
+    bool pre_on = false;
     if (io.out <= size_t(kInlineBytes) && std::getenv("SEPSO_NO_INLINE") == nullptr) {
         if (io.mtst != io.out)
             for (uint32_t sw = 0; sw < b.n; ++sw)
                 mt_seeded_state(b.seeds[sw], reinterpret_cast<uint64_t*>(h + io.mtst) + size_t(sw) * 312);
+        if (io.pre != io.out) {
+            PreRec* pr = reinterpret_cast<PreRec*>(h + io.pre);
+            pr->valid = 0;
+            pre_on = b.n == 1 && path && prewalk_enabled() && (ctx->hint_valid || ctx->pre != nullptr);
+            if (pre_on) {
+                if ((st = prewalk_setup(ctx->pre, 1, nwords)) != SF_OK) return st;
+                pre_used = prewalk_take(ctx, b.seeds[0], nwords, pr);
+            }
+            p.in_pre = int(io.pre);
+        }
         std::memcpy(payload.bytes, h, io.out);
         p.inl = 1;
         p.in_seed = int(io.seed); p.in_world = int(io.world); p.in_hyp = int(io.hyp);
@@ -452,7 +584,8 @@ int run_batch(sf_ctx* ctx, const BatchIn& b, BatchOut& r) {
     ctx->last_d2h = io.end - io.out;
     if (b.n == 1 && path && p.inl && zc_out && resident_enabled(ctx)) {
         const unsigned char* res = nullptr;
-        st = resident_run(ctx, p, b.problem, h, io.out, io.best - io.out, io.trace - io.out, io.end - io.out, &res);
+        st = resident_run(ctx, p, b.problem, h, io.out, io.best - io.out, io.trace - io.out, io.end - io.out, &res,
+                          [&]() { return pre_on ? prewalk_kick(ctx, nwords, pre_used) : SF_OK; });
         if (st != SF_OK) return st;
         std::memcpy(r.out.data(), res, sizeof(SwarmOut));
         std::memcpy(r.best.data(), res + (io.best - io.out), size_t(b.D) * 8);
@@ -461,6 +594,7 @@ int run_batch(sf_ctx* ctx, const BatchIn& b, BatchOut& r) {
     }
     st = launch_fused(ctx, fp, b.problem);
     if (st != SF_OK) return st;
+    if (pre_on && (st = prewalk_kick(ctx, nwords, pre_used)) != SF_OK) return st;
     if (!zc_out) {
         ce = cudaMemcpyAsync(h + io.out, d + io.out, io.end - io.out, cudaMemcpyDeviceToHost, ctx->stream);
         if (ce != cudaSuccess) return cuda_fail(ce, "D2H io");
@@ -519,6 +653,7 @@ int sf_ctx_destroy(sf_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     resident_destroy(ctx);
+    prewalk_destroy(ctx->pre);
     if (ctx->side) {
         cudaStreamSynchronize(ctx->side);
         cudaStreamDestroy(ctx->side);
@@ -1309,9 +1444,13 @@ int sf_run_scenario(sf_ctx* ctx, const sf_scenario_config* c, int variant, uint3
             cudaStreamSynchronize(ctx->stream);
         }
         std::vector<double> bp(cfg.dim);
+        // the next frame's seed: its init walk runs while this frame plans
+        ctx->hint_valid = f + 1 < frames;
+        ctx->hint_seed = derive_seed(c->root_seed, "plan", f + 1);
         st = sf_plan_frame(ctx, &w, have_prev ? prev.data() : nullptr, hyp.data(), &cfg,
                            derive_seed(c->root_seed, "plan", f), win.data(), &wl, uint32_t(win.size()),
                            &records[f], bp.data(), nullptr);
+        ctx->hint_valid = false;
         if (st) return st;
         prev = bp;
         have_prev = true;
@@ -1432,6 +1571,9 @@ struct sf_scene_batch {
     DevBuf worlds, hyp, roots, ones, win_vals, win_len, out, best, trace;
     DevBuf mtst[2];          // seeded mt19937 states: frame f reads [f & 1], leaves frame f + 1's in the other
     bool staged = false;
+    // few scenes (spare SMs): frame f + 1's init walks run while frame f plans
+    // (slot (f + 1) & 1, PreWalk::seed = the frame index); replaces mtst
+    PreWalk* pre = nullptr;
 };
 
 extern "C" {
@@ -1486,13 +1628,22 @@ int sf_scene_batch_create(sf_ctx* ctx, uint32_t n, const sf_scenario_config* cfg
     alloc(b->out, size_t(max_frames) * n * sizeof(SwarmOut));
     alloc(b->best, size_t(max_frames) * n * D * 8);
     alloc(b->trace, size_t(n) * cap * 8);
-    if (ctx->rng == SF_RNG_MT19937) {
+    // few scenes leave most SMs idle: there the next frame's init walks run
+    // ahead (one CTA per scene) while a frame plans
+    const long long nwords = 2ll * cfg->groups * cfg->per_group * D;
+    const bool ahead = ctx->rng == SF_RNG_MT19937 && prewalk_enabled() && n * uint32_t(b->fp.p.C) <= 64 && n <= 8;
+    if (ctx->rng == SF_RNG_MT19937 && !ahead) {
         alloc(b->mtst[0], size_t(n) * 312 * 8);
         alloc(b->mtst[1], size_t(n) * 312 * 8);
     }
     if (e != cudaSuccess) {
         delete b;
         return cuda_fail(e, "scene batch allocation");
+    }
+    if (ahead && (st = prewalk_setup(b->pre, int(n), nwords)) != SF_OK) {
+        prewalk_destroy(b->pre);
+        delete b;
+        return st;
     }
     std::vector<uint64_t> roots(n);
     for (uint32_t s = 0; s < n; ++s) roots[s] = cfgs[s].root_seed;
@@ -1554,8 +1705,37 @@ int sf_scene_batch_run(sf_scene_batch* b, uint32_t frames) {
         const bool mtp = b->mtst[0].p != nullptr;
         p.mt_pre = (mtp && f > 0) ? static_cast<const unsigned long long*>(b->mtst[f & 1].p) : nullptr;
         p.mt_next = mtp ? static_cast<unsigned long long*>(b->mtst[(f + 1) & 1].p) : nullptr;
+        PreWalk* W = b->pre;
+        const long long nwords = 2ll * b->cfg.groups * b->cfg.per_group * b->cfg.dim;
+        p.pre_words = nullptr;
+        if (W) {
+            const int k = int(f & 1);
+            if (W->nwords[k] == nwords && W->seed[k] == f) {      // frame f's walk, started during frame f - 1
+                p.pre_words = static_cast<const unsigned long long*>(W->words[k].p);
+                p.pre_pair = static_cast<const unsigned long long*>(W->pairs[k].p);
+                p.pre_flag = static_cast<const int*>(W->flags.p) + k * W->n;
+                p.pre_seq = W->seq[k];
+                W->nwords[k] = 0;
+            }
+            // frame f - 1 (the last reader of slot (f + 1) & 1) is done once
+            // this point of the planning stream is reached
+            cudaEventRecord(W->ev, ctx->stream);
+        }
         int st = launch_fused(ctx, b->fp, kPath);
         if (st) return st;
+        if (W && f + 1 < b->max_frames) {
+            const int k = int((f + 1) & 1);
+            if (++W->next_seq <= 0) W->next_seq = 1;
+            W->seq[k] = W->next_seq;
+            cudaStreamWaitEvent(W->st, W->ev, 0);
+            const int e = prewalk_late() ? 0 : launch_init_walk(int(b->n), nullptr, p.roots, p.tag_hash, int(f + 1), 0, nwords,
+                                           static_cast<unsigned long long*>(W->words[k].p),
+                                           static_cast<unsigned long long*>(W->pairs[k].p),
+                                           static_cast<int*>(W->flags.p) + k * W->n, W->seq[k], W->st);
+            if (e != 0) return cuda_fail(cudaError_t(e), "init walk launch");
+            W->seed[k] = f + 1;
+            W->nwords[k] = nwords;
+        }
     }
     b->frames_done += frames;
     return SF_OK;
@@ -1587,6 +1767,7 @@ int sf_scene_batch_destroy(sf_scene_batch* b) {
     if (!b) return SF_OK;
     cudaSetDevice(b->ctx->device);
     cudaStreamSynchronize(b->ctx->stream);
+    prewalk_destroy(b->pre);
     for (DevBuf* d : {&b->worlds, &b->hyp, &b->roots, &b->ones, &b->win_vals, &b->win_len, &b->out, &b->best,
                       &b->trace, &b->mtst[0], &b->mtst[1]})
         d->release();

@@ -242,6 +242,8 @@ FusedPlan plan_fused(sf_ctx* ctx, int problem, int n_swarms, int G, int N, int D
         if (C >= 16 || want_c > 0) break;
     }
     p.beta_int = 0;
+    p.in_pre = -1;
+    p.in_mtst = -1;
     return fp;
 }
 

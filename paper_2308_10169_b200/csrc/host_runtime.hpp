@@ -39,6 +39,19 @@ struct PinnedBuf {
 
 namespace sepso {
 struct Resident;   // resident planner of sf_plan_frame (capi.cpp)
+
+// The next frame's init walk, ahead of time on a spare SM (prewalk.cu): two
+// slots (frame parity), each n swarms x (2RD words, last generator pair, flag).
+struct PreWalk {
+    DevBuf words[2], pairs[2], flags;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev = nullptr;
+    uint64_t seed[2] = {0, 0};     // single-swarm slots: the seed walked
+    long long nwords[2] = {0, 0};  // 2RD of the walk in the slot (0: empty)
+    int seq[2] = {0, 0};
+    int next_seq = 0;
+    int n = 0;                     // swarms per slot the buffers hold
+};
 }
 
 struct sf_ctx {
@@ -61,6 +74,12 @@ struct sf_ctx {
     void* xuser = nullptr;
     sepso::DevBuf io, scratch, flush;
     sepso::Resident* resident = nullptr;
+    sepso::PreWalk* pre = nullptr;
+    // run_scenario: the seed of the frame after the one being planned
+    // (derive_seed(root, "plan", f + 1)); its init walk starts while this
+    // frame plans
+    bool hint_valid = false;
+    uint64_t hint_seed = 0;
     sepso::PinnedBuf hio;
 };
 

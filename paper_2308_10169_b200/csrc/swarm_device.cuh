@@ -41,6 +41,7 @@ template <class T> struct Misc {
     int mt_cur;                 // mt19937_64 generator bookkeeping (MtState outside generation)
     long long mt_blocks;
     int q64;                    // FP32 engine: Q of the final best path on the FP64 world
+    int pre_ok;                 // the ahead-of-time init walk arrived (prewalk.cu)
 };
 
 // alpha * q^beta (geometry.hpp:240): exact repeated product for small integer

@@ -128,10 +128,24 @@ struct SwarmParams {
     // init walk); n_swarms x 312 words each
     const unsigned long long* mt_pre;
     unsigned long long* mt_next;
+    // the init walk done ahead of time (prewalk.cu): per swarm 2RD tempered
+    // words, the generator's last pair + block count (kPrePairWords), and a
+    // flag that reads pre_seq once they are complete; nullptr = walk here.
+    // Inline inputs carry the same in a PreRec at byte in_pre (-1: none).
+    const unsigned long long* pre_words;
+    const unsigned long long* pre_pair;
+    const int* pre_flag;
+    int pre_seq, in_pre;
     // resident planner (inl layout, one swarm): jobs from here; nullptr = one pass
     ServerCtl* srv;
     // consistency build (-DSEPSO_CHECK): per swarm, CTA and iteration decision words
     long long* dbg;
+};
+
+constexpr int kPrePairWords = 640;   // 624 generator words + the block count, padded
+struct PreRec {                      // inline form of the pre_* fields (one swarm)
+    unsigned long long words, pair, flag;
+    int seq, valid;
 };
 
 // Small host-buffer launches (one paper scene: ~1.8 KB of inputs) pass their
@@ -234,5 +248,12 @@ int max_smem_per_block();
 // the reference's exact operation order).
 int launch_step_worlds(unsigned char* worlds, int n, long long stride, int off_offsets,
                        int off_verts, int off_vel, double dt, void* stream);
+
+// prewalk.cu: n swarms' init walks (seeds[s]; derive_seed(roots[s], tag,
+// frame) when seeds is null; seed0 when both are) into words / pairs,
+// flags[s] = seq at the end.
+int launch_init_walk(int n, const unsigned long long* seeds, const unsigned long long* roots,
+                     unsigned long long tag_hash, int frame, unsigned long long seed0, long long nwords,
+                     unsigned long long* words, unsigned long long* pairs, int* flags, int seq, void* stream);
 
 } // namespace sepso

@@ -159,6 +159,18 @@ __device__ __forceinline__ unsigned long long global_ns() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+
+// Wait (bounded, ~2 ms) until the ahead-of-time init walk publishes seq.
+static __device__ bool pre_wait(const int* flag, int seq) {
+    const unsigned long long t0 = global_ns();
+    for (;;) {
+        int v;
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+        if (v == seq) return true;
+        if (global_ns() - t0 > 2000000ull) return false;
+        __nanosleep(256);
+    }
+}
 // Every thread of every CTA of the cluster: wait for the next job.  Rank 0's
 // thread 0 polls the host words; rank 0's threads then read the job's input
 // bytes from pinned host memory once (one round trip over the bus) and store
@@ -440,8 +452,13 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
         p.mt_pre ? p.mt_pre + size_t(swarm) * 312
                  : ((p.inl && p.in_mtst >= 0) ? reinterpret_cast<const unsigned long long*>(jb + p.in_mtst) + size_t(swarm) * 312
                                               : nullptr);
+    // the init walk done ahead of time (prewalk.cu), when this frame has one
+    const bool pre_cand = (p.inl && p.in_pre >= 0) ? reinterpret_cast<const PreRec*>(jb + p.in_pre)->valid != 0
+                                                   : p.pre_words != nullptr;
     if (tid >= cw) {
-        if (seeded) {                         // the host's seeded state, one warp copies it
+        if (pre_cand) {
+            // the walk arrives from HBM (seeded here only if it is late)
+        } else if (seeded) {                  // the host's seeded state, one warp copies it
             for (int i = tid - cw; i < 312; i += nthr - cw) mtbuf[312 + i] = seeded[i];
         } else if (tid == cw) {
             mt_seed_words(mtbuf + 312, seed);
@@ -470,7 +487,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
             const int wl = p.carry ? (p.inl ? reinterpret_cast<const int*>(jb + p.in_win_len) : p.win_len)[swarm] : 0;
             m->win_len = wl < p.tw ? wl : p.tw;
             m->win_head = 0;
-            if (mt_on && cw == nthr) {
+            if (mt_on && cw == nthr && !pre_cand) {
                 if (seeded) for (int i = 0; i < 312; ++i) mtbuf[312 + i] = seeded[i];
                 else mt_seed_words(mtbuf + 312, seed);
             }
@@ -529,8 +546,41 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
             const long long RD = (long long)R * D, x0 = (long long)c.row0 * D, x1 = (long long)row1 * D;
             const MtGroup grp = nthr >= 288 ? MtGroup{tid, 256, 3} : (nthr >= 160 ? MtGroup{tid, 128, 3} : MtGroup{tid, nthr, 0});
             MtState mt{mtbuf, 0, 0};
+            bool pre_ok = false;
+            const PreRec* const prr = (p.inl && p.in_pre >= 0) ? reinterpret_cast<const PreRec*>(jb + p.in_pre) : nullptr;
+            const unsigned long long* const pre_w =
+                prr ? reinterpret_cast<const unsigned long long*>(prr->words) + size_t(swarm) * size_t(2 * RD)
+                    : p.pre_words + size_t(swarm) * size_t(2 * RD);
+            if (pre_cand) {
+                if (tid == 0) {
+                    const int* const pre_f = prr ? reinterpret_cast<const int*>(prr->flag) : p.pre_flag;
+                    c.m->pre_ok = pre_wait(pre_f + swarm, prr ? prr->seq : p.pre_seq) ? 1 : 0;
+                }
+                __syncthreads();
+                pre_ok = c.m->pre_ok != 0;
+                if (!pre_ok) {              // not in time: seed and walk here after all
+                    if (seeded) for (int i = tid; i < 312; i += nthr) mtbuf[312 + i] = seeded[i];
+                    else if (tid == 0) mt_seed_words(mtbuf + 312, seed);
+                    __syncthreads();
+                }
+            }
             SEPSO_IMARK(2);
-            if (tid < grp.n) {
+            if (pre_ok) {
+                // this CTA's x / v words straight from HBM, the generator's
+                // last pair where the step draws continue
+                const int nx = int(x1 - x0);
+                for (int e = tid; e < nx; e += nthr) {
+                    const int pl = int(c.fD.div(uint32_t(e))), d = e - pl * D;
+                    const unsigned long long wx = __ldcg(pre_w + x0 + e), wv = __ldcg(pre_w + RD + x0 + e);
+                    put_x(pl, d, unit_from_word<T>(wx));
+                    put_v(pl, d, unit_from_word<T>(wv));
+                }
+                const unsigned long long* pp = (prr ? reinterpret_cast<const unsigned long long*>(prr->pair) : p.pre_pair) +
+                                               size_t(swarm) * kPrePairWords;
+                for (int i = tid; i < 624; i += nthr) mtbuf[i] = __ldcg(pp + i);
+                if (tid == 0) { c.m->mt_cur = 0; c.m->mt_blocks = (long long)__ldcg(pp + 624); }
+                SEPSO_IMARK(5);
+            } else if (tid < grp.n) {
                 mt_generate(mt, grp, x0, x1, [&](int e, unsigned long long word) {
                     const int pl = int(c.fD.div(uint32_t(e)));
                     put_x(pl, e - pl * D, unit_from_word<T>(word));
