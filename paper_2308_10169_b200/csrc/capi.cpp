@@ -254,10 +254,13 @@ int prewalk_kick(sf_ctx* ctx, long long nwords, int used) {
         W->nwords[k] = nwords;
         return SF_OK;
     }
+    uint64_t st0[312];
+    mt_seeded_state(ctx->hint_seed, st0);
     const int e = launch_init_walk(1, nullptr, nullptr, 0, 0, ctx->hint_seed, nwords,
                                    static_cast<unsigned long long*>(W->words[k].p),
                                    static_cast<unsigned long long*>(W->pairs[k].p),
-                                   static_cast<int*>(W->flags.p) + k * W->n, W->seq[k], W->st);
+                                   static_cast<int*>(W->flags.p) + k * W->n, W->seq[k],
+                                   reinterpret_cast<const unsigned long long*>(st0), W->st);
     if (e != 0) {
         W->nwords[k] = 0;
         return cuda_fail(cudaError_t(e), "init walk launch");
@@ -422,9 +425,15 @@ int resident_run(sf_ctx* ctx, const SwarmParams& fp_p, int problem, const unsign
     std::atomic_thread_fence(std::memory_order_acquire);
     static const bool trace = std::getenv("SEPSO_RESIDENT_TRACE") != nullptr;
     if (trace)
-        std::fprintf(stderr, "[resident] init %.1f us loop %.1f us rec %.1f us out %.1f us\n",
-                     1e-3 * double(R.ctl->t_init - R.ctl->t_ready), 1e-3 * double(R.ctl->t_iter - R.ctl->t_init),
+        std::fprintf(stderr, "[resident] init %.1f us (pre %.1f wait %.1f) loop %.1f us rec %.1f us out %.1f us\n",
+                     1e-3 * double(R.ctl->t_init - R.ctl->t_ready), 1e-3 * double(R.ctl->t_pre - R.ctl->t_ready),
+                     1e-3 * double(R.ctl->t_wait - R.ctl->t_pre), 1e-3 * double(R.ctl->t_iter - R.ctl->t_init),
                      1e-3 * double(R.ctl->t_loop - R.ctl->t_iter), 1e-3 * double(R.ctl->t_done - R.ctl->t_loop));
+    if (trace)
+        std::fprintf(stderr, "[resident] prelude: hyp %.2f load_world %.2f misc %.2f consts %.2f sync %.2f\n",
+                     1e-3 * double(R.ctl->t_mark[0] - R.ctl->t_ready), 1e-3 * double(R.ctl->t_mark[1] - R.ctl->t_mark[0]),
+                     1e-3 * double(R.ctl->t_mark[2] - R.ctl->t_mark[1]), 1e-3 * double(R.ctl->t_mark[3] - R.ctl->t_mark[2]),
+                     1e-3 * double(R.ctl->t_pre - R.ctl->t_mark[3]));
     if (trace)
         std::fprintf(stderr, "[resident] host wait %.1f us | device: stage %.1f us, frame %.1f us, SM %.0f MHz, iters %u\n",
                      1e6 * (now_seconds() - t0), 1e-3 * double(R.ctl->t_ready - R.ctl->t_pick),
@@ -1574,6 +1583,7 @@ struct sf_scene_batch {
     // few scenes (spare SMs): frame f + 1's init walks run while frame f plans
     // (slot (f + 1) & 1, PreWalk::seed = the frame index); replaces mtst
     PreWalk* pre = nullptr;
+    uint64_t root0 = 0;      // scene 0's root seed (one-scene walks seed on the host)
 };
 
 extern "C" {
@@ -1647,6 +1657,7 @@ int sf_scene_batch_create(sf_ctx* ctx, uint32_t n, const sf_scenario_config* cfg
     }
     std::vector<uint64_t> roots(n);
     for (uint32_t s = 0; s < n; ++s) roots[s] = cfgs[s].root_seed;
+    b->root0 = roots[0];
     std::vector<uint8_t> ones(n, 1);
     cudaMemcpyAsync(b->worlds.p, wp.bytes.data(), wp.bytes.size(), cudaMemcpyHostToDevice, ctx->stream);
     cudaMemcpyAsync(b->hyp.p, hypers, size_t(cfg->groups) * 48, cudaMemcpyHostToDevice, ctx->stream);
@@ -1728,10 +1739,14 @@ int sf_scene_batch_run(sf_scene_batch* b, uint32_t frames) {
             if (++W->next_seq <= 0) W->next_seq = 1;
             W->seq[k] = W->next_seq;
             cudaStreamWaitEvent(W->st, W->ev, 0);
+            uint64_t st0[312];          // one scene: its seeded state from the host (derive_seed, simenv.hpp:256)
+            if (b->n == 1) mt_seeded_state(splitmix64(splitmix64(b->root0 ^ p.tag_hash) + uint64_t(f + 1)), st0);
             const int e = prewalk_late() ? 0 : launch_init_walk(int(b->n), nullptr, p.roots, p.tag_hash, int(f + 1), 0, nwords,
                                            static_cast<unsigned long long*>(W->words[k].p),
                                            static_cast<unsigned long long*>(W->pairs[k].p),
-                                           static_cast<int*>(W->flags.p) + k * W->n, W->seq[k], W->st);
+                                           static_cast<int*>(W->flags.p) + k * W->n, W->seq[k],
+                                           b->n == 1 ? reinterpret_cast<const unsigned long long*>(st0) : nullptr,
+                                           W->st);
             if (e != 0) return cuda_fail(cudaError_t(e), "init walk launch");
             W->seed[k] = f + 1;
             W->nwords[k] = nwords;

@@ -352,6 +352,8 @@ int launch_fused(sf_ctx* ctx, FusedPlan& fp, int problem) {
             std::fprintf(stderr, " | init: consts=%lld seed=%lld x=%lld v=%lld rest=%lld sync=%lld (seeded at %lld, staged at %lld)",
                          r[1] - r[0], r[2] - r[1], r[3] - r[2], r[4] - r[3], r[5] - r[4], r[6] - r[5],
                          r[13] - r[0], r[14] - r[0]);
+            std::fprintf(stderr, " (thread 0: hyp %lld world_regs %lld load_world %lld to misc %lld)",
+                         r[15] - r[0], r[16] - r[15], r[17] - r[16], r[18] - r[17]);
             std::fprintf(stderr, " | ns: init=%lld loop=%lld out=%lld exit=%lld total=%lld",
                          r[8] - r[7], r[9] - r[8], r[10] - r[9], r[11] - r[10], r[11] - r[7]);
             float ev_ms = 0.f;

@@ -84,6 +84,8 @@ struct ServerCtl {
     unsigned long long t_pick, t_ready, t_done;   // %globaltimer of the last job: seen, inputs staged, published
     long long c_ready, c_done;                    // clock64 at staged / published (the SM clock over the frame)
     unsigned long long t_init, t_loop, t_iter;    // %globaltimer after the initialisation / the record / the iterations
+    unsigned long long t_pre, t_wait;             // after the constants (prelude) / the init walk's arrival
+    unsigned long long t_mark[8];                 // finer %globaltimer stamps (SEPSO_RESIDENT_TRACE)
     alignas(16) unsigned char job[4608];   // = kInlineBytes
 };
 
@@ -250,10 +252,11 @@ int launch_step_worlds(unsigned char* worlds, int n, long long stride, int off_o
                        int off_verts, int off_vel, double dt, void* stream);
 
 // prewalk.cu: n swarms' init walks (seeds[s]; derive_seed(roots[s], tag,
-// frame) when seeds is null; seed0 when both are) into words / pairs,
-// flags[s] = seq at the end.
+// frame) when seeds is null; seed0 when both are; one swarm may bring its
+// host-seeded state) into words (untempered) / pairs, flags[s] = seq at the end.
 int launch_init_walk(int n, const unsigned long long* seeds, const unsigned long long* roots,
                      unsigned long long tag_hash, int frame, unsigned long long seed0, long long nwords,
-                     unsigned long long* words, unsigned long long* pairs, int* flags, int seq, void* stream);
+                     unsigned long long* words, unsigned long long* pairs, int* flags, int seq,
+                     const unsigned long long* seeded_host, void* stream);
 
 } // namespace sepso
