@@ -172,6 +172,7 @@ struct sepso::Resident {
 
 namespace {
 constexpr unsigned long long kResidentIdleNs = 1000000ull;   // 1 ms
+thread_local double g_trace_post = 0.0, g_trace_seen = 0.0;   // SEPSO_RESIDENT_TRACE: host-side split
 
 // ------------------------------------------------ init walk ahead of time
 // (prewalk.cu).  sf_run_scenario knows the next frame's seed; while frame f
@@ -389,6 +390,7 @@ int resident_run(sf_ctx* ctx, const SwarmParams& fp_p, int problem, const unsign
         if (st) return st;
     }
     std::memcpy(R.ctl->job, h, in_bytes);
+    g_trace_post = now_seconds();
     if (++R.seq == 0) ++R.seq;
     const uint32_t s = R.seq;
     std::atomic_thread_fence(std::memory_order_release);
@@ -423,6 +425,7 @@ int resident_run(sf_ctx* ctx, const SwarmParams& fp_p, int problem, const unsign
         }
     }
     std::atomic_thread_fence(std::memory_order_acquire);
+    g_trace_seen = now_seconds();
     static const bool trace = std::getenv("SEPSO_RESIDENT_TRACE") != nullptr;
     if (trace)
         std::fprintf(stderr, "[resident] init %.1f us (pre %.1f wait %.1f) loop %.1f us rec %.1f us out %.1f us\n",
@@ -430,10 +433,10 @@ int resident_run(sf_ctx* ctx, const SwarmParams& fp_p, int problem, const unsign
                      1e-3 * double(R.ctl->t_wait - R.ctl->t_pre), 1e-3 * double(R.ctl->t_iter - R.ctl->t_init),
                      1e-3 * double(R.ctl->t_loop - R.ctl->t_iter), 1e-3 * double(R.ctl->t_done - R.ctl->t_loop));
     if (trace)
-        std::fprintf(stderr, "[resident] prelude: hyp %.2f load_world %.2f misc %.2f consts %.2f sync %.2f\n",
-                     1e-3 * double(R.ctl->t_mark[0] - R.ctl->t_ready), 1e-3 * double(R.ctl->t_mark[1] - R.ctl->t_mark[0]),
-                     1e-3 * double(R.ctl->t_mark[2] - R.ctl->t_mark[1]), 1e-3 * double(R.ctl->t_mark[3] - R.ctl->t_mark[2]),
-                     1e-3 * double(R.ctl->t_pre - R.ctl->t_mark[3]));
+        std::fprintf(stderr, "[resident] prelude cycles: hyp %lld load_world %lld misc %lld consts %lld sync %lld\n",
+                     (long long)(R.ctl->t_mark[0] - (unsigned long long)R.ctl->c_ready),
+                     (long long)(R.ctl->t_mark[1] - R.ctl->t_mark[0]), (long long)(R.ctl->t_mark[2] - R.ctl->t_mark[1]),
+                     (long long)(R.ctl->t_mark[3] - R.ctl->t_mark[2]), (long long)(R.ctl->t_mark[4] - R.ctl->t_mark[3]));
     if (trace)
         std::fprintf(stderr, "[resident] host wait %.1f us | device: stage %.1f us, frame %.1f us, SM %.0f MHz, iters %u\n",
                      1e6 * (now_seconds() - t0), 1e-3 * double(R.ctl->t_ready - R.ctl->t_pick),
@@ -778,7 +781,12 @@ int sf_plan_frame(sf_ctx* ctx, const sf_world* world, const double* prev, const 
     if (carry && (st = carry_window(window, window_len, window_cap, cfg->tw, r.trace.data(), o.iterations)))
         return st;
     if (best) std::copy(r.best.begin(), r.best.begin() + cfg->dim, best);
-    fill_record(o, now_seconds() - t0, record);
+    const double t1 = now_seconds();
+    fill_record(o, t1 - t0, record);
+    static const bool trace = std::getenv("SEPSO_RESIDENT_TRACE") != nullptr;
+    if (trace && g_trace_post > t0)
+        std::fprintf(stderr, "[plan_frame] host prep %.2f us, post->seen %.2f us, after %.2f us\n",
+                     1e6 * (g_trace_post - t0), 1e6 * (g_trace_seen - g_trace_post), 1e6 * (t1 - g_trace_seen));
     return SF_OK;
 }
 
