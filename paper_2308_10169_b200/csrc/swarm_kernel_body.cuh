@@ -478,6 +478,28 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
     // the init walk done ahead of time (prewalk.cu), when this frame has one
     const bool pre_cand = (p.inl && p.in_pre >= 0) ? reinterpret_cast<const PreRec*>(jb + p.in_pre)->valid != 0
                                                    : p.pre_words != nullptr;
+    if (pre_cand) {
+        // pull this CTA's init words, the generator pair and the flag into L2
+        // now (non-binding: the loads after the flag's acquire read L2, which
+        // the walk's stores reach), so the init below waits on L2, not DRAM
+        const PreRec* prr = (p.inl && p.in_pre >= 0) ? reinterpret_cast<const PreRec*>(jb + p.in_pre) : nullptr;
+        const size_t RD2 = 2 * size_t(c.R) * size_t(c.D);
+        const char* w = reinterpret_cast<const char*>(
+            (prr ? reinterpret_cast<const unsigned long long*>(prr->words) : p.pre_words) + size_t(swarm) * RD2);
+        const size_t xb = size_t(c.row0) * c.D * 8, nb = size_t(c.P) * c.D * 8, vb = RD2 / 2 * 8;
+        const int nl = int((nb + 127) / 128) + 1;          // + the line a misaligned start spills into
+        const char* pp = reinterpret_cast<const char*>(
+            (prr ? reinterpret_cast<const unsigned long long*>(prr->pair) : p.pre_pair) + size_t(swarm) * kPrePairWords);
+        const char* pf = reinterpret_cast<const char*>((prr ? reinterpret_cast<const int*>(prr->flag) : p.pre_flag) + swarm);
+        if (tid < nl) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(w + xb + size_t(tid) * 128));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(w + vb + xb + size_t(tid) * 128));
+        } else if (tid - nl < kPrePairWords * 8 / 128) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pp + size_t(tid - nl) * 128));
+        } else if (tid - nl == kPrePairWords * 8 / 128) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pf));
+        }
+    }
     if (tid >= cw) {
         if (pre_cand) {
             // the walk arrives from HBM (seeded here only if it is late)
