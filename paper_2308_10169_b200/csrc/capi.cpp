@@ -68,8 +68,8 @@ Io io_layout(uint32_t n, size_t world_stride, uint32_t G, uint32_t D, uint32_t c
     o.hi = take(size_t(D) * 8);
     o.win = take(size_t(n) * std::max<uint32_t>(tw, 1) * 8);
     o.win_len = take(size_t(n) * 4);
-    o.mtst = take(mt_state ? size_t(n) * 312 * 8 : 0);
     o.pre = take(mt_state ? sizeof(PreRec) : 0);
+    o.mtst = take(mt_state ? size_t(n) * 312 * 8 : 0);   // last: a job whose init walk is ready omits it
     o.out = take(size_t(n) * sizeof(SwarmOut));
     o.best = take(size_t(n) * D * 8);
     o.trace = take(size_t(n) * cap * 8);
@@ -378,18 +378,17 @@ int resident_run(sf_ctx* ctx, const SwarmParams& fp_p, int problem, const unsign
     p.srv = R.ctl;
     const bool fp64 = ctx->precision == SF_FP64;
     const uint32_t jb = uint32_t((in_bytes + 15) & ~size_t(15));
-    if (!R.launched || R.problem != problem || R.fp64 != fp64 || std::memcmp(&p, &R.p, sizeof p) != 0 ||
-        R.ctl->job_bytes != jb) {
+    if (!R.launched || R.problem != problem || R.fp64 != fp64 || std::memcmp(&p, &R.p, sizeof p) != 0) {
         resident_stop(ctx);
         std::memcpy(&R.p, &p, sizeof p);
         R.problem = problem;
         R.fp64 = fp64;
-        R.ctl->job_bytes = jb;
         R.ctl->idle_ns = kResidentIdleNs;
         const int st = resident_launch(ctx, R);
         if (st) return st;
     }
     std::memcpy(R.ctl->job, h, in_bytes);
+    R.ctl->job_bytes = jb;             // per job (the device reads it after the job's sequence number)
     g_trace_post = now_seconds();
     if (++R.seq == 0) ++R.seq;
     const uint32_t s = R.seq;
@@ -596,7 +595,10 @@ int run_batch(sf_ctx* ctx, const BatchIn& b, BatchOut& r) {
     ctx->last_d2h = io.end - io.out;
     if (b.n == 1 && path && p.inl && zc_out && resident_enabled(ctx)) {
         const unsigned char* res = nullptr;
-        st = resident_run(ctx, p, b.problem, h, io.out, io.best - io.out, io.trace - io.out, io.end - io.out, &res,
+        // the seeded state travels only when the kernel may need it (no walk ready)
+        const bool pre_ready = io.pre != io.out && reinterpret_cast<const PreRec*>(h + io.pre)->valid;
+        st = resident_run(ctx, p, b.problem, h, pre_ready ? io.mtst : io.out, io.best - io.out, io.trace - io.out,
+                          io.end - io.out, &res,
                           [&]() { return pre_on ? prewalk_kick(ctx, nwords, pre_used) : SF_OK; });
         if (st != SF_OK) return st;
         std::memcpy(r.out.data(), res, sizeof(SwarmOut));

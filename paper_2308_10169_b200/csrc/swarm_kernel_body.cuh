@@ -190,7 +190,12 @@ static __device__ uint32_t server_next_job(ServerCtl* srv, uint32_t last, uint32
             uint32_t d = 0;
             for (;;) {
                 const uint32_t s = ld_acquire_sys(&srv->job_seq);
-                if (s != last) { d = s; srv->t_pick = global_ns(); break; }
+                if (s != last) {
+                    d = s;
+                    cmd[1] = ld_acquire_sys(reinterpret_cast<const volatile uint32_t*>(&srv->job_bytes));   // per job
+                    srv->t_pick = global_ns();
+                    break;
+                }
                 if (srv->quit) break;
                 if (global_ns() - t0 > srv->idle_ns) break;
             }
@@ -198,7 +203,7 @@ static __device__ uint32_t server_next_job(ServerCtl* srv, uint32_t last, uint32
         }
         __syncthreads();
         const uint32_t d = *cmd;
-        const int nb = d ? int(srv->job_bytes) / 16 : 0;
+        const int nb = d ? int(cmd[1]) / 16 : 0;
         const uint32_t js = smem_addr(jobsm), cs = smem_addr(cmd);
         for (int i = threadIdx.x; i < nb; i += blockDim.x) {
             const uint4 v = __ldcv(reinterpret_cast<const uint4*>(srv->job) + i);
@@ -617,9 +622,9 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
                 __syncthreads();
                 pre_ok = c.m->pre_ok != 0;
                 if (srv && c.crank == 0 && tid == 0) srv->t_wait = global_ns();
-                if (!pre_ok) {              // not in time: seed and walk here after all
-                    if (seeded) for (int i = tid; i < 312; i += nthr) mtbuf[312 + i] = seeded[i];
-                    else if (tid == 0) mt_seed_words(mtbuf + 312, seed);
+                if (!pre_ok) {              // not in time: seed and walk here after all (a job
+                    // with a walk ready carries no seeded state: seed from the seed)
+                    if (tid == 0) mt_seed_words(mtbuf + 312, seed);
                     __syncthreads();
                 }
             }
