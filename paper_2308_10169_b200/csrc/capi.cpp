@@ -425,25 +425,31 @@ int resident_run(sf_ctx* ctx, const SwarmParams& fp_p, int problem, const unsign
     }
     std::atomic_thread_fence(std::memory_order_acquire);
     g_trace_seen = now_seconds();
-    static const bool trace = std::getenv("SEPSO_RESIDENT_TRACE") != nullptr;
-    if (trace)
-        std::fprintf(stderr, "[resident] init %.1f us (pre %.1f wait %.1f) loop %.1f us rec %.1f us out %.1f us\n",
-                     1e-3 * double(R.ctl->t_init - R.ctl->t_ready), 1e-3 * double(R.ctl->t_pre - R.ctl->t_ready),
-                     1e-3 * double(R.ctl->t_wait - R.ctl->t_pre), 1e-3 * double(R.ctl->t_iter - R.ctl->t_init),
-                     1e-3 * double(R.ctl->t_loop - R.ctl->t_iter), 1e-3 * double(R.ctl->t_done - R.ctl->t_loop));
-    if (trace)
-        std::fprintf(stderr, "[resident] prelude cycles: hyp %lld load_world %lld misc %lld consts %lld sync %lld\n",
-                     (long long)(R.ctl->t_mark[0] - (unsigned long long)R.ctl->c_ready),
-                     (long long)(R.ctl->t_mark[1] - R.ctl->t_mark[0]), (long long)(R.ctl->t_mark[2] - R.ctl->t_mark[1]),
-                     (long long)(R.ctl->t_mark[3] - R.ctl->t_mark[2]), (long long)(R.ctl->t_mark[4] - R.ctl->t_mark[3]));
-    if (trace)
-        std::fprintf(stderr, "[resident] host wait %.1f us | device: stage %.1f us, frame %.1f us, SM %.0f MHz, iters %u\n",
-                     1e6 * (now_seconds() - t0), 1e-3 * double(R.ctl->t_ready - R.ctl->t_pick),
-                     1e-3 * double(R.ctl->t_done - R.ctl->t_ready),
-                     1e3 * double(R.ctl->c_done - R.ctl->c_ready) / double(R.ctl->t_done - R.ctl->t_ready),
-                     reinterpret_cast<const SwarmOut*>(R.outb)->iterations);
     *results = R.outb;
     return SF_OK;
+}
+
+// SEPSO_RESIDENT_TRACE: the last frame's device split, printed by
+// sf_plan_frame after its wall time is taken
+void resident_trace_print(sf_ctx* ctx) {
+    if (!ctx->resident || !ctx->resident->ctl) return;
+    Resident& R = *ctx->resident;
+    std::fprintf(stderr, "[resident] init %.1f us (pre %.1f wait %.1f) loop %.1f us rec %.1f us out %.1f us\n",
+                 1e-3 * double(R.ctl->t_init - R.ctl->t_ready), 1e-3 * double(R.ctl->t_pre - R.ctl->t_ready),
+                 1e-3 * double(R.ctl->t_wait - R.ctl->t_pre), 1e-3 * double(R.ctl->t_iter - R.ctl->t_init),
+                 1e-3 * double(R.ctl->t_loop - R.ctl->t_iter), 1e-3 * double(R.ctl->t_done - R.ctl->t_loop));
+    std::fprintf(stderr, "[resident] prelude cycles: to-pre-check %lld to-branch %lld\n",
+                 (long long)(R.ctl->t_mark[6] - (unsigned long long)R.ctl->c_ready),
+                 (long long)(R.ctl->t_mark[5] - R.ctl->t_mark[6]));
+    std::fprintf(stderr, "[resident] prelude cycles: hyp %lld load_world %lld misc %lld consts %lld sync %lld\n",
+                 (long long)(R.ctl->t_mark[0] - (unsigned long long)R.ctl->c_ready),
+                 (long long)(R.ctl->t_mark[1] - R.ctl->t_mark[0]), (long long)(R.ctl->t_mark[2] - R.ctl->t_mark[1]),
+                 (long long)(R.ctl->t_mark[3] - R.ctl->t_mark[2]), (long long)(R.ctl->t_mark[4] - R.ctl->t_mark[3]));
+    std::fprintf(stderr, "[resident] host wait %.1f us | device: stage %.1f us, frame %.1f us, SM %.0f MHz, iters %u\n",
+                 1e6 * (g_trace_seen - g_trace_post), 1e-3 * double(R.ctl->t_ready - R.ctl->t_pick),
+                 1e-3 * double(R.ctl->t_done - R.ctl->t_ready),
+                 1e3 * double(R.ctl->c_done - R.ctl->c_ready) / double(R.ctl->t_done - R.ctl->t_ready),
+                 reinterpret_cast<const SwarmOut*>(R.outb)->iterations);
 }
 
 int run_batch(sf_ctx* ctx, const BatchIn& b, BatchOut& r) {
@@ -786,9 +792,11 @@ int sf_plan_frame(sf_ctx* ctx, const sf_world* world, const double* prev, const 
     const double t1 = now_seconds();
     fill_record(o, t1 - t0, record);
     static const bool trace = std::getenv("SEPSO_RESIDENT_TRACE") != nullptr;
-    if (trace && g_trace_post > t0)
+    if (trace && g_trace_post > t0) {
         std::fprintf(stderr, "[plan_frame] host prep %.2f us, post->seen %.2f us, after %.2f us\n",
                      1e6 * (g_trace_post - t0), 1e6 * (g_trace_seen - g_trace_post), 1e6 * (t1 - g_trace_seen));
+        resident_trace_print(ctx);
+    }
     return SF_OK;
 }
 

@@ -186,18 +186,22 @@ static __device__ uint32_t server_next_job(ServerCtl* srv, uint32_t last, uint32
                                     int crank, int C) {
     if (crank == 0) {
         if (threadIdx.x == 0) {
+            const unsigned long long idle_ns = srv->idle_ns;
             const unsigned long long t0 = global_ns();
             uint32_t d = 0;
             for (;;) {
-                const uint32_t s = ld_acquire_sys(&srv->job_seq);
+                // job_seq and quit share one 8-byte word: one bus round trip per poll
+                unsigned long long jq;
+                asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(jq) : "l"(&srv->job_seq) : "memory");
+                const uint32_t s = uint32_t(jq);
                 if (s != last) {
                     d = s;
                     cmd[1] = ld_acquire_sys(reinterpret_cast<const volatile uint32_t*>(&srv->job_bytes));   // per job
                     srv->t_pick = global_ns();
                     break;
                 }
-                if (srv->quit) break;
-                if (global_ns() - t0 > srv->idle_ns) break;
+                if (uint32_t(jq >> 32)) break;                 // quit
+                if (global_ns() - t0 > idle_ns) break;
             }
             *cmd = d;
         }
@@ -481,6 +485,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
                  : ((p.inl && p.in_mtst >= 0) ? reinterpret_cast<const unsigned long long*>(jb + p.in_mtst) + size_t(swarm) * 312
                                               : nullptr);
     // the init walk done ahead of time (prewalk.cu), when this frame has one
+    SEPSO_SMARK(6);
     const bool pre_cand = (p.inl && p.in_pre >= 0) ? reinterpret_cast<const PreRec*>(jb + p.in_pre)->valid != 0
                                                    : p.pre_words != nullptr;
     if (pre_cand) {
@@ -517,6 +522,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
             p.prof[p.cap * kProfPhases + 13] = clock64();
         if (PATH) world_regs(c, wrec);
     } else {
+        SEPSO_SMARK(5);
         const double* hyp_src = (p.inl ? reinterpret_cast<const double*>(jb + p.in_hyp) : p.hypers) +
                                 size_t(swarm) * size_t(p.hypers_stride);
         for (int i = tid; i < G * 6; i += cw) c.hyp[i] = T(hyp_src[i]);
