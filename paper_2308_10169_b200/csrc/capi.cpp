@@ -455,7 +455,7 @@ void resident_trace_print(sf_ctx* ctx) {
 int run_batch(sf_ctx* ctx, const BatchIn& b, BatchOut& r) {
     DeviceGuard guard(ctx->device);
     const bool path = b.problem == kPath;
-    WorldPack wp;
+    static thread_local WorldPack wp;          // reused: no allocation per frame
     if (path) pack_worlds(b.worlds, b.n, wp);
     const int max_obs = path ? wp.lay.max_obs : 0, max_verts = path ? wp.lay.max_verts : 0;
     FusedPlan fp = plan_fused(ctx, b.problem, int(b.n), int(b.G), int(b.N), int(b.D), max_obs,
@@ -571,10 +571,11 @@ int run_batch(sf_ctx* ctx, const BatchIn& b, BatchOut& r) {
     const long long nwords = 2ll * b.G * b.N * b.D;
     int pre_used = -1;
     bool pre_on = false;
-    if (io.out <= size_t(kInlineBytes) && std::getenv("SEPSO_NO_INLINE") == nullptr) {
-        if (io.mtst != io.out)
-            for (uint32_t sw = 0; sw < b.n; ++sw)
-                mt_seeded_state(b.seeds[sw], reinterpret_cast<uint64_t*>(h + io.mtst) + size_t(sw) * 312);
+    static const bool no_inline = std::getenv("SEPSO_NO_INLINE") != nullptr;
+    // the resident planner takes the job from the pinned block; a launch needs the parameter block
+    const bool resident = b.n == 1 && path && zc_out && io.out <= size_t(kInlineBytes) && !no_inline &&
+                          resident_enabled(ctx);
+    if (io.out <= size_t(kInlineBytes) && !no_inline) {
         if (io.pre != io.out) {
             PreRec* pr = reinterpret_cast<PreRec*>(h + io.pre);
             pr->valid = 0;
@@ -585,7 +586,11 @@ int run_batch(sf_ctx* ctx, const BatchIn& b, BatchOut& r) {
             }
             p.in_pre = int(io.pre);
         }
-        std::memcpy(payload.bytes, h, io.out);
+        // the seeded states, unless the walk is ready (the kernel then needs none)
+        if (io.mtst != io.out && !(io.pre != io.out && reinterpret_cast<const PreRec*>(h + io.pre)->valid))
+            for (uint32_t sw = 0; sw < b.n; ++sw)
+                mt_seeded_state(b.seeds[sw], reinterpret_cast<uint64_t*>(h + io.mtst) + size_t(sw) * 312);
+        if (!resident) std::memcpy(payload.bytes, h, io.out);
         p.inl = 1;
         p.in_seed = int(io.seed); p.in_world = int(io.world); p.in_hyp = int(io.hyp);
         p.in_prev = int(io.prev); p.in_has_prev = int(io.has_prev); p.in_lo = int(io.lo);
@@ -599,7 +604,7 @@ int run_batch(sf_ctx* ctx, const BatchIn& b, BatchOut& r) {
     if (ce != cudaSuccess) return cuda_fail(ce, "H2D io");
     ctx->last_h2d = io.out;
     ctx->last_d2h = io.end - io.out;
-    if (b.n == 1 && path && p.inl && zc_out && resident_enabled(ctx)) {
+    if (resident) {
         const unsigned char* res = nullptr;
         // the seeded state travels only when the kernel may need it (no walk ready)
         const bool pre_ready = io.pre != io.out && reinterpret_cast<const PreRec*>(h + io.pre)->valid;
@@ -769,7 +774,7 @@ int sf_plan_frame(sf_ctx* ctx, const sf_world* world, const double* prev, const 
     const uint8_t hp = prev ? 1 : 0;
     b.prev = prev;
     b.has_prev = &hp;
-    std::vector<double> wtail;
+    static thread_local std::vector<double> wtail;
     uint32_t wl = 0;
     if (carry) {
         const uint32_t keep = std::min(*window_len, cfg->tw);
@@ -779,7 +784,7 @@ int sf_plan_frame(sf_ctx* ctx, const sf_world* world, const double* prev, const 
         b.win_vals = wtail.data();
         b.win_lens = &wl;
     }
-    BatchOut r;
+    static thread_local BatchOut r;             // reused: no allocation per frame
     if ((st = run_batch(ctx, b, r))) return st;
     const SwarmOut& o = r.out[0];
     if (o.status == 2) {

@@ -173,8 +173,11 @@ void pack_worlds(const sf_world* worlds, uint32_t n, WorldPack& out) {
 }
 
 bool force_staged() {
-    const char* e = std::getenv("SEPSO_FORCE_STAGED");
-    return e && e[0] == '1';
+    static const bool on = [] {
+        const char* e = std::getenv("SEPSO_FORCE_STAGED");
+        return e && e[0] == '1';
+    }();
+    return on;
 }
 
 static int env_int(const char* name, int def) {
@@ -199,8 +202,10 @@ FusedPlan plan_fused(sf_ctx* ctx, int problem, int n_swarms, int G, int N, int D
     p.tw = tw;
     p.max_obs = path ? std::max(max_obs, 1) : 0;
     p.max_verts = path ? std::max(max_verts, 3) : 0;
-    const int want_c = ctx->force_cluster ? ctx->force_cluster : env_int("SEPSO_CLUSTER", 0);
-    const int want_t = ctx->force_threads ? ctx->force_threads : env_int("SEPSO_THREADS", 0);
+    static const int env_c = env_int("SEPSO_CLUSTER", 0), env_t = env_int("SEPSO_THREADS", 0);
+    static const int env_no_ring = env_int("SEPSO_NO_RING", 0);
+    const int want_c = ctx->force_cluster ? ctx->force_cluster : env_c;
+    const int want_t = ctx->force_threads ? ctx->force_threads : env_t;
     // Launch shapes (measured, tools/sweep*.py):
     //  latency (few swarms): one swarm over up to 16 SMs, ~85 rows per CTA;
     //  medium (up to one swarm per SM, e.g. HSEF's 80 inner swarms): ~340 rows per
@@ -225,7 +230,7 @@ FusedPlan plan_fused(sf_ctx* ctx, int problem, int n_swarms, int G, int N, int D
             // worst case Rc*S*O entries; beyond the capacity entries are evaluated in place
             // throughput launches: per-warp rings of 64 compacted (item, obstacle)
             // pairs in A1 (latency launches keep one item per thread in place)
-            p.entry_cap = (!latency && env_int("SEPSO_NO_RING", 0) == 0) ? 1024 / 32 * 64 : 0;
+            p.entry_cap = (!latency && env_no_ring == 0) ? 1024 / 32 * 64 : 0;
             // one thread per (particle, segment) item; latency launches add four
             // warps (containment tasks, the stream generator) -- measured best
             p.nthreads = std::min(medium ? 512 : 1024, std::max(128, ((Rc * S) + 31) / 32 * 32 + (latency ? 128 : 0)));
