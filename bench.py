@@ -47,7 +47,7 @@ WORKLOAD_C2 = ("config2: paper dynamic scene (366 cm, 6 dynamic + 2 static obsta
                "+ PI + AT, G=8 N=170 D=16, cap 30, window carryover, root seed 3 (+rank); frames W..W+K-1, "
                "one frame per step")
 PROFILE_CSV = "profiles/r02_bench_launches.csv"        # ncu launch list of this bench (roofline.traffic)
-LATENCY_KERNEL = "swarm_kernel<float, 1, 0, 896, 0>"
+LATENCY_KERNEL = "swarm_kernel<float, 1, 0, 896, 0, 1>"
 
 
 def parse():
