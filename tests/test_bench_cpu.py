@@ -29,6 +29,6 @@ def test_reference_arm_json_line():
 def test_committed_launch_list_traffic():
     sys.path.insert(0, ROOT)
     import bench
-    t = bench.committed_dram_bytes("swarm_kernel<float, 1, 0, 896, 0>", "(16, 1, 1)")
+    t = bench.committed_dram_bytes(bench.LATENCY_KERNEL, "(16, 1, 1)")
     assert t is not None and 1e4 < t < 1e7             # bytes per config-2 launch
     assert bench.committed_dram_bytes("no_such_kernel", "(1, 1, 1)") is None
