@@ -7,7 +7,7 @@ import torch
 import paper_2308_10169_b200 as pe
 eng = pe.Engine(0, "fp32")
 planner = pe.PlannerConfig(max_iters_per_frame=30, window_carryover=True)
-stream = torch.cuda.Stream()
+stream = torch.cuda.ExternalStream(eng.stream, device=torch.device('cuda', 0))
 best = []
 for rep in range(3):
     sb = pe.SceneBatch(eng, [pe.ScenarioConfig(root_seed=s) for s in range(1024)], planner, pe.EVOLVED_PATH_HYPERS, 4)
