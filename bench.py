@@ -431,8 +431,9 @@ def main():
     e2e_s = dist.max(float(sum(r.wall_seconds for r in recs_e2e[W:])))
     e2e = {"value": K * ws / e2e_s, "unit": "plans/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
            "timing": "sum of PlanRecord.wall_seconds (host steady_clock around each sf_plan_frame call: validate + "
-                     "stage + H2D (inputs in the launch parameter block) + kernel (results stored into pinned host "
-                     "memory) + sync), frames W..W+K-1",
+                     "stage the inputs into pinned host memory + the resident cluster reads them over the bus, plans, "
+                     "stores the results into pinned host memory and publishes them + the host reads them; the "
+                     "next frame's init walk is launched inside the call, DESIGN.md section 1), frames W..W+K-1",
            "mean_iterations_per_frame": float(np.mean([r.iterations for r in recs_e2e[W:]]))}
 
     extras = {}

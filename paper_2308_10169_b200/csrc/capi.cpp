@@ -608,6 +608,7 @@ int run_batch(sf_ctx* ctx, const BatchIn& b, BatchOut& r) {
         const unsigned char* res = nullptr;
         // the seeded state travels only when the kernel may need it (no walk ready)
         const bool pre_ready = io.pre != io.out && reinterpret_cast<const PreRec*>(h + io.pre)->valid;
+        ctx->last_h2d = pre_ready ? io.mtst : io.out;      // the bytes the cluster reads over the bus
         st = resident_run(ctx, p, b.problem, h, pre_ready ? io.mtst : io.out, io.best - io.out, io.trace - io.out,
                           io.end - io.out, &res,
                           [&]() { return pre_on ? prewalk_kick(ctx, nwords, pre_used) : SF_OK; });
