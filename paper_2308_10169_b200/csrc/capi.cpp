@@ -161,8 +161,9 @@ struct BatchOut {
 // longer), on a shape change, and when the context is destroyed.
 struct sepso::Resident {
     ServerCtl* ctl = nullptr;          // pinned, device-mapped
-    unsigned char* outb = nullptr;     // pinned output block (record, best, trace, window)
+    unsigned char* outb = nullptr;     // pinned output block: the record as tagged chunks
     size_t outb_n = 0;
+    std::vector<unsigned char> dec;    // the record decoded (SwarmOut, best, trace)
     cudaStream_t stream = nullptr;
     SwarmParams p{};
     int problem = 0;
@@ -356,7 +357,8 @@ int resident_run(sf_ctx* ctx, const SwarmParams& fp_p, int problem, const unsign
     }
     Resident& R = *Rp;
     const size_t tw = size_t(std::max(fp_p.tw, 1));
-    const size_t need = ((out_bytes + 15) & ~size_t(15)) + tw * 8 + 16;
+    const size_t nchunk = 4 + size_t(fp_p.D) + size_t(std::max(fp_p.cap, 1));   // tagged result chunks
+    const size_t need = std::max(((out_bytes + 15) & ~size_t(15)) + tw * 8 + 16, nchunk * 16);
     if (need > R.outb_n) {
         resident_stop(ctx);
         if (R.outb) cudaFreeHost(R.outb);
@@ -365,6 +367,8 @@ int resident_run(sf_ctx* ctx, const SwarmParams& fp_p, int problem, const unsign
         const cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&R.outb), std::max<size_t>(need, 4096));
         if (e != cudaSuccess) return cuda_fail(e, "resident output block");
         R.outb_n = std::max<size_t>(need, 4096);
+        std::memset(R.outb, 0, R.outb_n);      // no stale chunk tags
+        R.dec.assign(R.outb_n, 0);
     }
     SwarmParams p;
     std::memcpy(&p, &fp_p, sizeof p);
@@ -400,13 +404,24 @@ int resident_run(sf_ctx* ctx, const SwarmParams& fp_p, int problem, const unsign
         const int st = after_post();
         if (st) return st;
     }
+    // the record arrives as tagged chunks (swarm_kernel_body.cuh put_chunk):
+    // complete when the header and every chunk it implies carry this job's number
+    auto tag = [&](size_t i) { return reinterpret_cast<const volatile uint32_t*>(R.outb)[4 * i + 3]; };
+    auto complete = [&]() {
+        if (tag(0) != s) return false;
+        const uint32_t its = reinterpret_cast<const volatile uint32_t*>(R.outb)[0];
+        const size_t n = 4 + size_t(fp_p.D) + std::min<size_t>(its, size_t(std::max(fp_p.cap, 1)));
+        for (size_t i = 1; i < n; ++i)
+            if (tag(i) != s) return false;
+        return true;
+    };
     for (uint64_t spin = 1;; ++spin) {
-        if (R.ctl->done_seq == s) break;
+        if (complete()) break;
         if (R.ctl->alive == 0) {          // the cluster exited (idle) before taking this job: relaunch it
             const cudaError_t e = cudaStreamSynchronize(R.stream);
             R.launched = false;
             if (e != cudaSuccess) return cuda_fail(e, "resident planner");
-            if (R.ctl->done_seq == s) break;
+            if (complete()) break;
             const int st = resident_launch(ctx, R);
             if (st) return st;
             continue;
@@ -425,7 +440,29 @@ int resident_run(sf_ctx* ctx, const SwarmParams& fp_p, int problem, const unsign
     }
     std::atomic_thread_fence(std::memory_order_acquire);
     g_trace_seen = now_seconds();
-    *results = R.outb;
+    // decode the chunks into the launch path's layout (SwarmOut, best, trace)
+    {
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(R.outb);
+        auto dbl = [&](size_t i) {
+            const uint64_t u = uint64_t(w[4 * i]) | (uint64_t(w[4 * i + 1]) << 32);
+            double v;
+            std::memcpy(&v, &u, 8);
+            return v;
+        };
+        SwarmOut o{};
+        o.iterations = w[0]; o.q = w[1]; o.status = w[2];
+        o.fitness = dbl(1); o.truncated = w[6];
+        o.length = dbl(2); o.window_len = w[10];
+        o.bad_g = w[12]; o.bad_n = w[13]; o.bad_k = w[14];
+        unsigned char* dst = R.dec.data();
+        std::memcpy(dst, &o, sizeof o);
+        double* best = reinterpret_cast<double*>(dst + out_off_best);
+        for (int d = 0; d < fp_p.D; ++d) best[d] = dbl(4 + size_t(d));
+        double* tr = reinterpret_cast<double*>(dst + out_off_trace);
+        const size_t n = std::min<size_t>(o.iterations, size_t(std::max(fp_p.cap, 1)));
+        for (size_t k = 0; k < n; ++k) tr[k] = dbl(4 + size_t(fp_p.D) + k);
+    }
+    *results = R.dec.data();
     return SF_OK;
 }
 
@@ -438,6 +475,9 @@ void resident_trace_print(sf_ctx* ctx) {
                  1e-3 * double(R.ctl->t_init - R.ctl->t_ready), 1e-3 * double(R.ctl->t_pre - R.ctl->t_ready),
                  1e-3 * double(R.ctl->t_wait - R.ctl->t_pre), 1e-3 * double(R.ctl->t_iter - R.ctl->t_init),
                  1e-3 * double(R.ctl->t_loop - R.ctl->t_iter), 1e-3 * double(R.ctl->t_done - R.ctl->t_loop));
+    std::fprintf(stderr, "[resident] record cycles: path_length64 %lld rest %lld\n",
+                 (long long)(R.ctl->t_mark[7] - R.ctl->t_mark[8]),
+                 (long long)((unsigned long long)R.ctl->c_done - R.ctl->t_mark[7]));
     std::fprintf(stderr, "[resident] prelude cycles: to-pre-check %lld to-branch %lld\n",
                  (long long)(R.ctl->t_mark[6] - (unsigned long long)R.ctl->c_ready),
                  (long long)(R.ctl->t_mark[5] - R.ctl->t_mark[6]));

@@ -85,7 +85,7 @@ struct ServerCtl {
     long long c_ready, c_done;                    // clock64 at staged / published (the SM clock over the frame)
     unsigned long long t_init, t_loop, t_iter;    // %globaltimer after the initialisation / the record / the iterations
     unsigned long long t_pre, t_wait;             // after the constants (prelude) / the init walk's arrival
-    unsigned long long t_mark[8];                 // finer %globaltimer stamps (SEPSO_RESIDENT_TRACE)
+    unsigned long long t_mark[16];                 // finer %globaltimer stamps (SEPSO_RESIDENT_TRACE)
     alignas(16) unsigned char job[4608];   // = kInlineBytes
 };
 

@@ -160,6 +160,20 @@ __device__ __forceinline__ unsigned long long global_ns() {
     return t;
 }
 
+// Resident planner results: 16-byte chunks {3 payload words, job number}, each
+// one store (one bus write), so the host knows a chunk is this job's from its
+// own tag -- no system fence between the record and the host seeing it.
+// Layout: [0] {iterations, q, status}  [1] {fitness, truncated}  [2] {length,
+// window_len}  [3] {bad_g, bad_n, bad_k}  [4 + d] best_x[d]  [4 + D + k] trace[k].
+__device__ __forceinline__ void put_chunk(void* base, int i, uint32_t a, uint32_t b, uint32_t c, uint32_t tag) {
+    asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};"
+                 ::"l"(reinterpret_cast<uint4*>(base) + i), "r"(a), "r"(b), "r"(c), "r"(tag) : "memory");
+}
+__device__ __forceinline__ void put_chunk_d(void* base, int i, double v, uint32_t c, uint32_t tag) {
+    const unsigned long long u = __double_as_longlong(v);
+    put_chunk(base, i, uint32_t(u), uint32_t(u >> 32), c, tag);
+}
+
 // v, as a value the compiler cannot treat as loop invariant
 __device__ __forceinline__ int opaque_int(int v) {
     asm volatile("mov.b32 %0, %0;" : "+r"(v));
@@ -894,7 +908,10 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
                 const int tw = p.tw;
                 if (lane == 0) {
                     m->tsrc_slot = tnew ? tg : -1;
-                    if (c.crank == 0) p.trace[size_t(swarm) * p.cap + (k - 1)] = tb;
+                    if (c.crank == 0) {
+                        if (srv) put_chunk_d(p.out, 4 + D + (k - 1), tb, 0u, jseq);
+                        else p.trace[size_t(swarm) * p.cap + (k - 1)] = tb;
+                    }
                 }
                 if (tw > 0) {
                     int at = r_wh + r_wl;
@@ -988,7 +1005,10 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
                 if (lane == 0) {
                     if (tnew) { m->tbf = tv; m->tbq = tbq; m->tsrc_slot = tg; }
                     else m->tsrc_slot = -1;
-                    if (c.crank == 0) p.trace[size_t(swarm) * p.cap + (k - 1)] = tb;
+                    if (c.crank == 0) {
+                        if (srv) put_chunk_d(p.out, 4 + D + (k - 1), tb, 0u, jseq);
+                        else p.trace[size_t(swarm) * p.cap + (k - 1)] = tb;
+                    }
                     if (p.tw > 0) {
                         int at = wh0 + wl0;                       // slot of the new value
                         if (wl0 == p.tw) at = wh0;
@@ -1193,7 +1213,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
                                     nthr - 32);
         if (hits) atomicAdd(&c.m->q64, hits);
     }
-    if (srv && c.crank == 0 && tid == 0) srv->t_loop = global_ns();
+    if (srv && c.crank == 0 && tid == 0) { srv->t_loop = global_ns(); srv->t_mark[8] = (unsigned long long)clock64(); }
     // record length = path_length(best) in FP64 (planner.hpp:194): warp 0 of
     // rank 0 computes the S segment hypots in parallel, summed in path order
     double path_len = 0.0;
@@ -1203,6 +1223,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
         path_len = path_length64(c.tbx, c.W, c.S, e64 ? e64[0] : double(c.sx), e64 ? e64[1] : double(c.sy),
                                  e64 ? e64[2] : double(c.tx), e64 ? e64[3] : double(c.ty), lane);
     }
+    SEPSO_SMARK(7);
     if (rec64) __syncthreads();
     if (c.crank == 0 && tid == 0) {
         const Misc<T>* m = c.m;
@@ -1224,14 +1245,25 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
             o.q = uint32_t(m->tbq);
             if (PATH) o.length = path_len;
         }
-        p.out[swarm] = o;
+        if (srv) {
+            put_chunk(p.out, 0, o.iterations, o.q, o.status, jseq);
+            put_chunk_d(p.out, 1, o.fitness, o.truncated, jseq);
+            put_chunk_d(p.out, 2, o.length, o.window_len, jseq);
+            put_chunk(p.out, 3, o.bad_g, o.bad_n, o.bad_k, jseq);
+        } else {
+            p.out[swarm] = o;
+        }
     }
     if (c.crank == 0) {
-        for (int d = tid; d < D; d += nthr) p.best_x[size_t(swarm) * D + d] = double(c.tbx[d]);
-        if (p.carry)
+        if (srv)
+            for (int d = tid; d < D; d += nthr) put_chunk_d(p.out, 4 + d, double(c.tbx[d]), 0u, jseq);
+        else
+            for (int d = tid; d < D; d += nthr) p.best_x[size_t(swarm) * D + d] = double(c.tbx[d]);
+        if (p.carry && !srv) {      // (the resident planner's host keeps the window from the trace)
             for (int i = tid; i < c.m->win_len; i += nthr)
                 p.win_vals[size_t(swarm) * p.tw + i] = c.win[(c.m->win_head + i) % p.tw];
-        if (tid == 0 && p.carry) p.win_len[swarm] = c.m->win_len;
+            if (tid == 0) p.win_len[swarm] = c.m->win_len;
+        }
     }
     // scene batches: advance this swarm's world record for the next frame
     // (simenv.hpp:155-184); every CTA staged it long ago.  Rank 1 does it
