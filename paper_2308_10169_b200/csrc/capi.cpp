@@ -279,6 +279,8 @@ void prewalk_destroy(PreWalk*& W) {
         cudaStreamDestroy(W->st);
     }
     if (W->ev) cudaEventDestroy(W->ev);
+    for (cudaEvent_t e : W->done)
+        if (e) cudaEventDestroy(e);
     for (int k = 0; k < 2; ++k) {
         W->words[k].release();
         W->pairs[k].release();
@@ -1705,7 +1707,15 @@ int sf_scene_batch_create(sf_ctx* ctx, uint32_t n, const sf_scenario_config* cfg
     // few scenes leave most SMs idle: there the next frame's init walks run
     // ahead (one CTA per scene) while a frame plans
     const long long nwords = 2ll * cfg->groups * cfg->per_group * D;
-    const bool ahead = ctx->rng == SF_RNG_MT19937 && prewalk_enabled() && n * uint32_t(b->fp.p.C) <= 64 && n <= 8;
+    const bool few = n * uint32_t(b->fp.p.C) <= 64 && n <= 8;
+    // many scenes (config 5) fill every SM: their walks run as one bulk
+    // launch (several walker CTAs per SM) ordered before the frame by an event,
+    // in the previous frame's tail instead of inside every cluster
+    static const bool bulk_on = [] {
+        const char* e = std::getenv("SEPSO_PREWALK_BULK");
+        return !(e && e[0] == '0');
+    }();
+    const bool ahead = ctx->rng == SF_RNG_MT19937 && prewalk_enabled() && (few || bulk_on);
     if (ctx->rng == SF_RNG_MT19937 && !ahead) {
         alloc(b->mtst[0], size_t(n) * 312 * 8);
         alloc(b->mtst[1], size_t(n) * 312 * 8);
@@ -1718,6 +1728,15 @@ int sf_scene_batch_create(sf_ctx* ctx, uint32_t n, const sf_scenario_config* cfg
         prewalk_destroy(b->pre);
         delete b;
         return st;
+    }
+    if (ahead && !few) {
+        b->pre->bulk = true;
+        for (cudaEvent_t& ev : b->pre->done)
+            if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+                prewalk_destroy(b->pre);
+                delete b;
+                return cuda_fail(cudaErrorMemoryAllocation, "init walk events");
+            }
     }
     std::vector<uint64_t> roots(n);
     for (uint32_t s = 0; s < n; ++s) roots[s] = cfgs[s].root_seed;
@@ -1791,6 +1810,7 @@ int sf_scene_batch_run(sf_scene_batch* b, uint32_t frames) {
                 p.pre_flag = static_cast<const int*>(W->flags.p) + k * W->n;
                 p.pre_seq = W->seq[k];
                 W->nwords[k] = 0;
+                if (W->bulk) cudaStreamWaitEvent(ctx->stream, W->done[k], 0);   // no spinning clusters
             }
             // frame f - 1 (the last reader of slot (f + 1) & 1) is done once
             // this point of the planning stream is reached
@@ -1812,6 +1832,7 @@ int sf_scene_batch_run(sf_scene_batch* b, uint32_t frames) {
                                            b->n == 1 ? reinterpret_cast<const unsigned long long*>(st0) : nullptr,
                                            W->st);
             if (e != 0) return cuda_fail(cudaError_t(e), "init walk launch");
+            if (W->bulk) cudaEventRecord(W->done[k], W->st);
             W->seed[k] = f + 1;
             W->nwords[k] = nwords;
         }

@@ -46,6 +46,8 @@ struct PreWalk {
     DevBuf words[2], pairs[2], flags;
     cudaStream_t st = nullptr;
     cudaEvent_t ev = nullptr;
+    cudaEvent_t done[2] = {nullptr, nullptr};   // bulk mode: slot k's walks complete (stream order, no spin)
+    bool bulk = false;
     uint64_t seed[2] = {0, 0};     // single-swarm slots: the seed walked
     long long nwords[2] = {0, 0};  // 2RD of the walk in the slot (0: empty)
     int seq[2] = {0, 0};

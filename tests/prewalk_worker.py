@@ -24,5 +24,13 @@ for prec in ("fp32", "fp64"):
         sb.close()
         out["batch"] = [[r.fitness, r.length, r.iterations, r.truncated, r.intersections] for r in rb] + \
                        [np.asarray(best, dtype=np.float64).ravel().tolist()]
+        # more than 8 scenes: the bulk walk (one launch for every scene, event-ordered)
+        sb = pe.SceneBatch(eng, [pe.ScenarioConfig(root_seed=20 + i) for i in range(12)], PLANNER,
+                           pe.EVOLVED_PATH_HYPERS, 4)
+        sb.run(4)
+        rb, best = sb.records(0, 4, with_best=True)
+        sb.close()
+        out["bulk"] = [[r.fitness, r.length, r.iterations, r.truncated, r.intersections] for r in rb] + \
+                      [np.asarray(best, dtype=np.float64).ravel().tolist()]
     eng.close()
 print(json.dumps(out))

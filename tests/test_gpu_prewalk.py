@@ -3,8 +3,10 @@ and scene batches read frame f+1's init words, walked on a spare SM while
 frame f planned, instead of walking them in the planning kernel.  The
 results must be bit-identical to walking in the kernel (SEPSO_PREWALK=0),
 and to the kernel's fallback when the announced walk never arrives
-(SEPSO_PREWALK_TEST=late: the kernel waits ~2 ms, then walks itself).  The
-FP64 reference parity of both paths is pinned in test_gpu_scene.py."""
+(SEPSO_PREWALK_TEST=late: the kernel waits ~2 ms, then walks itself).  Batches
+of more than 8 scenes take the bulk walk (one launch for every scene,
+ordered before the frame by an event).  The FP64 reference parity of the
+paths is pinned in test_gpu_scene.py."""
 import json
 import os
 import subprocess
@@ -29,6 +31,6 @@ def test_prewalk_equals_in_kernel_walk_and_fallback():
     ahead = _run(SEPSO_PREWALK="1")
     inkernel = _run(SEPSO_PREWALK="0")
     late = _run(SEPSO_PREWALK="1", SEPSO_PREWALK_TEST="late")
-    for key in ("fp32", "fp64", "batch"):
+    for key in ("fp32", "fp64", "batch", "bulk"):
         assert ahead[key] == inkernel[key], key
         assert late[key] == inkernel[key], key
