@@ -487,16 +487,41 @@ __global__ void __launch_bounds__(kWideThreads, 1) k_eval_path_wide(const unsign
         if (lane == 0) c.seglen[it] = seg_length<T>(Ar<T>::sub(a2x, a1x), Ar<T>::sub(a2y, a1y));
         const T lx = a1x < a2x ? a1x : a2x, hx = a1x < a2x ? a2x : a1x;
         const T ly = a1y < a2y ? a1y : a2y, hy = a1y < a2y ? a2y : a1y;
-        const int cx0 = cell_of(lx - extw), cx1 = cell_of(hx + c.margin);
         const int cy0 = cell_of(ly - exth), cy1 = cell_of(hy + c.margin);
         int cnt = 0, head = 0, pend = 0;
         // the cell rows' candidate ranges form one stream: lane r holds row r's
-        // start in gidx and its offset in the stream; 32 candidates per batch
+        // start in gidx and its offset in the stream; 32 candidates per batch.
+        // Row r's range is swept, not the whole box: an obstacle with an edge
+        // crossing the segment contains the crossing point P in its box, so its
+        // filed (lower) corner lies in P - [0, ext]; for the row's band of
+        // corners only the part of the segment at y in [band low, band high +
+        // ext_y] matters, and the columns follow from that part's x range.
+        // Obstacles the box test alone would pass (box overlaps the segment's
+        // box, no edge crosses) contribute no crossing either way, so Q is the
+        // same; bands and ranges are widened by a rounding guard.
         const int nrows = cy1 - cy0 + 1;                       // <= kGridDim = 32
         int rbeg = 0, rlen = 0;
         if (lane < nrows) {
-            rbeg = gstart[(cy0 + lane) * kGridDim + cx0];
-            rlen = gstart[(cy0 + lane) * kGridDim + cx1 + 1] - rbeg;
+            const int cy = cy0 + lane;
+            const T cs = T(1) / inv_cs, guard = cs * T(1e-3) + c.margin;
+            const T ya = cy == 0 ? -T(1e30) : T(cy) * cs - guard;
+            const T yb = cy == kGridDim - 1 ? T(1e30) : T(cy + 1) * cs + exth + guard;
+            const T dy = Ar<T>::sub(a2y, a1y), dx = Ar<T>::sub(a2x, a1x);
+            T px0 = lx, px1 = hx;
+            bool any = hy >= ya && ly <= yb;
+            if (any && (ly < ya || hy > yb) && dy != T(0)) {        // clip the segment to the slab
+                const T ta = (ya - a1y) / dy, tb = (yb - a1y) / dy;
+                const T t0 = fmax(T(0), fmin(ta, tb)), t1 = fmin(T(1), fmax(ta, tb));
+                const T xa = a1x + t0 * dx, xb = a1x + t1 * dx;
+                const T gx = guard + T(1e-4) * (hx - lx);
+                px0 = fmax(lx, fmin(xa, xb) - gx);
+                px1 = fmin(hx, fmax(xa, xb) + gx);
+            }
+            if (any) {
+                const int cx0 = cell_of(px0 - extw), cx1 = cell_of(px1 + c.margin);
+                rbeg = gstart[cy * kGridDim + cx0];
+                rlen = gstart[cy * kGridDim + cx1 + 1] - rbeg;
+            }
         }
         int rinc = rlen;
         for (int off = 1; off < 32; off <<= 1) {
