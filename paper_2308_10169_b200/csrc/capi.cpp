@@ -412,7 +412,10 @@ int resident_run(sf_ctx* ctx, const SwarmParams& fp_p, int problem, const unsign
     auto complete = [&]() {
         if (tag(0) != s) return false;
         const uint32_t its = reinterpret_cast<const volatile uint32_t*>(R.outb)[0];
-        const size_t n = 4 + size_t(fp_p.D) + std::min<size_t>(its, size_t(std::max(fp_p.cap, 1)));
+        const uint32_t status = reinterpret_cast<const volatile uint32_t*>(R.outb)[2];
+        // a failed frame (non-finite fitness) stops before its iteration's
+        // trace entry; its record needs none
+        const size_t n = 4 + size_t(fp_p.D) + (status == 0 ? std::min<size_t>(its, size_t(std::max(fp_p.cap, 1))) : 0);
         for (size_t i = 1; i < n; ++i)
             if (tag(i) != s) return false;
         return true;
@@ -461,7 +464,7 @@ int resident_run(sf_ctx* ctx, const SwarmParams& fp_p, int problem, const unsign
         double* best = reinterpret_cast<double*>(dst + out_off_best);
         for (int d = 0; d < fp_p.D; ++d) best[d] = dbl(4 + size_t(d));
         double* tr = reinterpret_cast<double*>(dst + out_off_trace);
-        const size_t n = std::min<size_t>(o.iterations, size_t(std::max(fp_p.cap, 1)));
+        const size_t n = o.status == 0 ? std::min<size_t>(o.iterations, size_t(std::max(fp_p.cap, 1))) : 0;
         for (size_t k = 0; k < n; ++k) tr[k] = dbl(4 + size_t(fp_p.D) + k);
     }
     *results = R.dec.data();
