@@ -431,13 +431,17 @@ __device__ void load_world(Ctx<T>& c, const unsigned char* wrec, int off_offsets
     // FP32 engine: the world is the FP32-rounded world; the cull margin is
     // conservative (never drops a pair the reference's 1e-9 cull keeps).
     c.margin = sizeof(T) == 8 ? T(1e-9) : T(1e-6) * (T(1) + (width > height ? width : height));
+    #pragma unroll 1
     for (int d = tid; d < c.D; d += nthr) {
         c.lo[d] = T(0);
         c.hi[d] = d < c.W ? width : height;                  // geometry.hpp:252-255
     }
+    #pragma unroll 1
     for (int i = tid; i <= c.O; i += nthr) c.ooff[i] = int(woff[i]);
+    #pragma unroll 1
     for (int i = tid; i < 2 * nv; i += nthr) c.vert[i] = T(wv[i]);
     if (c.vert64 != nullptr) {      // FP64 copy: vertices, then start and target
+        #pragma unroll 1
         for (int i = tid; i < 2 * nv; i += nthr) c.vert64[i] = wv[i];
         if (tid == 0) {
             c.vert64[2 * nv] = wh->sx; c.vert64[2 * nv + 1] = wh->sy;
@@ -446,6 +450,7 @@ __device__ void load_world(Ctx<T>& c, const unsigned char* wrec, int off_offsets
     }
     if (bar == 0) __syncthreads();
     else asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nthr) : "memory");
+    #pragma unroll 1
     for (int o = tid; o < c.O; o += nthr) {                  // bbox_of, geometry.hpp:167-177
         const int v0 = c.ooff[o], v1 = c.ooff[o + 1];
         T bx0 = c.vert[2 * v0], by0 = c.vert[2 * v0 + 1], bx1 = bx0, by1 = by0;

@@ -491,6 +491,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
         // offsets -> vertices reads below are not a chain of DRAM round trips
         const int nv4 = int(p.world_stride / 16);          // <= the layout's allocation (max_obs, max_verts)
         unsigned char* wsm = S8(L.wcopy);
+        #pragma unroll 1
         for (int i = tid; i < nv4; i += nthr)
             reinterpret_cast<uint4*>(wsm)[i] = __ldcg(reinterpret_cast<const uint4*>(wrec) + i);
         __syncthreads();
@@ -531,6 +532,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
         if (pre_cand) {
             // the walk arrives from HBM (seeded here only if it is late)
         } else if (seeded) {                  // the host's seeded state, one warp copies it
+            #pragma unroll 1
             for (int i = tid - cw; i < 312; i += nthr - cw) mtbuf[312 + i] = seeded[i];
         } else if (tid == cw) {
             mt_seed_words(mtbuf + 312, seed);
@@ -542,6 +544,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
         SEPSO_SMARK(5);
         const double* hyp_src = (p.inl ? reinterpret_cast<const double*>(jb + p.in_hyp) : p.hypers) +
                                 size_t(swarm) * size_t(p.hypers_stride);
+        #pragma unroll 1
         for (int i = tid; i < G * 6; i += cw) c.hyp[i] = T(hyp_src[i]);
         SEPSO_IMARK(15);
         SEPSO_SMARK(0);
@@ -554,6 +557,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
         } else {
             const double* lo_src = p.inl ? reinterpret_cast<const double*>(jb + p.in_lo) : p.lo;
             const double* hi_src = p.inl ? reinterpret_cast<const double*>(jb + p.in_hi) : p.hi;
+            #pragma unroll 1
             for (int d = tid; d < D; d += cw) { c.lo[d] = T(lo_src[d]); c.hi[d] = T(hi_src[d]); }
         }
         if (tid == 0) {
@@ -573,14 +577,18 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
             }
         }
         if (p.carry)
+            #pragma unroll 1
             for (int i = tid; i < p.tw; i += cw)
                 c.win[i] = (p.inl ? reinterpret_cast<const double*>(jb + p.in_win) : p.win_vals)[size_t(swarm) * p.tw + i];
+        #pragma unroll 1
         for (int g = tid; g < G; g += cw) {
             c.gbf[g] = A::inf(); c.gbq[g] = 0; c.chg[g] = -1;
             c.gtab[2 * g] = (g * N) / p.rows_per_cta;               // CTAs owning group g
             c.gtab[2 * g + 1] = ((g + 1) * N - 1) / p.rows_per_cta;
         }
+        #pragma unroll 1
         for (int cc = tid; cc < c.C; cc += cw) c.ctab[cc] = (cc * p.rows_per_cta) / N;
+        #pragma unroll 1
         for (int pl = tid; pl < c.P; pl += cw) { c.pbf[pl] = A::inf(); c.pbq[pl] = 0; c.q[pl] = 0; }
         SEPSO_IMARK(14);
         SEPSO_SMARK(3);
@@ -656,6 +664,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
                 // this CTA's x / v words straight from HBM, the generator's
                 // last pair where the step draws continue
                 const int nx = int(x1 - x0);
+                #pragma unroll 1
                 for (int e = tid; e < nx; e += nthr) {
                     const int pl = int(c.fD.div(uint32_t(e))), d = e - pl * D;
                     const unsigned long long wx = __ldcg(pre_w + x0 + e), wv = __ldcg(pre_w + RD + x0 + e);
@@ -664,6 +673,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
                 }
                 const unsigned long long* pp = (prr ? reinterpret_cast<const unsigned long long*>(prr->pair) : p.pre_pair) +
                                                size_t(swarm) * kPrePairWords;
+                #pragma unroll 1
                 for (int i = tid; i < 624; i += nthr) mtbuf[i] = __ldcg(pp + i);
                 if (tid == 0) { c.m->mt_cur = 0; c.m->mt_blocks = (long long)__ldcg(pp + 624); }
                 SEPSO_IMARK(5);
@@ -1105,6 +1115,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
         const T* pxb = c.px + size_t(buf) * c.C * LGM * D;  // this iteration's pushed rows
         if (c.m->stop || k == p.cap) {                       // no step after the last iteration
             if (tslot >= 0)
+                #pragma unroll 1
                 for (int d = tid; d < D; d += nthr) c.tbx[d] = pxb[tslot * D + d];
             __syncthreads();
             break;
@@ -1256,10 +1267,13 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
     }
     if (c.crank == 0) {
         if (srv)
+            #pragma unroll 1
             for (int d = tid; d < D; d += nthr) put_chunk_d(p.out, 4 + d, double(c.tbx[d]), 0u, jseq);
         else
+            #pragma unroll 1
             for (int d = tid; d < D; d += nthr) p.best_x[size_t(swarm) * D + d] = double(c.tbx[d]);
         if (p.carry && !srv) {      // (the resident planner's host keeps the window from the trace)
+            #pragma unroll 1
             for (int i = tid; i < c.m->win_len; i += nthr)
                 p.win_vals[size_t(swarm) * p.tw + i] = c.win[(c.m->win_head + i) % p.tw];
             if (tid == 0) p.win_len[swarm] = c.m->win_len;
@@ -1269,6 +1283,7 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
     // (simenv.hpp:155-184); every CTA staged it long ago.  Rank 1 does it
     // while rank 0 writes the record.
     if (PATH && p.step_dt != 0.0 && c.crank == (c.C > 1 ? 1 : 0))
+        #pragma unroll 1
         for (int t = tid - 2; t < c.O; t += nthr)
             step_world_part(const_cast<unsigned char*>(p.worlds) + size_t(swarm) * size_t(p.world_stride),
                             p.off_offsets, p.off_verts, p.off_vel, p.step_dt, t);
