@@ -396,6 +396,10 @@ __device__ __forceinline__ bool box_overlap<float>(float lx, float ly, float hx,
     return lx <= b.z + m && b.x <= hx + m && ly <= b.w + m && b.y <= hy + m;
 }
 
+#ifndef SEPSO_BOX_UNROLL
+#define SEPSO_BOX_UNROLL 8
+#endif
+constexpr int kBoxUnroll = SEPSO_BOX_UNROLL;
 // Total order key for a fitness value: orderable bits (+0 canonical), so the
 // group argmin can use 32-bit warp reductions (REDUX).
 __device__ __forceinline__ uint32_t order_key(float f) {
@@ -555,7 +559,7 @@ __device__ void path_fitness_phase(const SwarmParams& p, Ctx<T>& c, long long* p
                 uint32_t mask = 0;
                 if (valid) {
                     const int oe = min(32, O - o0);
-#pragma unroll 8
+#pragma unroll kBoxUnroll
                     for (int j = 0; j < oe; ++j)
                         if (box_overlap(lx, ly, hx, hy, c.obb + 4 * (o0 + j), c.margin)) mask |= 1u << j;
                 }
@@ -591,7 +595,7 @@ __device__ void path_fitness_phase(const SwarmParams& p, Ctx<T>& c, long long* p
             for (int o0 = 0; o0 < O; o0 += 32) {
                 uint32_t mask = 0;
                 const int oe = min(32, O - o0);
-#pragma unroll 8
+#pragma unroll kBoxUnroll
                 for (int j = 0; j < oe; ++j)
                     if (box_overlap(lx, ly, hx, hy, c.obb + 4 * (o0 + j), c.margin)) mask |= 1u << j;
                 while (mask) {
