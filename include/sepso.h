@@ -132,6 +132,14 @@ int sf_plan_frame(sf_ctx* ctx, const sf_world* world, const double* prev_particl
                   const double* hypers, const sf_planner_config* cfg, uint64_t seed,
                   double* window, uint32_t* window_len, uint32_t window_cap,
                   sf_plan_record* record, double* best_particle, uint64_t* bad);
+/* Optional hint for a caller that plans a sequence of frames itself (the
+ * run_scenario loop, simenv.hpp:239-276): the seed of the frame AFTER the next
+ * sf_plan_frame call on this context.  That call then starts the next frame's
+ * mt19937_64 init walk on a spare SM while it plans, and
+ * the following call with that seed skips the walk.  Consumed by the next
+ * sf_plan_frame; valid = 0 clears it.  Results never depend on it.
+ * (sf_run_scenario sets it itself.) */
+int sf_ctx_hint_next_seed(sf_ctx* ctx, uint64_t seed, int valid);
 
 /* Many independent planning queries in ONE launch (config 5).  Arrays are per
  * scene: worlds[n], prev (n*dim, rows used where has_prev[s]), seeds[n],

@@ -792,6 +792,13 @@ int sf_ctx_kernel_time(sf_ctx* ctx, double* total_ms, uint64_t* launches) {
     return SF_OK;
 }
 
+int sf_ctx_hint_next_seed(sf_ctx* ctx, uint64_t seed, int valid) {
+    if (!ctx) return fail(SF_INVALID_ARGUMENT, "ctx is null");
+    ctx->hint_seed = seed;
+    ctx->hint_valid = valid != 0;
+    return SF_OK;
+}
+
 // planner.hpp:156-199
 int sf_plan_frame(sf_ctx* ctx, const sf_world* world, const double* prev, const double* hypers,
                   const sf_planner_config* cfg, uint64_t seed, double* window, uint32_t* window_len,
@@ -831,7 +838,9 @@ int sf_plan_frame(sf_ctx* ctx, const sf_world* world, const double* prev, const 
         b.win_lens = &wl;
     }
     static thread_local BatchOut r;             // reused: no allocation per frame
-    if ((st = run_batch(ctx, b, r))) return st;
+    st = run_batch(ctx, b, r);
+    ctx->hint_valid = false;                    // a next-seed hint serves one call
+    if (st) return st;
     const SwarmOut& o = r.out[0];
     if (o.status == 2) {
         if (bad) { bad[0] = o.bad_g; bad[1] = o.bad_n; bad[2] = o.bad_k; }

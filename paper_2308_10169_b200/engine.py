@@ -40,6 +40,7 @@ ABI_SYMBOLS = [
     "sf_ctx_last_io_bytes", "sf_measure_fp32_peak", "sf_ctx_set_l2_flush",
     "sf_comm_unique_id", "sf_ctx_init_comm", "sf_plan_frame_sharded", "sf_ctx_set_rng",
     "sf_ctx_rng", "sf_mt_jump_poly", "sf_derive_seed", "sf_measure_step_kernel", "sf_ctx_set_exchange",
+    "sf_ctx_hint_next_seed",
 ]
 # sf_allgather_fn: int (*)(void* user, const void* send, void* recv, size_t bytes)
 _ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
@@ -176,6 +177,7 @@ def lib():
         "sf_measure_fp32_peak": (C.c_int, [C.c_void_p, _dp]),
         "sf_measure_step_kernel": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _dp, _dp]),
         "sf_ctx_set_exchange": (C.c_int, [C.c_void_p, C.c_int, C.c_int, _ALLGATHER_FN, C.c_void_p]),
+        "sf_ctx_hint_next_seed": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int]),
         "sf_mt_jump_poly": (C.c_int, [C.c_uint64, _u64p]),
         "sf_ctx_set_l2_flush": (C.c_int, [C.c_void_p, C.c_uint64]),
         "sf_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
@@ -520,6 +522,11 @@ class Engine:
         return ms.value, n.value
 
     # -- planner.hpp:156-199
+    def hint_next_seed(self, seed: Optional[int]):
+        """The seed of the frame after the next plan_frame call (None clears):
+        that call starts the next frame's init walk while it plans."""
+        _check(self._L.sf_ctx_hint_next_seed(self._h, C.c_uint64(seed or 0), 0 if seed is None else 1))
+
     def plan_frame(self, world: PolygonWorld, prev_best, hypers, config: PlannerConfig,
                    seed: int, carried_window: Optional[list] = None):
         """Returns a PlanRecord; `carried_window` (a list) is updated in place."""
