@@ -661,6 +661,8 @@ int run_batch(sf_ctx* ctx, const BatchIn& b, BatchOut& r) {
         std::memcpy(r.out.data(), res, sizeof(SwarmOut));
         std::memcpy(r.best.data(), res + (io.best - io.out), size_t(b.D) * 8);
         std::memcpy(r.trace.data(), res + (io.trace - io.out), size_t(b.cap) * 8);
+        // the record's tagged chunks the cluster wrote over the bus
+        ctx->last_d2h = 16 * (4 + uint64_t(b.D) + std::min<uint64_t>(r.out[0].iterations, b.cap));
         return SF_OK;
     }
     st = launch_fused(ctx, fp, b.problem);
