@@ -112,14 +112,16 @@ __device__ __forceinline__ void mt_store_quad(unsigned long long* nb, int t, con
 // that fall in [0, len), handed to the sink by the group's threads -- by the
 // threads beyond the four compute warps when the group has them, so delivery
 // stays off the generation chain.
-template <bool RAW = false, class Sink>
+// GEN: the group's generating lanes (128, or 96 for the three-warp step
+// generator); lanes beyond them, when the group has some, deliver alone.
+template <bool RAW = false, int GEN = 128, class Sink>
 __device__ __forceinline__ void mt_deliver_pair(const unsigned long long* pr, long long rel, int len,
                                                 const MtGroup& g, Sink& sink) {
     const int lo = rel < 0 ? int(-rel) : 0;
     const long long hi_ = (long long)len - rel;
     const int hi = hi_ < 624 ? int(hi_) : 624;
-    const bool helpers = g.n >= 256;
-    const int dl = helpers ? g.lt - 128 : g.lt, dn = helpers ? g.n - 128 : g.n;
+    const bool helpers = GEN == 96 ? g.n > 96 : g.n >= 256;
+    const int dl = helpers ? g.lt - GEN : g.lt, dn = helpers ? g.n - GEN : g.n;
     if (dl < 0) return;
     for (int i = lo + dl; i < hi; i += dn) sink(int(rel + i), RAW ? pr[i] : mt_temper(pr[i]));
 }
@@ -142,20 +144,24 @@ __device__ inline void mt_generate(MtState& s, const MtGroup& g, long long from,
     long long rel = 312 * s.blocks - from;        // offset of the next new word
     bool pend = s.blocks > 0 && rel > 0 && rel - 624 < len;   // the latest pair
     long long prel = rel - 624;
-    if (FN == 96) {
+    if (FN == 96 || FN == 97) {
         // three warps (the step generator off the first SM sub-partition, whose
         // warp runs the serial best update): lanes 0..95 take positions
-        // 0..95, lanes 0..59 also 96..155
+        // 0..95, lanes 0..59 also 96..155; FN 97: lanes 96.. (helper warps)
+        // only deliver
         const int lt = g.lt;
+        const bool gen = FN == 96 || lt < 96;
         const bool second = lt < 60;
         const int t2 = second ? 96 + lt : 96;
         while (rel < len) {
             const unsigned long long* o = s.buf + s.cur * 624 + 312;
             unsigned long long* nb = s.buf + (s.cur ^ 1) * 624;
-            const MtQuad q1 = mt_quad(o, lt, o[lt + 157], o[lt + 158]);
-            if (second) mt_store_quad(nb, t2, mt_quad_any(o, t2));
-            mt_store_quad(nb, lt, q1);
-            if (pend) mt_deliver_pair<RAW>(s.buf + s.cur * 624, prel, len, g, sink);
+            if (gen) {
+                const MtQuad q1 = mt_quad(o, lt, o[lt + 157], o[lt + 158]);
+                if (second) mt_store_quad(nb, t2, mt_quad_any(o, t2));
+                mt_store_quad(nb, lt, q1);
+            }
+            if (pend) mt_deliver_pair<RAW, FN == 97 ? 96 : 128>(s.buf + s.cur * 624, prel, len, g, sink);
             mt_sync(g);
             s.cur ^= 1;
             s.blocks += 2;
@@ -200,7 +206,7 @@ __device__ inline void mt_generate(MtState& s, const MtGroup& g, long long from,
             rel += 624;
         }
     }
-    if (pend) mt_deliver_pair<RAW>(s.buf + s.cur * 624, prel, len, g, sink);
+    if (pend) mt_deliver_pair<RAW, FN == 97 ? 96 : 128>(s.buf + s.cur * 624, prel, len, g, sink);
 }
 
 } // namespace sepso

@@ -58,6 +58,11 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         "}\n" ::"r"(bar), "r"(parity) : "memory");
 }
 
+#ifndef SEPSO_GEN_HELPERS
+#define SEPSO_GEN_HELPERS 8
+#endif
+constexpr int kGenHelpers = SEPSO_GEN_HELPERS;   // warps that deliver the step draws beside the generator
+
 // r1, r2, r3 of step k (draw_step_randoms, swarm.hpp:59-70): R words each at
 // 2RD + (k-1)*3R of the mt19937_64 stream; rows [row0, row1) keep a_j = c_j * r_j.
 template <int FN, class T>
@@ -760,19 +765,32 @@ __global__ void __launch_bounds__(MAXT, 1) swarm_kernel(const __grid_constant__ 
         const bool gen_early = (kLat || (p.rng == kMt19937 && nthr >= 192)) && k < p.cap;
         const int gw0 = (nthr >> 5) - 4;
         const bool gen_first = gen_early && (kLat || (gw0 * 32 >= c.P && c.LG <= gw0));
+        // helper warps below the generator (idle until the step: no partial,
+        // no best update) take the draws' delivery -- tempering and storing
+        // this CTA's 3P factors -- off the three generating warps
+        // (throughput launches only: there a CTA delivers 3 x ~680 words per
+        // step; the latency shape's 3 x 85 do not pay for the wider barrier)
+        constexpr int kHelp = RING ? kGenHelpers : 0;
+        const int hw0 = gw0 - kHelp;
+        const int gn = (kHelp > 0 && hw0 >= c.LG && hw0 >= 1) ? 96 + 32 * kHelp : 96;
         if (gen_first && warp >= gw0) {
             // three of the four warps generate (SM sub-partitions 1-3): the
             // ALU-bound generator then never competes with warp 0's serial
             // partial / best-update chain on sub-partition 0
             long long* gprof = (kProfiling && p.prof != nullptr && swarm == 0 && c.crank == 0 && tid == (gw0 + 1) * 32) ? p.prof : nullptr;
             if (gprof) gprof[(k - 1) * kProfPhases + 12] = clock64();
-            if (warp > gw0) mt_step_draws<96>(c, mtbuf, MtGroup{tid - (gw0 + 1) * 32, 96, 1}, k, row1);
+            if (warp > gw0) {
+                if (kHelp > 0 && gn > 96) mt_step_draws<97>(c, mtbuf, MtGroup{tid - (gw0 + 1) * 32, gn, 1}, k, row1);
+                else mt_step_draws<96>(c, mtbuf, MtGroup{tid - (gw0 + 1) * 32, 96, 1}, k, row1);
+            }
             if (gprof) gprof[(k - 1) * kProfPhases + 13] = clock64();
         } else {
         if (!PATH)                                   // path swarms: fused into A3 above
             for (int pl = tid; pl < c.P; pl += nthr) pbest_row(c, pl, c.fit[pl]);
         if (gen_first) asm volatile("bar.sync 2, %0;" ::"r"(gw0 * 32) : "memory");   // pbest done (not the generator)
         else __syncthreads();
+        if (kHelp > 0 && gen_first && gn > 96 && warp >= hw0)
+            mt_step_draws<97>(c, mtbuf, MtGroup{96 + tid - hw0 * 32, gn, 1}, k, row1);
         }
         SEPSO_MARK(5);
         if (tid == 0) mbar_expect(mbar0 + 8 * buf, xbytes);
