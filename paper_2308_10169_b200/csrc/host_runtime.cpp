@@ -475,7 +475,11 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
     // long init windows are generated in parallel segments from jumped states
     const long long init_words = 2ll * R * D;
     int jlevels = 0;
-    while (mt && jlevels < kMaxJumpLevels && (init_words >> (jlevels + 1)) >= (1ll << 17)) ++jlevels;
+    // (segments of >= 2^17 words; more than 64 only when each keeps >= 2^20: a
+    // level of jumps costs about as much as ~2^20 words of one segment's walk)
+    while (mt && jlevels < kMaxJumpLevels &&
+           (init_words >> (jlevels + 1)) >= (jlevels < kWideJumpLevels ? (1ll << 17) : (1ll << 20)))
+        ++jlevels;
     if (std::getenv("SEPSO_SEQ_FILL")) jlevels = 0;
     const bool jump = jlevels >= 2;
     const size_t o_jst = take(jump ? (size_t(1) << jlevels) * 312 * 8 : 0);

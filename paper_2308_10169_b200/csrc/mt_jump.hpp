@@ -8,7 +8,8 @@ namespace sepso {
 
 constexpr int kMtDegree = 19937;       // state bits of std::mt19937_64
 constexpr int kMtPolyWords = 312;      // 19,968 bits
-constexpr int kMaxJumpLevels = 6;      // parallel fills: at most 64 segments
+constexpr int kMaxJumpLevels = 8;      // parallel fills: at most 256 segments
+constexpr int kWideJumpLevels = 6;     // beyond 64 segments only for segments of >= 2^20 words
 
 // x^steps mod phi: applying it to the state at word w gives the state at w + steps
 std::vector<uint64_t> mt_jump_poly(uint64_t steps);

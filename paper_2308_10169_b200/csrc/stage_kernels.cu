@@ -632,22 +632,83 @@ int stage_eval_path(bool fp64, const unsigned char* world, int max_obs, int max_
     return int(cudaGetLastError());
 }
 
+// Benchmark fitness of many rows (benchmarks.hpp:56-88, the staged path): a
+// warp owns 32 rows, lane l row r0 + l, and walks them in 32-column tiles --
+// the warp loads a tile row by row (coalesced: 32 consecutive columns of one
+// row per load) into shared memory, then every lane folds its row's 32
+// elements in index order (bench_elem, the same arithmetic as the fused
+// kernel's bench_row).  A thread-per-row walk straight from HBM touches 32
+// cache lines per warp load and ran at ~40 % of the copy bandwidth.
+template <class T> constexpr int kBenchWarps = sizeof(T) == 8 ? 4 : 8;   // static tiles under 48 KB
+template <int K, class T>
+__device__ __forceinline__ void bench_rows_tiled(int D, int rows, const T* __restrict__ x, T* fit, int* q, T* tile) {
+    const int lane = threadIdx.x & 31;
+    const int nw = int(gridDim.x) * kBenchWarps<T>;
+    for (int r0 = (blockIdx.x * kBenchWarps<T> + (threadIdx.x >> 5)) * 32; r0 < rows; r0 += nw * 32) {
+        T s = T(0), t = bench_t0<K, T>(), xp = T(0);
+        const int nr = min(32, rows - r0);
+        const T* base = x + size_t(r0) * D + lane;
+        // software pipeline: the next tile's 32 loads are in flight (registers)
+        // while the lanes fold the current one from shared memory
+        T nxt[32];
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) nxt[rr] = (rr < nr && lane < D) ? base[size_t(rr) * D] : T(0);
+        for (int c0 = 0; c0 < D; c0 += 32) {
+#pragma unroll
+            for (int rr = 0; rr < 32; ++rr) tile[rr * 33 + lane] = nxt[rr];
+            __syncwarp();
+            const int c1 = c0 + 32;
+            if (c1 < D) {
+                const bool ok = c1 + lane < D;
+#pragma unroll
+                for (int rr = 0; rr < 32; ++rr) nxt[rr] = (rr < nr && ok) ? base[size_t(rr) * D + c1] : T(0);
+            }
+            const int n = min(32, D - c0);
+            if (n == 32) {
+#pragma unroll 8
+                for (int j = 0; j < 32; ++j) {
+                    const T v = tile[lane * 33 + j];
+                    bench_elem<K, T>(c0 + j, v, xp, s, t);
+                    xp = v;
+                }
+            } else {
+                for (int j = 0; j < n; ++j) {
+                    const T v = tile[lane * 33 + j];
+                    bench_elem<K, T>(c0 + j, v, xp, s, t);
+                    xp = v;
+                }
+            }
+            __syncwarp();
+        }
+        if (lane < nr) {
+            fit[r0 + lane] = bench_fin<K, T>(s, t, D);
+            if (q) q[r0 + lane] = 0;
+        }
+    }
+}
+
 template <class T>
-__global__ void k_eval_bench(int kind, int D, int rows, const T* x, T* fit, int* q,
-                             const IterState* gate) {
+__global__ void __launch_bounds__(kBenchWarps<T> * 32) k_eval_bench(int kind, int D, int rows, const T* __restrict__ x,
+                                                                 T* fit, int* q, const IterState* gate) {
+    __shared__ T tiles[kBenchWarps<T>][32 * 33];
     if (gate != nullptr && gate->stop) return;
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
-        fit[r] = bench_eval<T>(kind, x + size_t(r) * D, D);
-        if (q) q[r] = 0;
+    T* tile = tiles[threadIdx.x >> 5];
+    switch (kind) {
+    case kSphere: bench_rows_tiled<kSphere, T>(D, rows, x, fit, q, tile); break;
+    case kRosenbrock: bench_rows_tiled<kRosenbrock, T>(D, rows, x, fit, q, tile); break;
+    case kRastrigin: bench_rows_tiled<kRastrigin, T>(D, rows, x, fit, q, tile); break;
+    case kGriewank: bench_rows_tiled<kGriewank, T>(D, rows, x, fit, q, tile); break;
+    case kAckley: bench_rows_tiled<kAckley, T>(D, rows, x, fit, q, tile); break;
     }
 }
 
 int stage_eval_bench(bool fp64, int kind, int D, int rows, const void* x, void* fit, int* q,
                      const IterState* gate, void* stream) {
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const unsigned grid = grid_for(rows, 128);
-    if (fp64) k_eval_bench<double><<<grid, 128, 0, st>>>(kind, D, rows, (const double*)x, (double*)fit, q, gate);
-    else k_eval_bench<float><<<grid, 128, 0, st>>>(kind, D, rows, (const float*)x, (float*)fit, q, gate);
+    const int bw = fp64 ? kBenchWarps<double> : kBenchWarps<float>;
+    const unsigned grid = grid_for((rows + 31) / 32, bw);
+    if (fp64) k_eval_bench<double><<<grid, bw * 32, 0, st>>>(kind, D, rows, (const double*)x, (double*)fit, q, gate);
+    else k_eval_bench<float><<<grid, bw * 32, 0, st>>>(kind, D, rows, (const float*)x, (float*)fit, q, gate);
     return int(cudaGetLastError());
 }
 

@@ -60,93 +60,99 @@ __device__ __forceinline__ double penalty(double alpha, double beta, int beta_in
 
 // benchmarks.hpp:56-88 (+ Ackley extension).  FP64: std::cos as the
 // reference's host computes it (cos_glibc.cuh), so BF3 / BF4 runs stay bit-exact.
-template <class T> __device__ T bench_eval(int kind, const T* p, int D);
-template <> inline __device__ double bench_eval<double>(int kind, const double* p, int D) {
-    using A = Ar<double>;
-    const double two_pi = 6.283185307179586;   // 2.0 * std::numbers::pi
-    switch (kind) {
-    case kSphere: {
-        double s = 0.0;
-        for (int i = 0; i < D; ++i) s = A::add(s, A::mul(p[i], p[i]));
-        return s;
-    }
-    case kRosenbrock: {
-        double s = 0.0;
-        for (int i = 0; i + 1 < D; ++i) {
-            const double a = A::sub(p[i + 1], A::mul(p[i], p[i]));
-            const double b = A::sub(1.0, p[i]);
-            s = A::add(s, A::add(A::mul(A::mul(100.0, a), a), A::mul(b, b)));
+// One row is a stream of elements in index order: bench_elem<K> folds element
+// i (value x, previous value xp) into the running sums (s, t) exactly as the
+// reference's loop does -- Rosenbrock's term i - 1 pairs p[i-1] with p[i] --
+// and bench_fin<K> closes the row.  The fused kernel walks a row in place
+// (bench_row); the staged evaluation streams rows through shared-memory tiles
+// (k_eval_bench, stage_kernels.cu).  Both run this same arithmetic.
+template <int K, class T>
+__device__ __forceinline__ void bench_elem(int i, T x, T xp, T& s, T& t) {
+    if constexpr (sizeof(T) == 8) {
+        using A = Ar<double>;
+        const double two_pi = 6.283185307179586;   // 2.0 * std::numbers::pi
+        if constexpr (K == kSphere) {
+            s = A::add(s, A::mul(x, x));
+        } else if constexpr (K == kRosenbrock) {
+            if (i > 0) {
+                const double a = A::sub(x, A::mul(xp, xp));
+                const double b = A::sub(1.0, xp);
+                s = A::add(s, A::add(A::mul(A::mul(100.0, a), a), A::mul(b, b)));
+            }
+        } else if constexpr (K == kRastrigin) {
+            s = A::add(s, A::add(A::sub(A::mul(x, x), A::mul(10.0, cos_glibc(A::mul(two_pi, x)))), 10.0));
+        } else if constexpr (K == kGriewank) {
+            s = A::add(s, A::mul(x, x));
+            t = A::mul(t, cos_glibc(__ddiv_rn(x, __dsqrt_rn(double(i + 1)))));
+        } else {   // kAckley
+            s = A::add(s, A::mul(x, x));
+            t = A::add(t, cos_glibc(A::mul(two_pi, x)));
         }
-        return s;
-    }
-    case kRastrigin: {
-        double s = 0.0;
-        for (int i = 0; i < D; ++i)
-            s = A::add(s, A::add(A::sub(A::mul(p[i], p[i]), A::mul(10.0, cos_glibc(A::mul(two_pi, p[i])))),
-                                 10.0));
-        return s;
-    }
-    case kGriewank: {
-        double sum = 0.0, prod = 1.0;
-        for (int i = 0; i < D; ++i) {
-            sum = A::add(sum, A::mul(p[i], p[i]));
-            prod = A::mul(prod, cos_glibc(__ddiv_rn(p[i], __dsqrt_rn(double(i + 1)))));
+    } else {
+        const float two_pi = 6.2831853f;
+        if constexpr (K == kSphere) {
+            s += x * x;
+        } else if constexpr (K == kRosenbrock) {
+            if (i > 0) {
+                const float a = x - xp * xp;
+                const float b = 1.f - xp;
+                s += 100.f * a * a + b * b;
+            }
+        } else if constexpr (K == kRastrigin) {
+            s += x * x - 10.f * cosf(two_pi * x) + 10.f;
+        } else if constexpr (K == kGriewank) {
+            s += x * x;
+            t *= cosf(x * rsqrtf(float(i + 1)));
+        } else {   // kAckley
+            s += x * x;
+            t += cosf(two_pi * x);
         }
-        return A::sub(A::add(1.0, __ddiv_rn(sum, 4000.0)), prod);
     }
-    case kAckley: {
-        double s1 = 0.0, s2 = 0.0;
-        for (int i = 0; i < D; ++i) {
-            s1 = A::add(s1, A::mul(p[i], p[i]));
-            s2 = A::add(s2, cos_glibc(A::mul(two_pi, p[i])));
-        }
-        const double dd = double(D);
-        return -20.0 * exp(-0.2 * sqrt(s1 / dd)) - exp(s2 / dd) + 20.0 + 2.718281828459045;
-    }
-    }
-    return __longlong_as_double(0x7ff8000000000000ll);
 }
-template <> inline __device__ float bench_eval<float>(int kind, const float* p, int D) {
-    const float two_pi = 6.2831853f;
+
+template <int K, class T> __device__ __forceinline__ T bench_t0() { return K == kGriewank ? T(1) : T(0); }
+
+template <int K, class T>
+__device__ __forceinline__ T bench_fin(T s, T t, int D) {
+    if constexpr (sizeof(T) == 8) {
+        using A = Ar<double>;
+        if constexpr (K == kGriewank) return A::sub(A::add(1.0, __ddiv_rn(s, 4000.0)), t);
+        if constexpr (K == kAckley) {
+            const double dd = double(D);
+            return -20.0 * exp(-0.2 * sqrt(s / dd)) - exp(t / dd) + 20.0 + 2.718281828459045;
+        }
+        return s;
+    } else {
+        if constexpr (K == kGriewank) return 1.f + s / 4000.f - t;
+        if constexpr (K == kAckley) {
+            const float dd = float(D);
+            return -20.f * expf(-0.2f * sqrtf(s / dd)) - expf(t / dd) + 20.f + 2.7182817f;
+        }
+        return s;
+    }
+}
+
+template <int K, class T>
+__device__ __forceinline__ T bench_row(const T* p, int D) {
+    T s = T(0), t = bench_t0<K, T>(), xp = T(0);
+    for (int i = 0; i < D; ++i) {
+        const T x = p[i];
+        bench_elem<K, T>(i, x, xp, s, t);
+        xp = x;
+    }
+    return bench_fin<K, T>(s, t, D);
+}
+
+template <class T>
+__device__ T bench_eval(int kind, const T* p, int D) {
     switch (kind) {
-    case kSphere: {
-        float s = 0.f;
-        for (int i = 0; i < D; ++i) s += p[i] * p[i];
-        return s;
+    case kSphere: return bench_row<kSphere, T>(p, D);
+    case kRosenbrock: return bench_row<kRosenbrock, T>(p, D);
+    case kRastrigin: return bench_row<kRastrigin, T>(p, D);
+    case kGriewank: return bench_row<kGriewank, T>(p, D);
+    case kAckley: return bench_row<kAckley, T>(p, D);
     }
-    case kRosenbrock: {
-        float s = 0.f;
-        for (int i = 0; i + 1 < D; ++i) {
-            const float a = p[i + 1] - p[i] * p[i];
-            const float b = 1.f - p[i];
-            s += 100.f * a * a + b * b;
-        }
-        return s;
-    }
-    case kRastrigin: {
-        float s = 0.f;
-        for (int i = 0; i < D; ++i) s += p[i] * p[i] - 10.f * cosf(two_pi * p[i]) + 10.f;
-        return s;
-    }
-    case kGriewank: {
-        float sum = 0.f, prod = 1.f;
-        for (int i = 0; i < D; ++i) {
-            sum += p[i] * p[i];
-            prod *= cosf(p[i] * rsqrtf(float(i + 1)));
-        }
-        return 1.f + sum / 4000.f - prod;
-    }
-    case kAckley: {
-        float s1 = 0.f, s2 = 0.f;
-        for (int i = 0; i < D; ++i) {
-            s1 += p[i] * p[i];
-            s2 += cosf(two_pi * p[i]);
-        }
-        const float dd = float(D);
-        return -20.f * expf(-0.2f * sqrtf(s1 / dd)) - expf(s2 / dd) + 20.f + 2.7182817f;
-    }
-    }
-    return __int_as_float(0x7fc00000);
+    return T(__longlong_as_double(0x7ff8000000000000ll));
 }
 
 // -------------------------------------------------------- fast division
