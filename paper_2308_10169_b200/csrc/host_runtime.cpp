@@ -475,15 +475,16 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
     // long init windows are generated in parallel segments from jumped states
     const long long init_words = 2ll * R * D;
     int jlevels = 0;
-    // (segments of >= 2^17 words; more than 64 only when each keeps >= 2^20: a
-    // level of jumps costs about as much as ~2^20 words of one segment's walk)
+    // (segments of >= 2^17 words; more than 64 only when each keeps >= 2^20:
+    // level 7's 128 jumps cost ~230 us, and two segment walks on one SM run at
+    // ~65 % each, so 256 segments of 2^20 words lose to 128 of 2^21)
     while (mt && jlevels < kMaxJumpLevels &&
            (init_words >> (jlevels + 1)) >= (jlevels < kWideJumpLevels ? (1ll << 17) : (1ll << 20)))
         ++jlevels;
     if (std::getenv("SEPSO_SEQ_FILL")) jlevels = 0;
     const bool jump = jlevels >= 2;
     const size_t o_jst = take(jump ? (size_t(1) << jlevels) * 312 * 8 : 0);
-    const size_t o_jpoly = take(jump ? size_t(jlevels) * 312 * 8 : 0);
+    const size_t o_jpoly = take(jump ? size_t(jlevels) * kMtDegree * 2 : 0);   // exponent lists (uint16)
     cudaError_t ce = ctx->scratch.ensure(off);
     if (ce != cudaSuccess) return cuda_fail(ce, "staged arena");
     unsigned char* dev = static_cast<unsigned char*>(ctx->scratch.p);
@@ -533,16 +534,13 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
     if (mt && jump) {   // the reference stream, init words [0, 2RD) in 2^jlevels segments
         const long long seg = (init_words + (1ll << jlevels) - 1) >> jlevels;
         const long long Q = (seg + 623) / 624 * 624;                // whole generator passes
-        const std::vector<std::vector<uint64_t>>& ladder = mt_jump_ladder(uint64_t(Q), jlevels);
-        for (int j = 0; j < jlevels; ++j) {
-            ce = cudaMemcpyAsync(dev + o_jpoly + size_t(j) * 312 * 8, ladder[size_t(j)].data(), 312 * 8,
-                                 cudaMemcpyHostToDevice, st);
-            if (ce != cudaSuccess) return cuda_fail(ce, "jump polynomials");
-        }
+        const MtJumpTerms& jt = mt_jump_ladder_terms(uint64_t(Q), jlevels);   // cached: stays valid
+        ce = cudaMemcpyAsync(dev + o_jpoly, jt.terms.data(), jt.terms.size() * 2, cudaMemcpyHostToDevice, st);
+        if (ce != cudaSuccess) return cuda_fail(ce, "jump terms");
         const int fe = stage_mt_fill_parallel(mtg, r.seed, init_words, words,
                                               reinterpret_cast<unsigned long long*>(dev + o_jst),
-                                              reinterpret_cast<const unsigned long long*>(dev + o_jpoly), jlevels, Q,
-                                              st);
+                                              reinterpret_cast<const unsigned short*>(dev + o_jpoly), jt.count.data(),
+                                              jlevels, Q, st);
         if (fe) return cuda_fail(cudaError_t(fe), "stage_mt_fill_parallel");
     } else if (mt) {   // sequential
         const int fe = stage_mt_fill(mtg, r.seed, true, 0, init_words, words, st);

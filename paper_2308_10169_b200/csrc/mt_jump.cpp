@@ -160,4 +160,22 @@ const std::vector<std::vector<uint64_t>>& mt_jump_ladder(uint64_t quantum, int l
     return cache.emplace(std::make_pair(quantum, levels), std::move(polys)).first->second;
 }
 
+const MtJumpTerms& mt_jump_ladder_terms(uint64_t quantum, int levels) {
+    const std::vector<std::vector<uint64_t>>& ladder = mt_jump_ladder(quantum, levels);
+    static std::mutex mu;
+    static std::map<std::pair<uint64_t, int>, MtJumpTerms> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find({quantum, levels});
+    if (it != cache.end()) return it->second;
+    MtJumpTerms t;
+    t.terms.assign(size_t(levels) * kMtDegree, 0);
+    t.count.assign(size_t(levels), 0);
+    for (int j = 0; j < levels; ++j) {
+        uint16_t* e = t.terms.data() + size_t(j) * kMtDegree;
+        for (int b = 0; b < kMtDegree; ++b)
+            if (ladder[size_t(j)][size_t(b) >> 6] >> (b & 63) & 1u) e[t.count[size_t(j)]++] = uint16_t(b);
+    }
+    return cache.emplace(std::make_pair(quantum, levels), std::move(t)).first->second;
+}
+
 } // namespace sepso

@@ -17,4 +17,12 @@ std::vector<uint64_t> mt_jump_poly(uint64_t steps);
 // x^(quantum * 2^j) mod phi for j = 0 .. levels-1 (cached per process)
 const std::vector<std::vector<uint64_t>>& mt_jump_ladder(uint64_t quantum, int levels);
 
+// the same ladder as exponent lists: level j's ascending exponents at
+// terms[j * kMtDegree ..], count[j] of them (cached per process)
+struct MtJumpTerms {
+    std::vector<uint16_t> terms;
+    std::vector<int> count;
+};
+const MtJumpTerms& mt_jump_ladder_terms(uint64_t quantum, int levels);
+
 } // namespace sepso

@@ -76,47 +76,47 @@ __global__ void k_mt_seed_state(unsigned long long* st, unsigned long long seed)
     if (threadIdx.x == 0) mt_seed_words(st, seed);
 }
 
-// s_dst = XOR over g's terms i in this CTA's chunk of the window x[i .. i+311]
+// s_dst = XOR over g's terms i in this CTA's share of the window x[i .. i+311]
 // of s_src (split CTAs per jump); dst is zeroed by the host and combined with
-// atomicXor.
+// atomicXor.  g arrives as the sorted list of its exponents (idx, nidx terms):
+// the bit walk is the same for every lane, so it is done once on the host, and
+// a term costs a lane one shared-memory load and one 64-bit XOR.
+constexpr int kJumpTermsPerCta = 2560;      // >= ceil(kMtDegree / 8): split >= 8
 __global__ void __launch_bounds__(1024) k_mt_jump(unsigned long long* states, int n_src, int split,
-                                                  const unsigned long long* poly) {
+                                                  const unsigned short* __restrict__ idx, int nidx) {
     extern __shared__ __align__(16) unsigned long long jsm[];
     unsigned long long* buf = jsm;                      // generator (4 x 312)
-    unsigned long long* P = jsm + kMtStateWords;        // g, 312 words
-    unsigned long long* X = P + 312;                    // x[0 .. i1 + 311]
+    unsigned long long* X = jsm + kMtStateWords;        // x[0 .. i1 + 311]
+    unsigned short* I = reinterpret_cast<unsigned short*>(X + kMtDegree + 312);   // this CTA's terms
     const int tid = threadIdx.x, nthr = blockDim.x;
-    const int m = blockIdx.x / split, part = blockIdx.x % split, chunk = (kMtDegree + split - 1) / split;
-    const int i0 = part * chunk, i1 = min(kMtDegree, i0 + chunk);
+    const int m = blockIdx.x / split, part = blockIdx.x % split, chunk = (nidx + split - 1) / split;
+    const int j0 = min(nidx, part * chunk), j1 = min(nidx, j0 + chunk), n = j1 - j0;
     const unsigned long long* src = states + size_t(m) * 312;
     unsigned long long* dst = states + size_t(m + n_src) * 312;
     for (int k = tid; k < 312; k += nthr) {
         const unsigned long long w = src[k];
         buf[312 + k] = w;
         X[k] = w;
-        P[k] = poly[k];
     }
+    for (int j = tid; j < n; j += nthr) I[j] = idx[j0 + j];
+    const int i1 = n > 0 ? int(idx[j1 - 1]) + 1 : 0;    // words x[312 ..] this share reads
     __syncthreads();
     MtState s{buf, 0, 0};
     mt_generate<0, true>(s, MtGroup{tid, nthr, 0}, 0, i1,
                          [&](int rel, unsigned long long word) { X[312 + rel] = word; });
     __syncthreads();
-    unsigned long long acc = 0;
     const int k = tid % 312, sub = tid / 312;
     if (sub < 3) {
-        const int c3 = (i1 - i0 + 2) / 3, a = i0 + sub * c3, b = min(i1, a + c3);
-        for (int q = a >> 6; a < b && q <= (b - 1) >> 6; ++q) {
-            unsigned long long bits = P[q];
-            const int lo = q * 64;
-            if (a > lo) bits &= ~0ull << (a - lo);
-            if (b < lo + 64) bits &= (1ull << (b - lo)) - 1ull;
-            while (bits) {
-                const int bb = __ffsll((long long)bits) - 1;
-                bits &= bits - 1;
-                acc ^= X[lo + bb + k];
-            }
+        const int c3 = (n + 2) / 3, a = min(n, sub * c3), b = min(n, a + c3);
+        unsigned long long a0 = 0, a1 = 0;
+        int j = a;
+#pragma unroll 4
+        for (; j + 1 < b; j += 2) {
+            a0 ^= X[I[j] + k];
+            a1 ^= X[I[j + 1] + k];
         }
-        buf[tid] = acc;                                 // generator buffer is free now
+        if (j < b) a0 ^= X[I[j] + k];
+        buf[tid] = a0 ^ a1;                             // generator buffer is free now
     }
     __syncthreads();
     if (tid < 312) atomicXor(dst + tid, buf[tid] ^ buf[312 + tid] ^ buf[624 + tid]);
@@ -141,11 +141,11 @@ __global__ void __launch_bounds__(256) k_mt_fill_seg(const unsigned long long* s
     }
 }
 
-size_t mt_jump_smem_bytes() { return size_t(kMtStateWords + 312 + 312 + kMtDegree) * 8; }
+size_t mt_jump_smem_bytes() { return size_t(kMtStateWords + 312 + kMtDegree) * 8 + kJumpTermsPerCta * 2; }
 
 int stage_mt_fill_parallel(MtPersist* g, unsigned long long seed, long long upto, unsigned long long* out,
-                           unsigned long long* states, const unsigned long long* polys, int levels, long long Q,
-                           void* stream) {
+                           unsigned long long* states, const unsigned short* terms, const int* nterms, int levels,
+                           long long Q, void* stream) {
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     static thread_local unsigned attr = 0;          // function attributes are per device: one bit each
     int dev = 0;
@@ -162,7 +162,8 @@ int stage_mt_fill_parallel(MtPersist* g, unsigned long long seed, long long upto
         cudaError_t e = cudaMemsetAsync(states + size_t(n) * 312, 0, size_t(n) * 312 * 8, st);
         if (e != cudaSuccess) return int(e);
         const int split = std::max(8, std::min(32, 256 / n));      // fill the GPU at the narrow levels
-        k_mt_jump<<<n * split, 1024, mt_jump_smem_bytes(), st>>>(states, n, split, polys + size_t(j) * 312);
+        k_mt_jump<<<n * split, 1024, mt_jump_smem_bytes(), st>>>(states, n, split, terms + size_t(j) * kMtDegree,
+                                                                 nterms[j]);
     }
     k_mt_fill_seg<<<1u << levels, 256, 0, st>>>(states, Q, upto, out, g);
     return int(cudaGetLastError());

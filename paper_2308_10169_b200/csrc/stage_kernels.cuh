@@ -58,11 +58,13 @@ int stage_mt_fill(MtPersist* g, unsigned long long seed, bool reseed, long long 
                   long long upto, unsigned long long* out, void* stream);
 // The same fill of [0, upto) from a fresh seed in 2^levels parallel segments of
 // Q words (Q a multiple of 624, Q * 2^levels >= upto) started from jumped
-// states (mt_jump.cpp); polys = mt_jump_ladder(Q, levels) on the device,
-// states = scratch for 2^levels x 312 words.  Identical words and final g.
+// states (mt_jump.cpp); terms = level j's polynomial mt_jump_ladder(Q, levels)[j]
+// as the sorted list of its nterms[j] (host array) exponents, at terms + j *
+// kMtDegree on the device; states = scratch for 2^levels x 312 words.
+// Identical words and final g.
 int stage_mt_fill_parallel(MtPersist* g, unsigned long long seed, long long upto, unsigned long long* out,
-                           unsigned long long* states, const unsigned long long* polys, int levels, long long Q,
-                           void* stream);
+                           unsigned long long* states, const unsigned short* terms, const int* nterms, int levels,
+                           long long Q, void* stream);
 
 int stage_eval_path(bool fp64, const unsigned char* world, int max_obs, int max_verts,
                     int off_offsets, int off_verts, int D, int rows, const void* x,
