@@ -459,6 +459,7 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
     const size_t o_x = take(size_t(RL) * D * tsz), o_v = take(size_t(RL) * D * tsz);
     const size_t o_pb = take(size_t(RL) * D * tsz);
     const size_t o_fit = take(size_t(RL) * tsz), o_pbf = take(size_t(RL) * tsz);
+    const size_t o_imp = take(size_t(RL));     // rows whose pbest_x copy the step performs
     const size_t o_q = take(size_t(RL) * 4), o_pbq = take(size_t(RL) * 4);
     const size_t o_pf = take(size_t(G) * tsz), o_prow = take(size_t(G) * 4), o_pq = take(size_t(G) * 4);
     const size_t o_gbx = take(size_t(G) * D * tsz), o_gbf = take(size_t(G) * tsz), o_gbq = take(size_t(G) * 4);
@@ -582,11 +583,13 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
         e = stage_pbest_partials(fp64, s, dev + o_x, dev + o_fit, reinterpret_cast<int*>(dev + o_q),
                                  dev + o_pb, dev + o_pbf, reinterpret_cast<int*>(dev + o_pbq), dst,
                                  dev + o_pf, reinterpret_cast<int*>(dev + o_prow),
-                                 reinterpret_cast<int*>(dev + o_pq), dst, st);
+                                 reinterpret_cast<int*>(dev + o_pq), dst, st,
+                                 reinterpret_cast<unsigned char*>(dev + o_imp));
         if (e) return cuda_fail(cudaError_t(e), "stage_pbest");
         e = stage_group_bests(fp64, s, dev + o_pf, reinterpret_cast<int*>(dev + o_prow),
                               reinterpret_cast<int*>(dev + o_pq), dev + o_pb, dev + o_gbx, dev + o_gbf,
-                              reinterpret_cast<int*>(dev + o_gbq), dev + o_cand + cstride * r.rank, dst, st, dst);
+                              reinterpret_cast<int*>(dev + o_gbq), dev + o_cand + cstride * r.rank, dst, st, dst,
+                              dev + o_x, reinterpret_cast<const unsigned char*>(dev + o_imp));
         if (e) return cuda_fail(cudaError_t(e), "stage_group_bests");
         if (nranks > 1 && r.comm) {   // the only cross-GPU traffic: each rank's tbest candidate
             e = comm_allgather(r.comm, dev + o_cand + cstride * r.rank, dev + o_cand, cstride, st);
@@ -610,7 +613,8 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
             if (mt) cudaStreamWaitEvent(st, ctx->ev_fill, 0);
             e = stage_step(fp64, s, reinterpret_cast<double*>(dev + o_hyp), dev + o_lo, dev + o_hi,
                            dev + o_x, dev + o_v, dev + o_pb, dev + o_gbx, dev + o_tbx, r.seed, first,
-                           k, r.cap, dst, st, words, (long long)first);
+                           k, r.cap, dst, st, words, (long long)first,
+                           reinterpret_cast<const unsigned char*>(dev + o_imp));
             if (e) return cuda_fail(cudaError_t(e), "stage_step");
             if (mt) cudaEventRecord(ctx->ev_free, st);
         }

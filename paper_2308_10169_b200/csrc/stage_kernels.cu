@@ -228,20 +228,27 @@ int stage_init(bool fp64, const StageShape& s, const double* hypers, const void*
 // shared memory, then every element is read once and written once:
 // 20 B/element in FP32 (x, v, pbest in; x, v out).  VEC = 4 uses 16-byte
 // vector accesses when D % 4 == 0.
+// imp != nullptr (run_staged): the pbest row copy of this iteration's
+// improved rows (runner.hpp:73-80) was deferred to here -- for a row with
+// imp[row] set, pbest_x IS the current x, so the step takes it from x and
+// writes it to pb (x, v in; x, v, pb out: 20 B/element, and the separate copy
+// kernel's 8 B/element re-read and write are gone).
 constexpr int kStepRows = 32;
 
 template <class T, int VEC>
 __global__ void __launch_bounds__(256) k_step(StageShape s, const double* __restrict__ hypers,
                                               const T* __restrict__ lo, const T* __restrict__ hi,
                                               T* __restrict__ x, T* __restrict__ v,
-                                              const T* __restrict__ pb, const T* __restrict__ gbx,
+                                              T* __restrict__ pb, const T* __restrict__ gbx,
                                               const T* __restrict__ tbx, uint64_t seed,
                                               uint64_t first_draw, int k, int total,
                                               const IterState* gate,
-                                              const unsigned long long* words, long long wbase) {
+                                              const unsigned long long* words, long long wbase,
+                                              const unsigned char* __restrict__ imp) {
     using A = Ar<T>;
     if (gate != nullptr && gate->stop) return;
     __shared__ T coef[3 * kStepRows];
+    __shared__ unsigned char fl[kStepRows];
     __shared__ T hw[64 * 3];   // per group: omega_k, vmax scale (v_limit), spare
     const int R = s.G * s.N, D = s.D;
     const int r0 = blockIdx.x * kStepRows;
@@ -260,6 +267,7 @@ __global__ void __launch_bounds__(256) k_step(StageShape s, const double* __rest
         const T u = unit_from_word<T>(stream_word(seed, first_draw + uint64_t(j) * R + row, words, wbase));
         coef[j * kStepRows + rl] = A::mul(T(hypers[g * 6 + j]), u);
     }
+    for (int t = threadIdx.x; t < nr; t += blockDim.x) fl[t] = imp != nullptr ? imp[r0 + t] : 0;
     __syncthreads();
     const int DV = D / VEC;
     for (int e = threadIdx.x; e < nr * DV; e += blockDim.x) {
@@ -268,11 +276,13 @@ __global__ void __launch_bounds__(256) k_step(StageShape s, const double* __rest
         const T w = hw[(g - g_lo) * 3], vl = hw[(g - g_lo) * 3 + 1];
         const T a1 = coef[rl], a2 = coef[kStepRows + rl], a3 = coef[2 * kStepRows + rl];
         const size_t base = size_t(r0 + rl) * D + size_t(dv) * VEC;
+        const bool im = fl[rl] != 0;
         T xs[VEC], vs[VEC], ps[VEC], gs[VEC], ts[VEC], ls[VEC], hs[VEC];
         if constexpr (VEC == 4 && sizeof(T) == 4) {
             *reinterpret_cast<float4*>(xs) = *reinterpret_cast<const float4*>(x + base);
             *reinterpret_cast<float4*>(vs) = *reinterpret_cast<const float4*>(v + base);
-            *reinterpret_cast<float4*>(ps) = __ldcs(reinterpret_cast<const float4*>(pb + base));
+            if (im) *reinterpret_cast<float4*>(ps) = *reinterpret_cast<const float4*>(xs);
+            else *reinterpret_cast<float4*>(ps) = __ldcs(reinterpret_cast<const float4*>(pb + base));
             *reinterpret_cast<float4*>(gs) = *reinterpret_cast<const float4*>(gbx + size_t(g) * D + dv * 4);
             *reinterpret_cast<float4*>(ts) = *reinterpret_cast<const float4*>(tbx + dv * 4);
             *reinterpret_cast<float4*>(ls) = *reinterpret_cast<const float4*>(lo + dv * 4);
@@ -280,7 +290,7 @@ __global__ void __launch_bounds__(256) k_step(StageShape s, const double* __rest
         } else {
 #pragma unroll
             for (int i = 0; i < VEC; ++i) {
-                xs[i] = x[base + i]; vs[i] = v[base + i]; ps[i] = pb[base + i];
+                xs[i] = x[base + i]; vs[i] = v[base + i]; ps[i] = im ? xs[i] : pb[base + i];
                 gs[i] = gbx[size_t(g) * D + dv * VEC + i]; ts[i] = tbx[dv * VEC + i];
                 ls[i] = lo[dv * VEC + i]; hs[i] = hi[dv * VEC + i];
             }
@@ -299,36 +309,41 @@ __global__ void __launch_bounds__(256) k_step(StageShape s, const double* __rest
         if constexpr (VEC == 4 && sizeof(T) == 4) {
             *reinterpret_cast<float4*>(x + base) = *reinterpret_cast<const float4*>(xs);
             *reinterpret_cast<float4*>(v + base) = *reinterpret_cast<const float4*>(vs);
+            if (im) *reinterpret_cast<float4*>(pb + base) = *reinterpret_cast<const float4*>(ps);
         } else {
 #pragma unroll
-            for (int i = 0; i < VEC; ++i) { x[base + i] = xs[i]; v[base + i] = vs[i]; }
+            for (int i = 0; i < VEC; ++i) {
+                x[base + i] = xs[i];
+                v[base + i] = vs[i];
+                if (im) pb[base + i] = ps[i];
+            }
         }
     }
 }
 
 int stage_step(bool fp64, const StageShape& s, const double* hypers, const void* lo,
-               const void* hi, void* x, void* v, const void* pb, const void* gbx,
+               const void* hi, void* x, void* v, void* pb, const void* gbx,
                const void* tbx, uint64_t seed, uint64_t first_draw, int k, int total,
                const IterState* gate, void* stream, const unsigned long long* words,
-               long long wbase) {
+               long long wbase, const unsigned char* imp) {
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     const unsigned grid = unsigned((s.rows + kStepRows - 1) / kStepRows);
     if (grid == 0) return 0;
     if (fp64)
         k_step<double, 1><<<grid, 256, 0, st>>>(s, hypers, (const double*)lo, (const double*)hi,
-                                                (double*)x, (double*)v, (const double*)pb,
+                                                (double*)x, (double*)v, (double*)pb,
                                                 (const double*)gbx, (const double*)tbx, seed,
-                                                first_draw, k, total, gate, words, wbase);
+                                                first_draw, k, total, gate, words, wbase, imp);
     else if (s.D % 4 == 0)
         k_step<float, 4><<<grid, 256, 0, st>>>(s, hypers, (const float*)lo, (const float*)hi,
-                                               (float*)x, (float*)v, (const float*)pb,
+                                               (float*)x, (float*)v, (float*)pb,
                                                (const float*)gbx, (const float*)tbx, seed,
-                                               first_draw, k, total, gate, words, wbase);
+                                               first_draw, k, total, gate, words, wbase, imp);
     else
         k_step<float, 1><<<grid, 256, 0, st>>>(s, hypers, (const float*)lo, (const float*)hi,
-                                               (float*)x, (float*)v, (const float*)pb,
+                                               (float*)x, (float*)v, (float*)pb,
                                                (const float*)gbx, (const float*)tbx, seed,
-                                               first_draw, k, total, gate, words, wbase);
+                                               first_draw, k, total, gate, words, wbase, imp);
     return int(cudaGetLastError());
 }
 
@@ -735,6 +750,21 @@ __global__ void k_pbest(StageShape s, const T* __restrict__ x, const T* __restri
         for (int d = lane; d < s.D; d += 32) pb[size_t(rl) * s.D + d] = x[size_t(rl) * s.D + d];
 }
 
+// run_staged's pbest (runner.hpp:73-80) with the row copy deferred to the
+// step (k_step, imp): thread per row, strict '<', imp[row] = improved.
+template <class T>
+__global__ void k_pbest_flag(StageShape s, const T* __restrict__ fit, const int* __restrict__ q, T* pbf,
+                             int* pbq, unsigned char* imp, IterState* st, const IterState* gate) {
+    if (gate != nullptr && gate->stop) return;
+    for (int rl = blockIdx.x * blockDim.x + threadIdx.x; rl < s.rows; rl += gridDim.x * blockDim.x) {
+        const T f = fit[rl];
+        if (st != nullptr && !isfinite(f)) atomicMin(&st->nonfinite_row, s.row_begin + rl);
+        const bool better = f < pbf[rl];
+        if (better) { pbf[rl] = f; pbq[rl] = q ? q[rl] : 0; }
+        imp[rl] = better ? 1 : 0;
+    }
+}
+
 // Per local group: (pbest_f, global row) lexicographic min (runner.hpp:81-87 order).
 template <class T>
 __global__ void k_group_partial(StageShape s, const T* __restrict__ pbf, const int* __restrict__ pbq,
@@ -772,18 +802,25 @@ __global__ void k_group_partial(StageShape s, const T* __restrict__ pbf, const i
 int stage_pbest_partials(bool fp64, const StageShape& s, const void* x, const void* fit,
                          const int* q, void* pb, void* pbf, int* pbq, IterState* stt,
                          void* part_f, int* part_row, int* part_q, const IterState* gate,
-                         void* stream) {
+                         void* stream, unsigned char* imp) {
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     const unsigned grid = unsigned((s.rows * 32LL + 255) / 256);
     const int n_groups = (s.row_begin + s.rows - 1) / s.N - s.row_begin / s.N + 1;
-    if (fp64) {
+    if (imp != nullptr) {
+        const unsigned gf = grid_for(s.rows, 256);
+        if (fp64) k_pbest_flag<double><<<gf, 256, 0, st>>>(s, (const double*)fit, q, (double*)pbf, pbq, imp, stt, gate);
+        else k_pbest_flag<float><<<gf, 256, 0, st>>>(s, (const float*)fit, q, (float*)pbf, pbq, imp, stt, gate);
+    } else if (fp64) {
         k_pbest<double><<<grid, 256, 0, st>>>(s, (const double*)x, (const double*)fit, q,
                                               (double*)pb, (double*)pbf, pbq, stt, gate);
-        k_group_partial<double><<<n_groups, 256, 0, st>>>(s, (const double*)pbf, pbq,
-                                                          (double*)part_f, part_row, part_q, gate);
     } else {
         k_pbest<float><<<grid, 256, 0, st>>>(s, (const float*)x, (const float*)fit, q,
                                              (float*)pb, (float*)pbf, pbq, stt, gate);
+    }
+    if (fp64) {
+        k_group_partial<double><<<n_groups, 256, 0, st>>>(s, (const double*)pbf, pbq,
+                                                          (double*)part_f, part_row, part_q, gate);
+    } else {
         k_group_partial<float><<<n_groups, 256, 0, st>>>(s, (const float*)pbf, pbq,
                                                          (float*)part_f, part_row, part_q, gate);
     }
@@ -795,7 +832,8 @@ template <class T>
 __global__ void k_group_bests(StageShape s, const T* __restrict__ part_f,
                               const int* __restrict__ part_row, const int* __restrict__ part_q,
                               const T* __restrict__ pb, T* gbx, T* gbf, int* gbq,
-                              unsigned char* cand, const IterState* gate, const IterState* st) {
+                              unsigned char* cand, const IterState* gate, const IterState* st,
+                              const T* __restrict__ x, const unsigned char* __restrict__ imp) {
     if (gate != nullptr && gate->stop) return;
     extern __shared__ int chg[];
     const int g0 = s.row_begin / s.N;
@@ -813,7 +851,10 @@ __global__ void k_group_bests(StageShape s, const T* __restrict__ part_f,
     __syncthreads();
     for (int t = threadIdx.x; t < ng * s.D; t += blockDim.x) {
         const int lg = t / s.D, d = t - lg * s.D;
-        if (chg[lg] >= 0) gbx[size_t(g0 + lg) * s.D + d] = pb[size_t(chg[lg]) * s.D + d];
+        if (chg[lg] >= 0) {     // a row improved this iteration: its pbest_x is still in x (k_step, imp)
+            const T* src = imp != nullptr && imp[chg[lg]] ? x : pb;
+            gbx[size_t(g0 + lg) * s.D + d] = src[size_t(chg[lg]) * s.D + d];
+        }
     }
     __shared__ int best_g;
     if (threadIdx.x == 0) {
@@ -833,18 +874,19 @@ __global__ void k_group_bests(StageShape s, const T* __restrict__ part_f,
 
 int stage_group_bests(bool fp64, const StageShape& s, const void* part_f, const int* part_row,
                       const int* part_q, const void* pb, void* gbx, void* gbf, int* gbq,
-                      void* cand, const IterState* gate, void* stream, const IterState* stt) {
+                      void* cand, const IterState* gate, void* stream, const IterState* stt,
+                      const void* x, const unsigned char* imp) {
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int ng = (s.row_begin + s.rows - 1) / s.N - s.row_begin / s.N + 1;
     const size_t sm = size_t(ng) * 4;
     if (fp64)
         k_group_bests<double><<<1, 256, sm, st>>>(s, (const double*)part_f, part_row, part_q,
                                                   (const double*)pb, (double*)gbx, (double*)gbf,
-                                                  gbq, (unsigned char*)cand, gate, stt);
+                                                  gbq, (unsigned char*)cand, gate, stt, (const double*)x, imp);
     else
         k_group_bests<float><<<1, 256, sm, st>>>(s, (const float*)part_f, part_row, part_q,
                                                  (const float*)pb, (float*)gbx, (float*)gbf, gbq,
-                                                 (unsigned char*)cand, gate, stt);
+                                                 (unsigned char*)cand, gate, stt, (const float*)x, imp);
     return int(cudaGetLastError());
 }
 

@@ -40,11 +40,14 @@ int stage_init(bool fp64, const StageShape& s, const double* hypers, const void*
                double pi_radius, void* x, void* v, void* pbest_x, void* stream,
                const unsigned long long* words = nullptr, long long wbase = 0);
 
+// imp != nullptr: rows with imp[row] set improved their pbest this iteration
+// and their pbest_x copy was deferred (stage_pbest_partials with imp): the
+// step reads pbest_x from x and writes it to pbest_x.
 int stage_step(bool fp64, const StageShape& s, const double* hypers, const void* lo,
-               const void* hi, void* x, void* v, const void* pbest_x, const void* gbest_x,
+               const void* hi, void* x, void* v, void* pbest_x, const void* gbest_x,
                const void* tbest_x, uint64_t seed, uint64_t first_draw, int k, int total,
                const IterState* gate, void* stream, const unsigned long long* words = nullptr,
-               long long wbase = 0);
+               long long wbase = 0, const unsigned char* imp = nullptr);
 
 // Persisted mt19937_64 generator for the staged path (device memory).
 struct MtPersist {
@@ -75,17 +78,20 @@ int stage_eval_bench(bool fp64, int kind, int D, int rows, const void* x, void* 
                      int* q, const IterState* gate, void* stream);
 
 // pbest update + per-group partial (value, global row, q) for the local groups.
+// imp != nullptr: improved rows are flagged in imp instead of copying x into
+// pbest_x (the copy happens in the next stage_step / stage_group_bests with imp).
 int stage_pbest_partials(bool fp64, const StageShape& s, const void* x, const void* fit,
                          const int* q, void* pbest_x, void* pbest_f, int* pbest_q,
                          IterState* st, void* part_f, int* part_row, int* part_q,
-                         const IterState* gate, void* stream);
+                         const IterState* gate, void* stream, unsigned char* imp = nullptr);
 
 // gbest (local groups) from the partials; writes this device's tbest
 // candidate: best local group (value, q, global group) + its x.
 int stage_group_bests(bool fp64, const StageShape& s, const void* part_f, const int* part_row,
                       const int* part_q, const void* pbest_x, void* gbest_x, void* gbest_f,
                       int* gbest_q, void* cand /*packed candidate*/, const IterState* gate,
-                      void* stream, const IterState* st = nullptr);
+                      void* stream, const IterState* st = nullptr, const void* x = nullptr,
+                      const unsigned char* imp = nullptr);
 
 // Scan n_cand candidates (ascending group order) for tbest, push the window,
 // evaluate AT; trace[k-1] = tbest_f.  cand layout: see big_swarm.cu.
