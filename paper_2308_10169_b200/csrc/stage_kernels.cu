@@ -776,7 +776,19 @@ __global__ void k_group_partial(StageShape s, const T* __restrict__ pbf, const i
     const int l1 = min((g + 1) * s.N, s.row_begin + s.rows) - s.row_begin;
     T bf = A::inf();
     int br = INT_MAX;
-    for (int r = l0 + threadIdx.x; r < l1; r += blockDim.x) {
+    // eight loads in flight per thread (the scan is latency-bound: one CTA per
+    // group), then the compares in row order
+    int r = l0 + threadIdx.x;
+    const int step = blockDim.x;
+    for (; r + 7 * step < l1; r += 8 * step) {
+        T f8[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) f8[i] = pbf[r + i * step];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (f8[i] < bf) { bf = f8[i]; br = r + i * step; }
+    }
+    for (; r < l1; r += step) {
         const T f = pbf[r];
         if (f < bf) { bf = f; br = r; }
     }
@@ -827,15 +839,17 @@ int stage_pbest_partials(bool fp64, const StageShape& s, const void* x, const vo
     return int(cudaGetLastError());
 }
 
-// gbest for the local groups, then this device's tbest candidate.
+// gbest for the local groups, then this device's tbest candidate
+// (runner.hpp:81-91).  One CTA takes the decisions -- a group's gbest changes
+// on a strict '<', and the header of the candidate -- and leaves the changed
+// group's row in part_row (-1: unchanged); a wide grid then copies the changed
+// rows into gbest_x and the candidate's x (one CTA copying every row was
+// load-latency bound).
 template <class T>
-__global__ void k_group_bests(StageShape s, const T* __restrict__ part_f,
-                              const int* __restrict__ part_row, const int* __restrict__ part_q,
-                              const T* __restrict__ pb, T* gbx, T* gbf, int* gbq,
-                              unsigned char* cand, const IterState* gate, const IterState* st,
-                              const T* __restrict__ x, const unsigned char* __restrict__ imp) {
+__global__ void k_group_bests(StageShape s, const T* __restrict__ part_f, int* __restrict__ part_row,
+                              const int* __restrict__ part_q, T* gbf, int* gbq, unsigned char* cand,
+                              const IterState* gate, const IterState* st) {
     if (gate != nullptr && gate->stop) return;
-    extern __shared__ int chg[];
     const int g0 = s.row_begin / s.N;
     const int ng = (s.row_begin + s.rows - 1) / s.N - g0 + 1;
     for (int lg = threadIdx.x; lg < ng; lg += blockDim.x) {
@@ -843,20 +857,11 @@ __global__ void k_group_bests(StageShape s, const T* __restrict__ part_f,
         if (part_row[lg] >= 0 && part_f[lg] < gbf[g]) {
             gbf[g] = part_f[lg];
             gbq[g] = part_q[lg];
-            chg[lg] = part_row[lg];
         } else {
-            chg[lg] = -1;
+            part_row[lg] = -1;
         }
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < ng * s.D; t += blockDim.x) {
-        const int lg = t / s.D, d = t - lg * s.D;
-        if (chg[lg] >= 0) {     // a row improved this iteration: its pbest_x is still in x (k_step, imp)
-            const T* src = imp != nullptr && imp[chg[lg]] ? x : pb;
-            gbx[size_t(g0 + lg) * s.D + d] = src[size_t(chg[lg]) * s.D + d];
-        }
-    }
-    __shared__ int best_g;
     if (threadIdx.x == 0) {
         CandHdr h{__longlong_as_double(0x7ff0000000000000ll), 0, -1, st ? st->nonfinite_row : INT_MAX, 0};
         for (int lg = 0; lg < ng; ++lg) {
@@ -864,12 +869,37 @@ __global__ void k_group_bests(StageShape s, const T* __restrict__ part_f,
             if (f < h.f) { h.f = f; h.q = gbq[g0 + lg]; h.g = g0 + lg; }
         }
         *reinterpret_cast<CandHdr*>(cand) = h;
-        best_g = h.g;
     }
-    __syncthreads();
+}
+
+// element t of the copies: t < ng*D: gbest_x of local group t / D (if it
+// changed); then the candidate's x.  A changed group's row is read from x
+// when it improved this iteration (its pbest_x copy is deferred to k_step).
+template <class T>
+__global__ void k_group_rows(StageShape s, const int* __restrict__ part_row, const T* __restrict__ pb,
+                             T* gbx, unsigned char* cand, const IterState* gate, const T* __restrict__ x,
+                             const unsigned char* __restrict__ imp) {
+    if (gate != nullptr && gate->stop) return;
+    const int g0 = s.row_begin / s.N;
+    const int ng = (s.row_begin + s.rows - 1) / s.N - g0 + 1;
+    const int D = s.D;
+    const int bg = reinterpret_cast<const CandHdr*>(cand)->g;
     T* cx = reinterpret_cast<T*>(cand + sizeof(CandHdr));
-    if (best_g >= 0)
-        for (int d = threadIdx.x; d < s.D; d += blockDim.x) cx[d] = gbx[size_t(best_g) * s.D + d];
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)(ng + 1) * D;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int lg = int(t / D), d = int(t - (long long)lg * D);
+        if (lg < ng) {
+            const int row = part_row[lg];
+            if (row >= 0) {
+                const T* src = imp != nullptr && imp[row] ? x : pb;
+                gbx[size_t(g0 + lg) * D + d] = src[size_t(row) * D + d];
+            }
+        } else if (bg >= 0) {         // the candidate: the best group's (new or kept) gbest_x
+            const int row = part_row[bg - g0];
+            const T* src = row < 0 ? gbx + size_t(bg) * D : (imp != nullptr && imp[row] ? x : pb) + size_t(row) * D;
+            cx[d] = src[d];
+        }
+    }
 }
 
 int stage_group_bests(bool fp64, const StageShape& s, const void* part_f, const int* part_row,
@@ -878,15 +908,19 @@ int stage_group_bests(bool fp64, const StageShape& s, const void* part_f, const 
                       const void* x, const unsigned char* imp) {
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int ng = (s.row_begin + s.rows - 1) / s.N - s.row_begin / s.N + 1;
-    const size_t sm = size_t(ng) * 4;
-    if (fp64)
-        k_group_bests<double><<<1, 256, sm, st>>>(s, (const double*)part_f, part_row, part_q,
-                                                  (const double*)pb, (double*)gbx, (double*)gbf,
-                                                  gbq, (unsigned char*)cand, gate, stt, (const double*)x, imp);
-    else
-        k_group_bests<float><<<1, 256, sm, st>>>(s, (const float*)part_f, part_row, part_q,
-                                                 (const float*)pb, (float*)gbx, (float*)gbf, gbq,
-                                                 (unsigned char*)cand, gate, stt, (const float*)x, imp);
+    int* prow = const_cast<int*>(part_row);      // consumed here: unchanged groups marked -1
+    const unsigned grid = grid_for((long long)(ng + 1) * s.D, 256);
+    if (fp64) {
+        k_group_bests<double><<<1, 256, 0, st>>>(s, (const double*)part_f, prow, part_q, (double*)gbf, gbq,
+                                                 (unsigned char*)cand, gate, stt);
+        k_group_rows<double><<<grid, 256, 0, st>>>(s, prow, (const double*)pb, (double*)gbx, (unsigned char*)cand,
+                                                   gate, (const double*)x, imp);
+    } else {
+        k_group_bests<float><<<1, 256, 0, st>>>(s, (const float*)part_f, prow, part_q, (float*)gbf, gbq,
+                                                (unsigned char*)cand, gate, stt);
+        k_group_rows<float><<<grid, 256, 0, st>>>(s, prow, (const float*)pb, (float*)gbx, (unsigned char*)cand,
+                                                  gate, (const float*)x, imp);
+    }
     return int(cudaGetLastError());
 }
 
