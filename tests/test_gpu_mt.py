@@ -129,3 +129,22 @@ def test_parallel_stream_fill_equals_sequential(eng64mt, per_group):
     b = eng64mt.plan_frame_sharded(w, None, EVOLVED_PATH_HYPERS, cfg, 99)
     assert a.iterations == b.iterations == 4
     assert a.fitness == b.fitness and np.array_equal(a.best_path, b.best_path)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_wide_parallel_fill_and_staged_bests_equal_sequential(prec, eng32mt, eng64mt):
+    """A staged benchmark swarm whose init fill takes 128 jumped segments (2^27
+    words: seven jump levels, exponent-list jumps): trace and final point
+    equal the same run with the sequential fill.  (The staged bookkeeping --
+    pbest copies deferred to the step -- is pinned against the reference by
+    test_gpu_workloads' scale-harness test.)"""
+    eng = eng32mt if prec == "fp32" else eng64mt
+    G, N, D, T = 8, 8192, 1024, 3                 # 2 * 65,536 * 1,024 = 2^27 init words
+    os.environ["SEPSO_SEQ_FILL"] = "1"
+    try:
+        a = eng.run_dtpso("BF1", pe.DEFAULT_GROUP_HYPERS, G, N, T, 21, dim=D)
+    finally:
+        del os.environ["SEPSO_SEQ_FILL"]
+    b = eng.run_dtpso("BF1", pe.DEFAULT_GROUP_HYPERS, G, N, T, 21, dim=D)
+    assert np.array_equal(a["trace"], b["trace"]) and np.array_equal(a["final_point"], b["final_point"])
+    assert np.all(np.diff(b["trace"]) <= 0)       # tbest never worsens

@@ -261,7 +261,7 @@ def test_fp32_record_is_the_reference_evaluation_of_its_path(eng32mt):
 
 
 # --------------------------------------- the `scale` harness (8(f) 4)
-@pytest.mark.parametrize("shape", [(8, 64, 32, 12), (8, 2048, 64, 4)])
+@pytest.mark.parametrize("shape", [(8, 64, 32, 12), (8, 2048, 64, 4), (8, 4096, 32, 10)])
 def test_engine_equals_per_particle_oracle(shape, eng64mt):
     """proj/tools/swarmforge.cpp:202-255 compares the batched run_dtpso with the
     per-particle run_dppso_reference (runner.hpp:135-239); the FP64 engine --
