@@ -673,7 +673,6 @@ def bench_scale(a, eng, pe):
     run_dppso_reference (runner.hpp:135-239), each timed for T=1 on this host
     and extrapolated to T=10 (declared)."""
     import ctypes as C
-    from oracle_lib import ptr
     G, N, D, T = 8, 16384, 1000, 10
     eng.run_dtpso("BF1", pe.DEFAULT_GROUP_HYPERS, G, N, 2, 1, dim=D)         # warm-up (arena)
     t0 = time.perf_counter()
@@ -683,6 +682,7 @@ def bench_scale(a, eng, pe):
          "gpu_seconds": gpu_s, "evals_per_s": G * N * T / gpu_s}
     r = _ref()
     if r is not None and not a.no_cpu_baseline:
+        from oracle_lib import ptr            # CPU baseline only: the reference's ctypes helpers
         h = np.ascontiguousarray(pe.DEFAULT_GROUP_HYPERS)
         bad = (C.c_size_t * 3)()
 
