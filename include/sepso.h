@@ -242,10 +242,11 @@ int sf_run_scenario(sf_ctx* ctx, const sf_scenario_config* cfg, int variant, uin
 /* ---- device-resident scenarios (run_scenario frame loop on the device) --- */
 /* n independent scenarios (simenv.hpp:239-276) kept in HBM: worlds are made by
  * generate_world(cfgs[s], derive_seed(cfgs[s].root_seed, "world")) once; each
- * frame is ONE fused planning launch (seed derive_seed(root, "plan", f) derived
- * on the device, prev best and carried window chained in HBM) followed by one
- * on-device step_world launch.  `cfg` is the final planner config (variant
- * already applied).  Up to max_frames frames may be run in total. */
+ * frame is ONE fused launch (seed derive_seed(root, "plan", f) derived on the
+ * device, prev best and carried window chained in HBM; after planning, the
+ * cluster advances the world record for the next frame, step_world on the
+ * device).  `cfg` is the final planner config (variant already applied).  Up
+ * to max_frames frames may be run in total. */
 typedef struct sf_scene_batch sf_scene_batch;
 int sf_scene_batch_create(sf_ctx* ctx, uint32_t n, const sf_scenario_config* cfgs,
                           const sf_planner_config* cfg, const double* hypers, uint32_t max_frames,
