@@ -730,8 +730,10 @@ int sf_ctx_destroy(sf_ctx* ctx) {
     if (ctx->side) {
         cudaStreamSynchronize(ctx->side);
         cudaStreamDestroy(ctx->side);
-        cudaEventDestroy(ctx->ev_free);
-        cudaEventDestroy(ctx->ev_fill);
+        for (int b = 0; b < 2; ++b) {
+            if (ctx->ev_free[b]) cudaEventDestroy(ctx->ev_free[b]);
+            if (ctx->ev_fill[b]) cudaEventDestroy(ctx->ev_fill[b]);
+        }
     }
     ctx->io.release();
     ctx->scratch.release();

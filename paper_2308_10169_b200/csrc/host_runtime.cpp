@@ -471,8 +471,9 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
     const size_t o_trace = take(size_t(r.cap) * 8);
     const bool mt = ctx->rng == SF_RNG_MT19937;
     const size_t o_mt = take(mt ? sizeof(MtPersist) : 0);
-    // init window (2RD words); each step's 3R draws reuse it, so it holds the larger of the two
-    const size_t o_words = take(mt ? std::max(size_t(2) * R * D, size_t(3) * R) * 8 : 0);
+    // init window (2RD words); the steps' 3R draws reuse it as two alternating
+    // windows, so it holds the larger of 2RD and 6R
+    const size_t o_words = take(mt ? std::max(size_t(2) * R * D, size_t(6) * R) * 8 : 0);
     // long init windows are generated in parallel segments from jumped states
     const long long init_words = 2ll * R * D;
     int jlevels = 0;
@@ -552,25 +553,33 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
                        dev + o_x, dev + o_v, dev + o_pb, st, words, 0);
     if (e) return cuda_fail(cudaError_t(e), "stage_init");
     // mt19937: step k's 3R draws are generated on a side stream while the
-    // fitness and best kernels of iteration k run (the generator is one CTA
-    // and sequential); the word window is free again once the previous step
-    // (or the initialisation) has read it
+    // fitness and best kernels run (the generator is one CTA and sequential),
+    // into window k & 1: window b is free again once step k - 2 (or the
+    // initialisation) has read it, so the generator runs up to a step ahead
+    // and its ~0.2 ms per step at 393 k draws (scale harness) never holds a
+    // step up
     if (mt && !ctx->side) {
         ce = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
-        if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&ctx->ev_free, cudaEventDisableTiming);
-        if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&ctx->ev_fill, cudaEventDisableTiming);
+        for (int b = 0; b < 2 && ce == cudaSuccess; ++b) {
+            ce = cudaEventCreateWithFlags(&ctx->ev_free[b], cudaEventDisableTiming);
+            if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&ctx->ev_fill[b], cudaEventDisableTiming);
+        }
         if (ce != cudaSuccess) return cuda_fail(ce, "side stream");
     }
-    if (mt) cudaEventRecord(ctx->ev_free, st);
+    if (mt) {
+        cudaEventRecord(ctx->ev_free[0], st);
+        cudaEventRecord(ctx->ev_free[1], st);
+    }
     const WorldLayout& wl = wp.lay;
     for (int k = 1; k <= r.cap; ++k) {
         if (mt && k < r.cap) {   // draws of step k (the generator persists across iterations)
             const uint64_t first = 2ull * uint64_t(R) * D + uint64_t(k - 1) * 3ull * R;
-            cudaStreamWaitEvent(ctx->side, ctx->ev_free, 0);
-            const int fe = stage_mt_fill(mtg, r.seed, false, (long long)first, (long long)first + 3ll * R, words,
-                                         ctx->side);
+            const int b = k & 1;
+            cudaStreamWaitEvent(ctx->side, ctx->ev_free[b], 0);
+            const int fe = stage_mt_fill(mtg, r.seed, false, (long long)first, (long long)first + 3ll * R,
+                                         words + size_t(b) * 3 * R, ctx->side);
             if (fe) return cuda_fail(cudaError_t(fe), "stage_mt_fill");
-            cudaEventRecord(ctx->ev_fill, ctx->side);
+            cudaEventRecord(ctx->ev_fill[b], ctx->side);
         }
         if (path)
             e = stage_eval_path(fp64, dev + o_world, wl.max_obs, wl.max_verts, int(wl.off_offsets),
@@ -610,13 +619,14 @@ int run_staged(sf_ctx* ctx, StagedRun& r) {
         if (e) return cuda_fail(cudaError_t(e), "stage_finish");
         if (k < r.cap) {
             const uint64_t first = 2ull * uint64_t(R) * D + uint64_t(k - 1) * 3ull * R;
-            if (mt) cudaStreamWaitEvent(st, ctx->ev_fill, 0);
+            const int b = k & 1;
+            if (mt) cudaStreamWaitEvent(st, ctx->ev_fill[b], 0);
             e = stage_step(fp64, s, reinterpret_cast<double*>(dev + o_hyp), dev + o_lo, dev + o_hi,
                            dev + o_x, dev + o_v, dev + o_pb, dev + o_gbx, dev + o_tbx, r.seed, first,
-                           k, r.cap, dst, st, words, (long long)first,
+                           k, r.cap, dst, st, mt ? words + size_t(b) * 3 * R : nullptr, (long long)first,
                            reinterpret_cast<const unsigned char*>(dev + o_imp));
             if (e) return cuda_fail(cudaError_t(e), "stage_step");
-            if (mt) cudaEventRecord(ctx->ev_free, st);
+            if (mt) cudaEventRecord(ctx->ev_free[b], st);
         }
     }
     if (ctx->timing) {

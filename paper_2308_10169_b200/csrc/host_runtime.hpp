@@ -62,7 +62,7 @@ struct sf_ctx {
     int rng = SF_RNG_MT19937;
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;         // staged path: the next step's draws are generated here, overlapping the fitness
-    cudaEvent_t ev_free = nullptr, ev_fill = nullptr;
+    cudaEvent_t ev_free[2] = {nullptr, nullptr}, ev_fill[2] = {nullptr, nullptr};   // per step-draw window
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool timing = false;
     double kernel_ms = 0.0;
