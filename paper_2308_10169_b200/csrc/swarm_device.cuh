@@ -66,6 +66,18 @@ __device__ __forceinline__ double penalty(double alpha, double beta, int beta_in
 // and bench_fin<K> closes the row.  The fused kernel walks a row in place
 // (bench_row); the staged evaluation streams rows through shared-memory tiles
 // (k_eval_bench, stage_kernels.cu).  Both run this same arithmetic.
+// Rastrigin's term of one element, x^2 - 10 cos(2 pi x) + 10 (benchmarks.hpp:56-88)
+template <class T> __device__ __forceinline__ T rastrigin_term(T x);
+template <> __device__ __forceinline__ double rastrigin_term<double>(double x) {
+    using A = Ar<double>;
+    const double two_pi = 6.283185307179586;   // 2.0 * std::numbers::pi
+    return A::add(A::sub(A::mul(x, x), A::mul(10.0, cos_glibc(A::mul(two_pi, x)))), 10.0);
+}
+template <> __device__ __forceinline__ float rastrigin_term<float>(float x) {
+    const float two_pi = 6.2831853f;
+    return x * x - 10.f * cosf(two_pi * x) + 10.f;
+}
+
 template <int K, class T>
 __device__ __forceinline__ void bench_elem(int i, T x, T xp, T& s, T& t) {
     if constexpr (sizeof(T) == 8) {
@@ -80,7 +92,7 @@ __device__ __forceinline__ void bench_elem(int i, T x, T xp, T& s, T& t) {
                 s = A::add(s, A::add(A::mul(A::mul(100.0, a), a), A::mul(b, b)));
             }
         } else if constexpr (K == kRastrigin) {
-            s = A::add(s, A::add(A::sub(A::mul(x, x), A::mul(10.0, cos_glibc(A::mul(two_pi, x)))), 10.0));
+            s = A::add(s, rastrigin_term<double>(x));
         } else if constexpr (K == kGriewank) {
             s = A::add(s, A::mul(x, x));
             t = A::mul(t, cos_glibc(__ddiv_rn(x, __dsqrt_rn(double(i + 1)))));
@@ -99,7 +111,7 @@ __device__ __forceinline__ void bench_elem(int i, T x, T xp, T& s, T& t) {
                 s += 100.f * a * a + b * b;
             }
         } else if constexpr (K == kRastrigin) {
-            s += x * x - 10.f * cosf(two_pi * x) + 10.f;
+            s += rastrigin_term<float>(x);
         } else if constexpr (K == kGriewank) {
             s += x * x;
             t *= cosf(x * rsqrtf(float(i + 1)));
@@ -648,6 +660,23 @@ __device__ void path_fitness_phase(const SwarmParams& p, Ctx<T>& c, long long* p
 
 template <class T>
 __device__ void bench_fitness_phase(int kind, Ctx<T>& c) {
+    if (kind == kRastrigin) {
+        // the cosines of all P x D elements on every thread (one row per
+        // thread would leave most of the CTA idle behind D sequential cos
+        // calls), then each row's terms summed in index order by one thread:
+        // the same terms and additions as bench_row<kRastrigin>
+        const int PD = c.P * c.D;
+        for (int e = threadIdx.x; e < PD; e += blockDim.x) c.seglen[e] = rastrigin_term<T>(c.x[e]);
+        __syncthreads();
+        for (int pl = threadIdx.x; pl < c.P; pl += blockDim.x) {
+            const T* t = c.seglen + pl * c.D;
+            T s = T(0);
+            for (int i = 0; i < c.D; ++i) s = Ar<T>::add(s, t[i]);
+            c.fit[pl] = s;
+            c.q[pl] = 0;
+        }
+        return;
+    }
     for (int pl = threadIdx.x; pl < c.P; pl += blockDim.x) {
         c.fit[pl] = bench_eval<T>(kind, c.x + pl * c.D, c.D);
         c.q[pl] = 0;

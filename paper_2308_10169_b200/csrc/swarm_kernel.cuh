@@ -205,7 +205,7 @@ SEPSO_LHD SmemLayout smem_layout(const SwarmParams& p, size_t tsz, bool path) {
     L.q = take(P * 4);
     L.fit = take(P * tsz);
     L.imp = take(P * 4);
-    L.seglen = take(path ? P * S * tsz : 0);
+    L.seglen = take((path ? P * S : P * D) * tsz);   // path: segment lengths; benchmarks: per-element terms
     L.coef = take(3 * P * tsz);
     L.lo = take(D * tsz);
     L.hi = take(D * tsz);
