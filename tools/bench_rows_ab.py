@@ -36,6 +36,10 @@ for prec in ("fp32", "fp64"):
     r = eng.run_dtpso("BF3", pe.DEFAULT_GROUP_HYPERS, 8, 10, 200, 11, dim=30)          # fused
     out[f"{prec}_fused_trace"] = r["trace"]
     out[f"{prec}_fused_fp"] = r["final_point"]
+    for prob in ("BF1", "BF2", "BF4", 5):                                             # fused, every function
+        r = eng.run_dtpso(prob, pe.DEFAULT_GROUP_HYPERS, 8, 10, 150, 13, dim=30)
+        out[f"{prec}_fused_{prob}_trace"] = r["trace"]
+        out[f"{prec}_fused_{prob}_fp"] = r["final_point"]
     eng.run_dtpso("BF1", pe.DEFAULT_GROUP_HYPERS, 8, 16384, 2, 1, dim=1000)
     t0 = time.perf_counter()
     r = eng.run_dtpso("BF1", pe.DEFAULT_GROUP_HYPERS, 8, 16384, 4, 1, dim=1000)       # staged
