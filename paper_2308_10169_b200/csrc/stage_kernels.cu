@@ -175,16 +175,17 @@ template <class T>
 __global__ void k_init(StageShape s, const double* __restrict__ hypers, const T* __restrict__ lo,
                        const T* __restrict__ hi, uint64_t seed, uint64_t first,
                        const double* __restrict__ prev, int warm, double pi_radius, T* x, T* v,
-                       T* pb, const unsigned long long* words, long long wbase, FastDiv fD, FastDiv fN) {
+                       T* pb, const unsigned long long* words, long long wbase, FastDiv fD, FastDiv fN,
+                       bool wide) {
     using A = Ar<T>;
     const long long total = (long long)s.rows * s.D;
     const int R = s.G * s.N;
     const T rad = T(pi_radius);
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x) {
-        // (fast divisions: rows * D < 2^31, checked by stage_init; the 64-bit
-        // division made the kernel issue-bound)
-        const int rl = int(fD.div(uint32_t(e))), d = int(e - (long long)rl * s.D);
+        // (fast 32-bit division while rows * D < 2^31 -- the 64-bit one made
+        // the kernel issue-bound; `wide` arrays beyond that take the 64-bit one)
+        const int rl = wide ? int(e / s.D) : int(fD.div(uint32_t(e))), d = int(e - (long long)rl * s.D);
         const int row = s.row_begin + rl, g = int(fN.div(uint32_t(row))), n = row - g * s.N;
         const uint64_t ix = first + uint64_t(row) * uint64_t(s.D) + uint64_t(d);
         const T ux = unit_from_word<T>(stream_word(seed, ix, words, wbase));
@@ -212,8 +213,7 @@ int stage_init(bool fp64, const StageShape& s, const double* hypers, const void*
                double pi_radius, void* x, void* v, void* pb, void* stream,
                const unsigned long long* words, long long wbase) {
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if ((long long)s.rows * s.D >= (1ll << 31) || (long long)s.G * s.N >= (1ll << 31))
-        return int(cudaErrorInvalidValue);                  // FastDiv range (> 8 GB per array)
+    const bool wide = (long long)s.rows * s.D >= (1ll << 31);     // beyond FastDiv's range
     const unsigned grid = grid_for((long long)s.rows * s.D, 256);
     FastDiv fD, fN;
     fD.init(uint32_t(s.D));
@@ -221,11 +221,11 @@ int stage_init(bool fp64, const StageShape& s, const double* hypers, const void*
     if (fp64)
         k_init<double><<<grid, 256, 0, st>>>(s, hypers, (const double*)lo, (const double*)hi, seed,
                                               first, prev, warm, pi_radius, (double*)x, (double*)v,
-                                              (double*)pb, words, wbase, fD, fN);
+                                              (double*)pb, words, wbase, fD, fN, wide);
     else
         k_init<float><<<grid, 256, 0, st>>>(s, hypers, (const float*)lo, (const float*)hi, seed,
                                              first, prev, warm, pi_radius, (float*)x, (float*)v,
-                                             (float*)pb, words, wbase, fD, fN);
+                                             (float*)pb, words, wbase, fD, fN, wide);
     return int(cudaGetLastError());
 }
 
